@@ -1,0 +1,174 @@
+"""Generate tests/golden/*.npz from the compiled reference (oracle/_ref).
+
+Runs ``oracle/_ref/pinnlab_ref_driver`` -- the unmodified reference sources of
+/root/reference/proj/core compiled by oracle/Makefile -- on small cases that
+cover every model feature and residual on the hot path, and stores its float64
+inputs and outputs. Rerun with ``python tests/golden/make_golden.py`` in the
+build container (the GPU box has no /root/reference; the fixtures travel).
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+DRIVER = os.path.join(ROOT, "oracle", "_ref", "pinnlab_ref_driver")
+
+BURGERS = {"pde": {"id": "burgers"}, "domain": [[0, 2], [0, 1]], "initial": "sin_pi_x"}
+MAXWELL = {"pde": {"id": "maxwell_te", "epsilon": 1.0, "mu": 1.0},
+           "domain": [[-1, 1], [-1, 1], [0, 1.5]], "initial": "gauss25"}
+
+CASES = {
+    # C1 family: plain tanh MLP, Dirichlet BC
+    "burgers_tanh": dict(BURGERS, bc="dirichlet_zero",
+                         model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1, "activation": "tanh"},
+                         collocation={"mode": "uniform", "dims": [12, 10], "n_ic": 16, "n_bc": 8},
+                         workers=[1, 2, 3]),
+    # C1 shape at full width (4x64) on a small grid
+    "burgers_c1_shape": dict(BURGERS, bc="dirichlet_zero",
+                             model={"in_dim": 2, "hidden_dim": 64, "depth": 4, "out_dim": 1, "activation": "tanh"},
+                             collocation={"mode": "uniform", "dims": [16, 16], "n_ic": 32, "n_bc": 16},
+                             workers=[1, 4]),
+    # C2 family: RFF + RWF
+    "burgers_rff_rwf": dict(BURGERS, bc="dirichlet_zero",
+                            model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1, "activation": "tanh",
+                                   "rff": {"width": 8, "sigma": 10.0, "mean": 0.0},
+                                   "rwf": {"mean": 1.0, "stddev": 0.1}},
+                            collocation={"mode": "uniform", "dims": [10, 8], "n_ic": 16, "n_bc": 8},
+                            workers=[1, 2]),
+    # C4 family: Maxwell TE, hard BC
+    "maxwell_tanh": dict(MAXWELL, bc="hard",
+                         model={"in_dim": 3, "hidden_dim": 16, "depth": 3, "out_dim": 3, "activation": "tanh"},
+                         collocation={"mode": "uniform", "dims": [5, 5, 4], "n_ic": 16},
+                         workers=[1, 2]),
+    # Maxwell with strict spatial periodicity and a trainable time period + RFF
+    "maxwell_periodic_rff": dict(MAXWELL, bc="hard",
+                                 model={"in_dim": 3, "hidden_dim": 12, "depth": 2, "out_dim": 3, "activation": "tanh",
+                                        "periodic_axes": [{"periodic": True, "period": 2.0, "trainable": False},
+                                                          {"periodic": True, "period": 2.0, "trainable": False},
+                                                          {"periodic": True, "period": 1.5, "trainable": True}],
+                                        "rff": {"width": 6, "sigma": 1.0, "mean": 0.0}},
+                                 collocation={"mode": "uniform", "dims": [4, 4, 3], "n_ic": 9},
+                                 workers=[1]),
+    # second-order stream, sine activation, soft periodic BC
+    "allen_cahn_sine": dict(pde={"id": "allen_cahn"}, domain=[[-1, 1], [0, 1]], initial="sin_pi_x",
+                            bc="soft_periodic",
+                            model={"in_dim": 2, "hidden_dim": 12, "depth": 2, "out_dim": 1, "activation": "sine",
+                                   "sine_w0": 2.0},
+                            collocation={"mode": "uniform", "dims": [8, 6], "n_ic": 10, "n_bc": 6},
+                            workers=[1, 2]),
+    # swish activation, advection, periodic x with trainable period
+    "advection_swish_periodic": dict(pde={"id": "advection", "advection_c": 3.0}, domain=[[0, 6.283185307179586], [0, 1]],
+                                     initial="sin_x", bc="soft_periodic",
+                                     model={"in_dim": 2, "hidden_dim": 10, "depth": 2, "out_dim": 1,
+                                            "activation": "swish",
+                                            "periodic_axes": [{"periodic": True, "period": 6.283185307179586,
+                                                               "trainable": True},
+                                                              {"periodic": False, "period": 0.0, "trainable": False}]},
+                                     collocation={"mode": "uniform", "dims": [7, 5], "n_ic": 8, "n_bc": 5},
+                                     workers=[1]),
+    # Allen-Cahn second order with tanh (tanh second-order jet rule)
+    "allen_cahn_tanh": dict(pde={"id": "allen_cahn"}, domain=[[-1, 1], [0, 1]], initial="sin_pi_x",
+                            bc="dirichlet_zero",
+                            model={"in_dim": 2, "hidden_dim": 16, "depth": 3, "out_dim": 1, "activation": "tanh"},
+                            collocation={"mode": "uniform", "dims": [9, 7], "n_ic": 10, "n_bc": 6},
+                            workers=[1]),
+}
+
+TRAJ = {
+    # N-step Adam trajectory (balancing off), W=2 workers
+    "traj_burgers": dict(BURGERS, bc="dirichlet_zero",
+                         model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1, "activation": "tanh"},
+                         collocation={"mode": "uniform", "dims": [12, 10], "n_ic": 16, "n_bc": 8},
+                         workers=2, train={"epochs": 30, "lr": 1e-2, "gamma": 0.99, "balancing": False}),
+    "traj_maxwell": dict(MAXWELL, bc="hard",
+                         model={"in_dim": 3, "hidden_dim": 16, "depth": 2, "out_dim": 3, "activation": "tanh"},
+                         collocation={"mode": "uniform", "dims": [5, 5, 4], "n_ic": 16},
+                         workers=1, train={"epochs": 20, "lr": 5e-3, "gamma": 1.0, "balancing": False}),
+}
+
+
+def _run(job: dict) -> tuple[dict, str]:
+    d = tempfile.mkdtemp(prefix="golden_")
+    job = dict(job, out=d)
+    with open(os.path.join(d, "job.json"), "w") as f:
+        json.dump(job, f)
+    subprocess.run([DRIVER, os.path.join(d, "job.json")], check=True)
+    with open(os.path.join(d, "meta.json")) as f:
+        return json.load(f), d
+
+
+def _f64(d, name):
+    p = os.path.join(d, name)
+    return np.fromfile(p, dtype="<f8") if os.path.exists(p) else np.zeros(0)
+
+
+def _points(v, d):
+    return v.reshape(d, -1).T.copy() if v.size else np.zeros((0, d))
+
+
+def make_case(name, case):
+    base = {k: v for k, v in case.items() if k not in ("workers",)}
+    dim = len(case["domain"])
+    fields = case["model"]["out_dim"]
+    arrays = {}
+    grads = {}
+    losses = {}
+    for w in case["workers"]:
+        meta, d = _run(dict(base, mode="step", workers=w, dump_residuals=(w == case["workers"][0])))
+        grads[w] = _f64(d, "grad.bin")
+        losses[w] = meta["worker_losses"]
+        if w == case["workers"][0]:
+            arrays.update(
+                params=_f64(d, "params.bin"), rffB=_f64(d, "rff_B.bin"),
+                interior=_points(_f64(d, "interior.bin"), dim),
+                ic_points=_points(_f64(d, "ic_points.bin"), dim),
+                ic_targets=_f64(d, "ic_targets.bin").reshape(fields, -1).T.copy(),
+                bc_a=_points(_f64(d, "bc_a.bin"), dim), bc_b=_points(_f64(d, "bc_b.bin"), dim),
+                residuals=_f64(d, "residuals.bin").reshape(-1, meta["n_interior"]),
+                outputs=_f64(d, "outputs.bin").reshape(meta["n_interior"], fields),
+            )
+            if meta["rff_shape"]:
+                arrays["rffB"] = arrays["rffB"].reshape(meta["rff_shape"])
+            param_meta = meta["params"]
+    for w in case["workers"]:
+        arrays[f"grad_w{w}"] = grads[w]
+    case_meta = {"case": base, "workers": case["workers"], "worker_losses": {str(w): losses[w] for w in losses},
+                 "params": param_meta}
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), meta=json.dumps(case_meta), **arrays)
+
+
+def make_traj(name, case):
+    meta, d = _run(dict(case, mode="train"))
+    fields = case["model"]["out_dim"]
+    dim = len(case["domain"])
+    m = np.array([row[:8] for row in meta["metrics"]], dtype=np.float64)
+    case_meta = {"case": case, "hashes": meta["hashes"], "aborted": meta["aborted"]}
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), meta=json.dumps(case_meta),
+                        params=_f64(d, "params.bin"), final_params=_f64(d, "final_params.bin"),
+                        metrics=m, rffB=_f64(d, "rff_B.bin"),
+                        interior=_points(_f64(d, "interior.bin"), dim),
+                        ic_points=_points(_f64(d, "ic_points.bin"), dim),
+                        ic_targets=_f64(d, "ic_targets.bin").reshape(fields, -1).T.copy(),
+                        bc_a=_points(_f64(d, "bc_a.bin"), dim), bc_b=_points(_f64(d, "bc_b.bin"), dim))
+
+
+def main():
+    if not os.path.exists(DRIVER):
+        sys.exit(f"{DRIVER} missing: run `make -C oracle` (needs /root/reference)")
+    for n, c in CASES.items():
+        make_case(n, c)
+        print("wrote", n)
+    for n, c in TRAJ.items():
+        make_traj(n, c)
+        print("wrote", n)
+
+
+if __name__ == "__main__":
+    main()

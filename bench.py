@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""PINN train-step throughput (collocation points/s per train step) on B200.
+
+One step = fwd + Taylor jets + residual + loss + parameter gradient (+ NCCL
+all-reduce of the flat gradient when N>1) + device Adam, over every
+collocation point of the rank's shard. Default workload: C5 weak scaling --
+BASELINE.json configs[4] (C4's Maxwell TE 6x256 model) with 1,048,576 points
+per GPU (so N=1 is configs[3]'s 1M-point Maxwell set on one GPU).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c1|c2|c3|c4]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+  python bench.py --impl reference ...   # reference CPU implementation arm
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "collocation points/s per train step (residual+grad), 1/2/4/8 B200 vs CPU"
+UNIT = "points/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--points-per-gpu", type=int, default=1 << 20)
+    ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc3xtf32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def workload(args, world):
+    from paper_2604_15645_b200 import configs
+    if args.config == "c5":
+        wl = configs.get_config("c4")
+        dims = configs.weak_scaling_dims(args.points_per_gpu, world)
+        name = f"c5_weak_maxwell_te_6x256_{args.points_per_gpu}pts_per_gpu"
+    else:
+        wl = configs.get_config(args.config)
+        dims = wl.dims
+        name = wl.name
+    return wl, dims, name
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile(prefix="clocks_", suffix=".csv", delete=False).name
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.out, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.out):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference implementation on this host's cores
+# ---------------------------------------------------------------------------
+
+REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "pinnlab_ref_driver")
+
+
+def cpu_reference(wl, seconds: float):
+    """Time the reference train() (trainer.cpp:332; cfg.workers threads,
+    trainer.cpp:445-457) on a bounded sample of the same model/PDE. Falls
+    back to the FP64 numpy restatement (kind "port") when oracle/_ref is
+    absent. Returns the cpu_baseline dict."""
+    cores = os.cpu_count() or 1
+    if os.path.exists(REF_DRIVER) and wl.res.id != "ns_steady":
+        # reference RSS is ~0.9 MB per point for 6x256 (graph keeps every node)
+        per_point_mb = 0.9 * (wl.spec.hidden_dim / 256.0) * (wl.spec.depth / 6.0) * (wl.streams() / 4.0)
+        try:
+            mem_mb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_AVPHYS_PAGES") / 2**20
+        except Exception:
+            mem_mb = 32768
+        threads = min(cores, 64)
+        # size so one epoch takes ~seconds/4 at ~250 pts/s/thread (6x256) scaled by model cost
+        rate = 250.0 * (7_901_184 / wl.flops_per_point()) * threads
+        n = int(min(rate * seconds / 4.0, 0.4 * mem_mb / max(per_point_mb, 1e-3), 65536))
+        n = max(n, threads * 16)
+        d = len(wl.domain)
+        per = max(2, int(round(n ** (1.0 / d))))
+        dims = [per] * d
+        n = int(np.prod(dims))
+        job = {"mode": "train", "model": _spec_json(wl.spec), "seed": 0,
+               "pde": {"id": wl.res.id, "advection_c": wl.res.advection_c, "epsilon": wl.res.epsilon,
+                       "mu": wl.res.mu},
+               "domain": [list(b) for b in wl.domain], "initial": wl.initial, "bc": wl.bc,
+               "collocation": {"mode": "uniform", "dims": dims, "n_ic": wl.n_ic, "n_bc": wl.n_bc},
+               "workers": threads, "train": {"epochs": 4, "lr": 1e-3}}
+        with tempfile.TemporaryDirectory() as td:
+            job["out"] = td
+            jp = os.path.join(td, "job.json")
+            json.dump(job, open(jp, "w"))
+            r = subprocess.run([REF_DRIVER, jp], capture_output=True, text=True, timeout=600)
+            if r.returncode == 0:
+                m = json.load(open(os.path.join(td, "meta.json")))["metrics"]
+                wall = [row[8] for row in m]
+                steps = np.diff([0.0] + wall)[1:]  # drop the first (allocation warm-up) epoch
+                t = float(np.median(steps))
+                return {"value": n / t, "unit": UNIT, "cores": threads, "kind": "reference",
+                        "sample": f"reference train() (oracle/_ref, Eigen-API shim) {n} pts {dims}, "
+                                  f"{threads} worker threads, median of {len(steps)} epochs after 1 warm-up",
+                        "t_step_s": t}
+    raise RuntimeError("oracle/_ref not built")
+
+
+def _spec_json(s):
+    import dataclasses
+    j = {"in_dim": s.in_dim, "hidden_dim": s.hidden_dim, "depth": s.depth, "out_dim": s.out_dim,
+         "activation": s.activation, "sine_w0": s.sine_w0}
+    if s.periodic_axes:
+        j["periodic_axes"] = [dataclasses.asdict(a) for a in s.periodic_axes]
+    if s.rff:
+        j["rff"] = dataclasses.asdict(s.rff)
+    if s.rwf:
+        j["rwf"] = dataclasses.asdict(s.rwf)
+    return j
+
+
+def cpu_port(wl, seconds: float):
+    """FP64 numpy restatement (oracle/pinn_oracle.py), one process."""
+    from oracle import pinn_oracle as po
+    from paper_2604_15645_b200 import configs
+    spec = po.ModelSpec(wl.spec.in_dim, wl.spec.hidden_dim, wl.spec.depth, wl.spec.out_dim, wl.spec.activation)
+    if wl.spec.rff:
+        spec.rff = po.RFFSpec(wl.spec.rff.width, wl.spec.rff.sigma, wl.spec.rff.mean)
+    if wl.spec.rwf:
+        spec.rwf = po.RWFSpec(wl.spec.rwf.mean, wl.spec.rwf.stddev)
+    res = po.ResidualSpec(wl.res.id, wl.res.advection_c, wl.res.epsilon, wl.res.mu, wl.res.reynolds)
+    n = 4096
+    d = len(wl.domain)
+    per = max(2, int(round(n ** (1.0 / d))))
+    dims = [per] * d
+    col = configs.collocation(wl, dims)
+    ocol = po.Collocation(col["interior"], col["ic_points"], col["ic_targets"], col["bc_a"], col["bc_b"],
+                          col["bc_targets"])
+    flat, rffB = po.init_params(spec, 0)
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        po.worker_step(spec, flat, rffB, res, ocol.interior, ocol, wl.bc)
+        k += 1
+        if time.perf_counter() - t0 > seconds / 3 or k >= 3:
+            break
+    t = (time.perf_counter() - t0) / k
+    npts = int(np.prod(dims))
+    return {"value": npts / t, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"numpy FP64 restatement, {npts} pts {dims}, mean of {k} steps", "t_step_s": t}
+
+
+def cpu_baseline(wl, seconds):
+    try:
+        return cpu_reference(wl, seconds)
+    except Exception:
+        return cpu_port(wl, seconds)
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl, dims, name = workload(args, args.gpus)
+    t0 = time.time()
+    cb = cpu_baseline(wl, args.cpu_seconds)
+    v = cb["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * cb["t_step_s"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": name, "model": "reference pinnlab CPU",
+                                            "parallelism": f"{cb['cores']} std::threads"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.time() - t0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    import paper_2604_15645_b200 as pk
+    from paper_2604_15645_b200 import configs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = max(world, 1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    wl, dims, name = workload(args, world)
+    col = configs.collocation(wl, dims)
+    n_total = len(col["interior"])
+    lo, hi = pk.shard_interior(n_total, world)[rank]
+    shard = col["interior"][lo:hi]
+    flat, rffB = pk.init_params(wl.spec, seed=0)
+    worker = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, shard, col["ic_points"], col["ic_targets"],
+                            col["bc_a"], col["bc_b"], col["bc_targets"], device=local, engine=args.engine)
+    P = worker.n_params
+    params = torch.tensor(flat, dtype=torch.float32, device=dev)
+    grad = torch.zeros(P, dtype=torch.float32, device=dev)
+    m = torch.zeros_like(params)
+    v = torch.zeros_like(params)
+    losses = torch.zeros(3, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    st = stream.cuda_stream
+    lam = (1.0, 1.0, 1.0)
+    t_adam = [0]
+
+    def step():
+        worker.step_device(params, grad, lam, losses, stream=st)
+        if world > 1:
+            dist.all_reduce(grad, op=dist.ReduceOp.SUM)
+        t_adam[0] += 1
+        worker.adam_step_device(params, grad, m, v, t_adam[0], 1e-3, grad_scale=1.0 / world, stream=st)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    worker.check()
+    launches_per_step = worker.launch_count() + 1
+
+    # ---- timed region (device-resident inputs) ----
+    clk = ClockSampler(local)
+    worker.profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    prof = worker.profile_read()
+    worker.profile(False)
+    worker.check()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = n_total / (ms_step / 1e3)
+
+    # ---- e2e: reference-facing C-ABI call with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        host_params = flat.copy()
+        opt_m = np.zeros_like(host_params)
+        opt_v = np.zeros_like(host_params)
+        shard_pinned = torch.from_numpy(np.ascontiguousarray(shard)).pin_memory()
+        g_dev = torch.zeros(P, dtype=torch.float64, device=dev)
+        h2d = d2h = 0
+
+        def e2e_step(k):
+            nonlocal h2d, d2h
+            pts = shard_pinned.numpy()
+            worker.set_points(pts)                      # H2D of this step's collocation batch
+            g_host, l = worker.step(host_params, lam)   # H2D params, D2H grad + losses
+            if world > 1:
+                g_dev.copy_(torch.from_numpy(g_host))
+                dist.all_reduce(g_dev, op=dist.ReduceOp.SUM)
+                g_host = g_dev.cpu().numpy() / world
+            b1, b2 = 0.9, 0.999                          # host Adam (optim.cpp:7-41)
+            opt_m[:] = b1 * opt_m + (1 - b1) * g_host
+            opt_v[:] = b2 * opt_v + (1 - b2) * g_host * g_host
+            host_params[:] -= 1e-3 * (opt_m / (1 - b1 ** k)) / (np.sqrt(opt_v / (1 - b2 ** k)) + 1e-8)
+            h2d = pts.nbytes + P * 4
+            d2h = P * 4 + 3 * 8
+
+        for k in range(1, 3):
+            e2e_step(k)
+        if world > 1:
+            dist.barrier()
+        ke = max(3, args.steps // 2)
+        t0 = time.perf_counter()
+        for k in range(3, 3 + ke):
+            e2e_step(k)
+        te = torch.tensor([(time.perf_counter() - t0) / ke], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_total / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(te.item()),
+               "path": "pnx_set_points + pnx_step (float64 host buffers) + host Adam"}
+
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        # roofline of the dominant kernel class (CUDA events on the launching stream)
+        S = wl.streams()
+        H = wl.spec.hidden_dim
+        rows = hi - lo
+        hidden_gemms = wl.spec.depth - 1  # H x H layers per pass
+        flops_cls = {"fwd_gemm": 2.0 * S * rows * (H * H * hidden_gemms + wl.spec.first_layer_width() * H),
+                     "bwd_gemm": 2.0 * S * rows * H * H * hidden_gemms,
+                     "wgrad_gemm": 2.0 * S * rows * (H * H * hidden_gemms + wl.spec.first_layer_width() * H)}
+        dom = max(flops_cls, key=lambda k: prof[k][0])
+        tms, nl = prof[dom]
+        per_launch_flops = flops_cls[dom] / max(1, nl / args.steps)
+        avg_launch_s = tms / max(nl, 1) / 1e3
+        achieved = per_launch_flops / avg_launch_s / 1e12
+        use_tc = args.engine == "tc3xtf32" or (args.engine == "auto" and H >= 128)
+        fp32_peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
+        peak = fp32_peak
+        peak_note = "FP32 FFMA peak 148 SM x 128 x 2 x sm_max_mhz (derived from MEASURED_PEAKS.json clocks)"
+        step_flops = wl.flops_per_point() * n_total
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak"
+            if args.config == "c5" else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (uniform collocation grid, numpy Xavier init; no dataset)",
+            "config": {"workload": name, "pde": wl.res.id, "model": f"tanh MLP {wl.spec.depth}x{H}",
+                       "points_total": n_total, "points_per_gpu": rows, "streams": S,
+                       "params": P, "engine": args.engine, "parallelism": f"dp{world}",
+                       "l2": "inputs larger than L2 (per-step activations >> 126 MB)"},
+            "tflops_step": step_flops / (ms_step / 1e3) / 1e12,
+            "roofline": {"bound": "tensor" if use_tc else "fp32", "kernel": dom, "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_note,
+                         "per_launch_flops": per_launch_flops, "avg_launch_ms": avg_launch_s * 1e3},
+            "kernel_ms_per_step": {k: prof[k][0] / args.steps for k in prof},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "clocks": clocks,
+            "e2e": e2e,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = {k: v for k, v in cpu_baseline(wl, args.cpu_seconds).items() if k != "t_step_s"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

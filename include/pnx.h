@@ -1,0 +1,143 @@
+/*
+ * pnx.h -- C ABI of the B200 PINN train-step hot path (libpnx.so).
+ *
+ * Drop-in boundary for the reference pinnlab core (/root/reference/proj/core).
+ * The reference has no FFI; its seam is the per-worker step
+ *   run_worker_epoch(const WorkerTask&) -> WorkerOutput   (trainer.cpp:189-262)
+ * and the public one-step contract
+ *   data_parallel_gradient(Model&, const TrainingProblem&,
+ *                          const TrainConfig&, int W)     (trainer.hpp:118-119)
+ * Each entry point below names the reference interface it replaces. Arrays
+ * crossing the ABI are plain pointers + sizes; floating-point data at the host
+ * boundary is float64 like the reference's Tensor (tensor.hpp:19-22); the
+ * device computes in float32 (FP32 FMA / 3xTF32 tensor-core contractions).
+ *
+ * Errors: every call returns PNX_OK (0) or a negative code; pnx_last_error()
+ * returns the message, which uses the reference's TensorError text where one
+ * exists (e.g. "residual_loss: non-finite residual at point index 17",
+ * losses.cpp:86-90; "data parallel: fewer interior points than workers",
+ * trainer.cpp:147). No exceptions cross the ABI. A context is single-threaded
+ * (like Graph, graph.hpp:69-70) and bound to one CUDA device.
+ */
+#ifndef PNX_H_
+#define PNX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PNX_OK 0
+#define PNX_ERR_ARG -1       /* invalid argument / shape (TensorError) */
+#define PNX_ERR_CUDA -2      /* CUDA runtime failure / no device */
+#define PNX_ERR_NONFINITE -3 /* non-finite residual, loss or gradient */
+#define PNX_ERR_STATE -4     /* call order (e.g. step before set_points) */
+
+typedef struct pnx_ctx pnx_ctx;
+
+/* Activation (model.hpp:12). */
+enum { PNX_ACT_TANH = 0, PNX_ACT_SINE = 1, PNX_ACT_SWISH = 2 };
+/* PdeId (losses.hpp:14) + the ns_steady extension. */
+enum { PNX_PDE_ADVECTION = 0, PNX_PDE_ALLEN_CAHN = 1, PNX_PDE_BURGERS = 2,
+       PNX_PDE_MAXWELL_TE = 3, PNX_PDE_NS_STEADY = 4 };
+/* TrainingProblem::Bc (trainer.hpp:23-27). */
+enum { PNX_BC_HARD = 0, PNX_BC_SOFT_PERIODIC = 1, PNX_BC_DIRICHLET_ZERO = 2 };
+/* Contraction engine for the hidden layers. */
+enum { PNX_ENGINE_AUTO = 0, PNX_ENGINE_FFMA = 1, PNX_ENGINE_TC3XTF32 = 2 };
+
+/* ModelSpec (model.hpp:41-57). rff_B is the frozen RFF matrix Model::rff_matrix()
+ * [embedded_width x rff_width] row-major (model.cpp:58-62); NULL when rff_width==0.
+ * periodic/period/period_trainable have n_periodic_axes entries (0 or in_dim)
+ * mirroring ModelSpec::periodic_axes (AxisPeriodic, model.hpp:32-36). */
+typedef struct {
+    int32_t in_dim, hidden_dim, depth, out_dim;
+    int32_t activation;
+    double sine_w0;
+    int32_t n_periodic_axes;
+    const int32_t* periodic;
+    const double* period;
+    const int32_t* period_trainable;
+    int32_t rff_width;
+    const double* rff_B;
+    int32_t rwf; /* 1: layers are (V, s) pairs, W = V * exp(s) (model.cpp:117-126) */
+} pnx_model_desc;
+
+/* ResidualSpec (losses.hpp:22-30) + TrainingProblem::bc. */
+typedef struct {
+    int32_t pde;
+    double advection_c, epsilon, mu, reynolds;
+    int32_t bc;
+} pnx_problem_desc;
+
+/* Create a worker context on CUDA device `device`. Replaces the per-worker
+ * Graph + Model::bind of run_worker_epoch (trainer.cpp:205-207). */
+int pnx_create(const pnx_model_desc* model, const pnx_problem_desc* problem, int device,
+               pnx_ctx** out);
+void pnx_destroy(pnx_ctx* ctx);
+const char* pnx_last_error(const pnx_ctx* ctx);
+/* Message of the last failure of pnx_create (no context exists then). */
+const char* pnx_create_error(void);
+
+/* Model::trainable_count() (model.cpp:104-108); the flat layout is
+ * flatten_params (trainer.cpp:290-298): trainable() order, row-major. */
+int pnx_param_count(const pnx_ctx* ctx, int64_t* n);
+
+/* Interior collocation shard (WorkerTask::interior, trainer.cpp:192), axis-major
+ * float64 [n_axes][n] (Points::coords, losses.hpp:39-43; space first, time last). */
+int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes);
+/* Replicated IC set + per-field targets [out_dim][n] (CollocationData::ic_points /
+ * ic_targets, trainer.hpp:140-146; losses.cpp:113-119). */
+int pnx_set_ic(pnx_ctx* ctx, const double* coords, const double* targets, int64_t n);
+/* Replicated BC set (trainer.cpp:98-125). soft_periodic: a and b paired traces
+ * (losses.cpp:121-135), targets NULL. dirichlet_zero: a = stacked traces,
+ * b NULL, targets [out_dim][n] (losses.cpp:137-144). */
+int pnx_set_bc(pnx_ctx* ctx, const double* a, const double* b, const double* targets, int64_t n);
+
+/* One worker step: losses + gradient of total = lam_pde L_pde + lam_ic L_ic
+ * (+ lam_bc L_bc) (trainer.cpp:234-253) for the current shard. params/grad_out
+ * are flat float64 in trainable() order; losses_out = {pde, ic, bc}
+ * (TermLosses, trainer.cpp:179-181). Host buffers; synchronous. */
+int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double* grad_out,
+             double losses_out[3]);
+
+/* Device-resident variant (no host copies): d_params/d_grad are float32 device
+ * pointers of param_count entries, d_losses (may be NULL) receives 3 doubles;
+ * work is enqueued on `stream` (a cudaStream_t, 0 = legacy default). The
+ * non-finite check is deferred: call pnx_check(ctx) after synchronizing. */
+int pnx_step_device(pnx_ctx* ctx, const float* d_params, const double lambdas[3], float* d_grad,
+                    double* d_losses, void* stream);
+int pnx_check(pnx_ctx* ctx);
+
+/* Device Adam (optim.cpp:7-41) with ExponentialLr lr = base*gamma^epoch
+ * (optim.cpp:71-73) and an optional 1/W gradient scale (average_grads,
+ * trainer.cpp:278-280), fused in one kernel: p -= lr*mhat/(sqrt(vhat)+eps).
+ * t is the step count AFTER increment (first step t=1). */
+int pnx_adam_step_device(pnx_ctx* ctx, float* d_params, const float* d_grad, float* d_m, float* d_v,
+                         int64_t n, double lr, double beta1, double beta2, double eps, int64_t t,
+                         double grad_scale, void* stream);
+
+/* Engine selection and chunking (rows per pass through the layer stack). */
+int pnx_set_engine(pnx_ctx* ctx, int engine);
+int pnx_set_chunk_rows(pnx_ctx* ctx, int64_t rows);
+/* Number of kernels the last step launched (for bench evidence). */
+int pnx_last_launch_count(const pnx_ctx* ctx, int64_t* n);
+
+/* Kernel-class timing with CUDA events recorded on the launching stream around
+ * every launch of a class (0 input, 1 forward GEMM, 2 head, 3 reverse GEMM,
+ * 4 weight-gradient GEMM, 5 finalize). pnx_profile(ctx, 1) resets and enables;
+ * pnx_profile_read synchronizes and returns accumulated ms and launch counts. */
+int pnx_profile(pnx_ctx* ctx, int on);
+int pnx_profile_read(pnx_ctx* ctx, double* ms, int64_t* counts, int n);
+
+/* Diagnostics mirroring residual_components (losses.hpp:51-53): when capture
+ * is on, pnx_step records the interior residuals, copied out component-major
+ * [K][n_interior] as float64. */
+int pnx_capture_residuals(pnx_ctx* ctx, int on);
+int pnx_copy_residuals(pnx_ctx* ctx, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PNX_H_ */

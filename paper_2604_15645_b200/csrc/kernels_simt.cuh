@@ -1,0 +1,832 @@
+// kernels_simt.cuh -- FP32 CUDA-core (FFMA) kernels of the jet train step.
+//
+// Data layout in HBM (per chunk of Rpad rows, Rpad a multiple of 64):
+//   Hin  [S][Rpad][K0]   input-feature jets after embedding / RFF
+//   Z_l  [S][Rpad][H]    pre-activation jets of hidden layer l
+//   Zb   [S][Rpad][H]    adjoints of a hidden layer's pre-activation jets
+// Stream-major, feature-contiguous: every GEMM operand is a plain row-major
+// [rows x features] matrix per stream, and all S streams of one
+// (point, feature) element meet in one thread for the jet epilogues.
+//
+// Reverse mode of the jet program (see oracle/pinn_oracle.py):
+//   forward   Z_l[s] = act(Z_{l-1})[s] W_l + [s==0] b_l         (model.cpp:163-175)
+//   head      O = act(Z_{L-2}) W_L + b_L, residual, seeds Obar     (losses.cpp:26-95)
+//   reverse   Zb_{l-1} = act^T(Zb_l W_l^T ; Z_{l-1})              (graph.cpp:468-502)
+//             dW_l = sum_s act(Z_{l-1})[s]^T Zb_l[s],  db_l = colsum Zb_l[0]
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "jets.cuh"
+#include "residuals.cuh"
+
+namespace pnx {
+
+constexpr int kMaxLayers = 16;
+constexpr int kMaxAxes = 4;
+
+// ---------------------------------------------------------------------------
+// parameter preparation: W = V*exp(s) (model.cpp:117-126), W^T, bias
+// ---------------------------------------------------------------------------
+struct LayerTab {
+    int n;                       // number of linear layers (depth + 1)
+    int K[kMaxLayers], N[kMaxLayers];
+    int64_t offW[kMaxLayers];    // flat offset of W or V
+    int64_t offS[kMaxLayers];    // flat offset of s (RWF) or -1
+    int64_t offB[kMaxLayers];    // flat offset of b
+    int64_t dW[kMaxLayers];      // offset into the materialised weight arena
+    int64_t dB[kMaxLayers];      // offset into the bias arena
+};
+
+__global__ void k_prep(const float* __restrict__ params, LayerTab t, float* __restrict__ W,
+                       float* __restrict__ Wt, float* __restrict__ bias) {
+    const int l = blockIdx.y;
+    if (l >= t.n) return;
+    const int K = t.K[l], N = t.N[l];
+    const int64_t total = (int64_t)K * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total + N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < total) {
+            const int k = (int)(i / N), n = (int)(i % N);
+            float w = params[t.offW[l] + i];
+            if (t.offS[l] >= 0) w = w * expf(params[t.offS[l] + n]);
+            W[t.dW[l] + i] = w;
+            Wt[t.dW[l] + (int64_t)n * K + k] = w;
+        } else {
+            const int n = (int)(i - total);
+            bias[t.dB[l] + n] = params[t.offB[l] + n];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// input features: coordinate embedding (model.cpp:134-154) + RFF (:157-161),
+// evaluated in float64 from float64 coordinates, stored as float32 jets.
+// ---------------------------------------------------------------------------
+struct InputArgs {
+    const double* coords;   // [d][ld] float64, global rows
+    int64_t ld;             // leading dimension of coords
+    int64_t row0;           // first global row of this chunk
+    int nrows, Rpad;
+    int in_dim;
+    int periodic[kMaxAxes];
+    double period[kMaxAxes];
+    int64_t period_off[kMaxAxes];  // flat param offset of a trainable period, else -1
+    const float* params;
+    int E;                  // embedded width
+    int rff_w;              // 0 = off
+    const double* rffB;     // [E][rff_w]
+    int K0;                 // feature width written (E or 2*rff_w)
+    float* Hin;             // [S][Rpad][K0]
+};
+
+// embedding jets e[s][c] (c < E) for one row, float64
+template <int L>
+__device__ __forceinline__ void embed_row(const InputArgs& a, int64_t g, double (*e)[2 * kMaxAxes]) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    int c = 0;
+    for (int ax = 0; ax < a.in_dim; ++ax) {
+        const double x = a.coords[(int64_t)ax * a.ld + g];
+        if (!a.periodic[ax]) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                e[s][c] = (s == 0) ? x : ((St::order(s) == 1 && St::axis(s) == ax) ? 1.0 : 0.0);
+            c += 1;
+            continue;
+        }
+        double kappa, phi;
+        if (a.period_off[ax] >= 0) {  // phase = affine(scale(x, P^-1), 2pi) (model.cpp:144-147)
+            const double P = (double)a.params[a.period_off[ax]];
+            kappa = 2.0 * CUDART_PI * (1.0 / P);
+            phi = 2.0 * CUDART_PI * (x * (1.0 / P));
+        } else {  // affine(x, 2pi/P) (model.cpp:149)
+            kappa = 2.0 * CUDART_PI / a.period[ax];
+            phi = x * kappa;
+        }
+        double sp, cp;
+        sincos(phi, &sp, &cp);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            double C = 0.0, Sn = 0.0;
+            if (s == 0) {
+                C = cp;
+                Sn = sp;
+            } else if (St::axis(s) == ax) {
+                if (St::order(s) == 1) {
+                    C = -sp * kappa;
+                    Sn = cp * kappa;
+                } else {
+                    C = -cp * kappa * kappa;
+                    Sn = -sp * kappa * kappa;
+                }
+            }
+            e[s][c] = C;
+            e[s][c + 1] = Sn;
+        }
+        c += 2;
+    }
+}
+
+template <int L>
+__global__ void k_input(InputArgs a) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    const int per_row = a.rff_w > 0 ? a.rff_w : 1;
+    const int64_t total = (int64_t)a.Rpad * per_row;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / per_row), c = (int)(i % per_row);
+        const int64_t RK = (int64_t)a.Rpad * a.K0;
+        float* out = a.Hin + (int64_t)r * a.K0;
+        if (r >= a.nrows) {  // zero padding rows so they stay finite downstream
+            if (a.rff_w > 0) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    out[s * RK + c] = 0.0f;
+                    out[s * RK + a.rff_w + c] = 0.0f;
+                }
+            } else {
+                for (int s = 0; s < S; ++s)
+                    for (int k = 0; k < a.K0; ++k) out[s * RK + k] = 0.0f;
+            }
+            continue;
+        }
+        double e[S][2 * kMaxAxes];
+        embed_row<L>(a, a.row0 + r, e);
+        if (a.rff_w == 0) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                for (int k = 0; k < a.E; ++k) out[s * RK + k] = (float)e[s][k];
+            continue;
+        }
+        // m = e B  (B frozen, float64), then [cos m, sin m] jets
+        double m[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            double acc = 0.0;
+            for (int k = 0; k < a.E; ++k) acc += e[s][k] * a.rffB[(int64_t)k * a.rff_w + c];
+            m[s] = acc;
+        }
+        double sm, cm;
+        sincos(m[0], &sm, &cm);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            double C, Sn;
+            if (s == 0) {
+                C = cm;
+                Sn = sm;
+            } else if (St::order(s) == 1) {
+                C = -sm * m[s];
+                Sn = cm * m[s];
+            } else {
+                const double ma = m[St::partner(s)];
+                C = -sm * m[s] - cm * ma * ma;
+                Sn = cm * m[s] - sm * ma * ma;
+            }
+            out[s * RK + c] = (float)C;
+            out[s * RK + a.rff_w + c] = (float)Sn;
+        }
+    }
+}
+
+// Trainable-period gradient: given Hbar_in [S][Rpad][K0] (adjoint of the input
+// features), back through RFF (B frozen) and the embedding to each trainable
+// period: d phi/dP = -phi/P, d kappa/dP = -kappa/P.
+template <int L>
+__global__ void k_input_bwd(InputArgs a, const float* __restrict__ Hb, double* __restrict__ partP) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    double accP[kMaxAxes] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t RK = (int64_t)a.Rpad * a.K0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.nrows; r += gridDim.x * blockDim.x) {
+        double e[S][2 * kMaxAxes];
+        embed_row<L>(a, a.row0 + r, e);
+        double eb[S][2 * kMaxAxes];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            for (int k = 0; k < a.E; ++k) eb[s][k] = 0.0;
+        const float* hb = Hb + (int64_t)r * a.K0;
+        if (a.rff_w == 0) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                for (int k = 0; k < a.E; ++k) eb[s][k] = hb[s * RK + k];
+        } else {
+            for (int c = 0; c < a.rff_w; ++c) {
+                double m[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    double acc = 0.0;
+                    for (int k = 0; k < a.E; ++k) acc += e[s][k] * a.rffB[(int64_t)k * a.rff_w + c];
+                    m[s] = acc;
+                }
+                double sm, cm;
+                sincos(m[0], &sm, &cm);
+                double Cb[S], Sb[S], mb[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    Cb[s] = hb[s * RK + c];
+                    Sb[s] = hb[s * RK + a.rff_w + c];
+                    mb[s] = 0.0;
+                }
+                double cmb = Cb[0], smb = Sb[0];
+#pragma unroll
+                for (int s = 1; s < S; ++s) {
+                    if (St::order(s) == 1) {
+                        cmb += Sb[s] * m[s];
+                        smb += -Cb[s] * m[s];
+                        mb[s] += -sm * Cb[s] + cm * Sb[s];
+                    } else {
+                        const int p = St::partner(s);
+                        const double ma = m[p], maa = m[s];
+                        cmb += -Cb[s] * ma * ma + Sb[s] * maa;
+                        smb += -Cb[s] * maa - Sb[s] * ma * ma;
+                        mb[p] += -2.0 * cm * ma * Cb[s] - 2.0 * sm * ma * Sb[s];
+                        mb[s] += -sm * Cb[s] + cm * Sb[s];
+                    }
+                }
+                mb[0] += -sm * cmb + cm * smb;
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+                    for (int k = 0; k < a.E; ++k) eb[s][k] += mb[s] * a.rffB[(int64_t)k * a.rff_w + c];
+            }
+        }
+        // embedding transpose, trainable periods only
+        int col = 0;
+        for (int ax = 0; ax < a.in_dim; ++ax) {
+            if (!a.periodic[ax]) {
+                col += 1;
+                continue;
+            }
+            if (a.period_off[ax] >= 0) {
+                const double x = a.coords[(int64_t)ax * a.ld + a.row0 + r];
+                const double P = (double)a.params[a.period_off[ax]];
+                const double kappa = 2.0 * CUDART_PI * (1.0 / P);
+                const double phi = 2.0 * CUDART_PI * (x * (1.0 / P));
+                double sp, cp;
+                sincos(phi, &sp, &cp);
+                double phib = -sp * eb[0][col] + cp * eb[0][col + 1], kb = 0.0;
+#pragma unroll
+                for (int s = 1; s < S; ++s) {
+                    if (St::axis(s) != ax) continue;
+                    const double Cb = eb[s][col], Sbv = eb[s][col + 1];
+                    if (St::order(s) == 1) {
+                        phib += -cp * kappa * Cb - sp * kappa * Sbv;
+                        kb += -sp * Cb + cp * Sbv;
+                    } else {
+                        phib += sp * kappa * kappa * Cb - cp * kappa * kappa * Sbv;
+                        kb += -2.0 * cp * kappa * Cb - 2.0 * sp * kappa * Sbv;
+                    }
+                }
+                accP[ax] += phib * (-phi / P) + kb * (-kappa / P);
+            }
+            col += 2;
+        }
+    }
+    // block reduction (fixed order) -> partP[block][axis]
+    __shared__ double red[kMaxAxes][256];
+    for (int ax = 0; ax < kMaxAxes; ++ax) red[ax][threadIdx.x] = accP[ax];
+    __syncthreads();
+    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off)
+            for (int ax = 0; ax < kMaxAxes; ++ax) red[ax][threadIdx.x] += red[ax][threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int ax = 0; ax < kMaxAxes; ++ax) partP[blockIdx.x * kMaxAxes + ax] += red[ax][0];
+}
+
+// ---------------------------------------------------------------------------
+// Tiled FFMA GEMM over all streams with fused jet prologue / epilogue.
+//   C[s] = PRO(A[s]) (Rpad x K) * B (K x N)
+//   EPI_BIAS : out[s] = C[s] + [s==0] bias           (forward layer)
+//   EPI_ACTT : out[s] = act^T(Zlow; C)[s]            (reverse layer)
+//   EPI_RAW  : out[s] = C[s]
+// ---------------------------------------------------------------------------
+enum Epi : int { EPI_BIAS = 0, EPI_ACTT = 1, EPI_RAW = 2 };
+
+struct GemmArgs {
+    const float* A;   // [S][Rpad][K]
+    const float* B;   // [K][N]
+    const float* bias;
+    const float* Zlow;  // [S][Rpad][N] (EPI_ACTT)
+    float* out;       // [S][Rpad][N]
+    int Rpad, K, N;
+    float w0;
+};
+
+constexpr int GT_M = 64, GT_N = 64, GT_K = 16;
+
+template <int L, int PRO, int EPI, int EACT>
+__global__ void __launch_bounds__(256) k_gemm(GemmArgs g) {
+    constexpr int S = Streams<L>::S;
+    __shared__ __align__(16) float As[S][GT_K][GT_M + 4];
+    __shared__ __align__(16) float Bs[GT_K][GT_N + 4];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int r0 = blockIdx.x * GT_M, n0 = blockIdx.y * GT_N;
+    const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * g.N;
+    float acc[S][4][4];
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[s][i][j] = 0.0f;
+
+    for (int k0 = 0; k0 < g.K; k0 += GT_K) {
+#pragma unroll
+        for (int e = 0; e < (GT_M * GT_K) / 256; ++e) {
+            const int idx = tid + 256 * e;
+            const int r = idx / GT_K, k = idx % GT_K;
+            float z[S], h[S];
+            if (k0 + k < g.K) {
+                const float* p = g.A + (int64_t)(r0 + r) * g.K + k0 + k;
+#pragma unroll
+                for (int s = 0; s < S; ++s) z[s] = p[s * RK];
+                act_fwd<L, PRO>(z, h, g.w0);
+            } else {
+#pragma unroll
+                for (int s = 0; s < S; ++s) h[s] = 0.0f;
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) As[s][k][r] = h[s];
+        }
+#pragma unroll
+        for (int e = 0; e < (GT_K * GT_N) / 256; ++e) {
+            const int idx = tid + 256 * e;
+            const int k = idx / GT_N, n = idx % GT_N;
+            Bs[k][n] = (k0 + k < g.K && n0 + n < g.N) ? g.B[(int64_t)(k0 + k) * g.N + n0 + n] : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < GT_K; ++kk) {
+            const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+            const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const float4 a4 = *reinterpret_cast<const float4*>(&As[s][kk][ty * 4]);
+                const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[s][i][j] = fmaf(a[i], b[j], acc[s][i][j]);
+            }
+        }
+        __syncthreads();
+    }
+
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = r0 + ty * 4 + i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx * 4 + j;
+            if (n >= g.N) continue;
+            const int64_t o = (int64_t)r * g.N + n;
+            if constexpr (EPI == EPI_BIAS) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) g.out[s * RN + o] = acc[s][i][j] + (s == 0 ? g.bias[n] : 0.0f);
+            } else if constexpr (EPI == EPI_RAW) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) g.out[s * RN + o] = acc[s][i][j];
+            } else {
+                float z[S], hb[S], zb[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    z[s] = g.Zlow[s * RN + o];
+                    hb[s] = acc[s][i][j];
+                }
+                act_bwd<L, EACT>(z, hb, zb, g.w0);
+#pragma unroll
+                for (int s = 0; s < S; ++s) g.out[s * RN + o] = zb[s];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Weight gradient: part[split][k][n] += sum_s sum_r PRO(A[s][r][k]) Bm[s][r][n]
+// (FP32 over a 16-row block, FP64 across blocks; deterministic split order).
+// blockIdx.y == 0 CTAs also produce db[n] = sum_r Bm[0][r][n].
+// ---------------------------------------------------------------------------
+struct WgradArgs {
+    const float* A;   // [S][Rpad][K]
+    const float* Bm;  // [S][Rpad][N]
+    double* part;     // [splits][K*N + N]
+    int Rpad, nrows_valid, K, N, rows_per_split;
+    float w0;
+};
+
+constexpr int WT_R = 16;
+
+template <int L, int PRO>
+__global__ void __launch_bounds__(256) k_wgrad(WgradArgs g) {
+    constexpr int S = Streams<L>::S;
+    __shared__ __align__(16) float As[S][WT_R][64 + 4];
+    __shared__ __align__(16) float Bs[S][WT_R][64 + 4];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int n0 = blockIdx.x * 64, k0 = blockIdx.y * 64;
+    const int rbeg = blockIdx.z * g.rows_per_split;
+    const int rend = min(g.nrows_valid, rbeg + g.rows_per_split);
+    const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * g.N;
+    double dacc[4][4];
+    double dbias[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dacc[i][j] = 0.0;
+
+    for (int rb = rbeg; rb < rend; rb += WT_R) {
+#pragma unroll
+        for (int e = 0; e < (WT_R * 64) / 256; ++e) {
+            const int idx = tid + 256 * e;
+            const int r = idx / 64, c = idx % 64;
+            const bool rv = rb + r < rend;
+            float z[S], h[S];
+            if (rv && k0 + c < g.K) {
+                const float* p = g.A + (int64_t)(rb + r) * g.K + k0 + c;
+#pragma unroll
+                for (int s = 0; s < S; ++s) z[s] = p[s * RK];
+                act_fwd<L, PRO>(z, h, g.w0);
+            } else {
+#pragma unroll
+                for (int s = 0; s < S; ++s) h[s] = 0.0f;
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) As[s][r][c] = h[s];
+            const bool cv = rv && n0 + c < g.N;
+            const float* q = g.Bm + (int64_t)(rb + r) * g.N + n0 + c;
+#pragma unroll
+            for (int s = 0; s < S; ++s) Bs[s][r][c] = cv ? q[s * RN] : 0.0f;
+        }
+        __syncthreads();
+        float acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+        float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int r = 0; r < WT_R; ++r) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const float4 a4 = *reinterpret_cast<const float4*>(&As[s][r][ty * 4]);
+                const float4 b4 = *reinterpret_cast<const float4*>(&Bs[s][r][tx * 4]);
+                const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+                const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                if (s == 0) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) bsum[j] += b[j];
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dacc[i][j] += (double)acc[i][j];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dbias[j] += (double)bsum[j];
+        __syncthreads();
+    }
+    double* part = g.part + (int64_t)blockIdx.z * ((int64_t)g.K * g.N + g.N);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = k0 + ty * 4 + i;
+        if (k >= g.K) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx * 4 + j;
+            if (n < g.N) part[(int64_t)k * g.N + n] += dacc[i][j];
+        }
+    }
+    if (blockIdx.y == 0 && ty == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx * 4 + j;
+            if (n < g.N) part[(int64_t)g.K * g.N + n] += dbias[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Head: last linear layer + residual / data losses + seeds + first reverse
+// step, one warp per row (losses.cpp:77-144, trainer.cpp:234-236).
+// ---------------------------------------------------------------------------
+constexpr int kHeadMaxJ = 16;  // hidden width <= 512
+constexpr int kHeadWarps = 8;
+
+struct HeadArgs {
+    const float* Z;      // [S][Rpad][H]
+    float* Zb;           // [S][Rpad][H]
+    const float* W;      // [H][F]
+    const float* b;      // [F]
+    int H, Rpad, nrows;
+    int64_t row0;        // global row of chunk row 0
+    // global row segments: [bca0,bca1) [bcb0,bcb1) [ic0,ic1) [int0,int1)
+    int64_t bca0, bca1, bcb0, bcb1, ic0, ic1, int0, int1;
+    int bc_mode;
+    const float* ic_t;   // [F][n_ic]
+    const float* bc_t;   // [F][n_bc]
+    const float* bc_vals;  // periodic: [2][n_pairs][F]
+    float w_pde, w_ic, w_bc;  // 2*lambda/n per term
+    PdeConst pc;
+    float w0;
+    double* loss_part;   // [grid][3]
+    double* head_part;   // [grid][H*F + F]
+    int* bad;            // [3] first non-finite interior index per component
+    float* resid_out;    // optional [K][n_int] (interior residuals, diagnostics)
+    int values_only;     // periodic prepass: write O[0] of bc rows to bc_vals
+    float* vals_out;
+};
+
+template <int P, int ACT, int J>
+__global__ void __launch_bounds__(32 * kHeadWarps) k_head(HeadArgs a) {
+    using Tr = PdeTraits<P>;
+    constexpr int L = Tr::L, F = Tr::F, K = Tr::K;
+    constexpr int S = Streams<L>::S;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int gw = blockIdx.x * kHeadWarps + wid, nw = gridDim.x * kHeadWarps;
+    const int64_t RH = (int64_t)a.Rpad * a.H;
+
+    float wreg[J][F];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int k = lane + 32 * j;
+#pragma unroll
+        for (int f = 0; f < F; ++f) wreg[j][f] = (k < a.H) ? a.W[k * F + f] : 0.0f;
+    }
+    double accW[J][F];
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int f = 0; f < F; ++f) accW[j][f] = 0.0;
+    double accB[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) accB[f] = 0.0;
+    double lpde = 0.0, lic = 0.0, lbc = 0.0;
+
+    for (int r = gw; r < a.nrows; r += nw) {
+        const int64_t g = a.row0 + r;
+        float z[S][J], h[S][J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int k = lane + 32 * j;
+            float zz[S], hh[S];
+            if (k < a.H) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) zz[s] = a.Z[s * RH + (int64_t)r * a.H + k];
+                act_fwd<L, ACT>(zz, hh, a.w0);
+            } else {
+#pragma unroll
+                for (int s = 0; s < S; ++s) zz[s] = hh[s] = 0.0f;
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                z[s][j] = zz[s];
+                h[s][j] = hh[s];
+            }
+        }
+        float o[S * F];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+                float v = 0.0f;
+#pragma unroll
+                for (int j = 0; j < J; ++j) v = fmaf(h[s][j], wreg[j][f], v);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                o[s * F + f] = v + (s == 0 ? a.b[f] : 0.0f);
+            }
+
+        if (a.values_only) {
+            if (lane == 0) {
+                int64_t slot = -1;
+                if (g >= a.bca0 && g < a.bca1) slot = g - a.bca0;
+                else if (g >= a.bcb0 && g < a.bcb1) slot = (a.bca1 - a.bca0) + (g - a.bcb0);
+                if (slot >= 0)
+                    for (int f = 0; f < F; ++f) a.vals_out[slot * F + f] = o[f];
+            }
+            continue;
+        }
+
+        float ob[S * F];
+#pragma unroll
+        for (int i = 0; i < S * F; ++i) ob[i] = 0.0f;
+        if (g >= a.int0 && g < a.int1) {
+            float res[K], rb[K];
+            residual<P>(o, res, a.pc);
+            float sq = 0.0f;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                sq += res[k] * res[k];
+                rb[k] = a.w_pde * res[k];
+                if (lane == 0 && !isfinite(res[k])) atomicMin(&a.bad[k], (int)(g - a.int0));
+            }
+            if (a.resid_out && lane == 0) {
+                const int64_t n_int = a.int1 - a.int0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) a.resid_out[k * n_int + (g - a.int0)] = res[k];
+            }
+            lpde += (double)sq;
+            residual_seed<P>(o, rb, ob, a.pc);
+        } else if (g >= a.ic0 && g < a.ic1) {
+            const int64_t i = g - a.ic0, n = a.ic1 - a.ic0;
+            float sq = 0.0f;
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+                const float d = o[f] - a.ic_t[f * n + i];
+                sq += d * d;
+                ob[f] = a.w_ic * d;
+            }
+            lic += (double)sq;
+        } else if (a.bc_mode == 2 && g >= a.bca0 && g < a.bca1) {  // dirichlet
+            const int64_t i = g - a.bca0, n = a.bca1 - a.bca0;
+            float sq = 0.0f;
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+                const float d = o[f] - a.bc_t[f * n + i];
+                sq += d * d;
+                ob[f] = a.w_bc * d;
+            }
+            lbc += (double)sq;
+        } else if (a.bc_mode == 1 && g >= a.bca0 && g < a.bca1) {  // periodic side a
+            const int64_t i = g - a.bca0, np = a.bca1 - a.bca0;
+            float sq = 0.0f;
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+                const float d = o[f] - a.bc_vals[(np + i) * F + f];
+                sq += d * d;
+                ob[f] = a.w_bc * d;
+            }
+            lbc += (double)sq;
+        } else if (a.bc_mode == 1 && g >= a.bcb0 && g < a.bcb1) {  // periodic side b
+            const int64_t i = g - a.bcb0;
+#pragma unroll
+            for (int f = 0; f < F; ++f) ob[f] = -a.w_bc * (a.bc_vals[i * F + f] - o[f]);
+        }
+        // reverse through the head: hbar = Obar W^T, dW_L += h^T Obar
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int k = lane + 32 * j;
+            float hb[S], zz[S], zb[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                float v = 0.0f;
+#pragma unroll
+                for (int f = 0; f < F; ++f) v = fmaf(ob[s * F + f], wreg[j][f], v);
+                hb[s] = v;
+                zz[s] = z[s][j];
+            }
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+                float v = 0.0f;
+#pragma unroll
+                for (int s = 0; s < S; ++s) v = fmaf(h[s][j], ob[s * F + f], v);
+                accW[j][f] += (double)v;
+            }
+            if (k < a.H) {
+                act_bwd<L, ACT>(zz, hb, zb, a.w0);
+#pragma unroll
+                for (int s = 0; s < S; ++s) a.Zb[s * RH + (int64_t)r * a.H + k] = zb[s];
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < F; ++f) accB[f] += (double)ob[f];
+    }
+    if (a.values_only) return;
+    // pad rows of the chunk: zero adjoints so they contribute nothing
+    for (int r = a.nrows + gw; r < a.Rpad; r += nw)
+        for (int k = lane; k < a.H; k += 32)
+#pragma unroll
+            for (int s = 0; s < S; ++s) a.Zb[s * RH + (int64_t)r * a.H + k] = 0.0f;
+
+    // deterministic block reduction: warps in order
+    __shared__ double sh[512 * 3 + 3 + 3];
+    const int nWF = a.H * F;
+    for (int i = threadIdx.x; i < nWF + F + 3; i += blockDim.x) sh[i] = 0.0;
+    __syncthreads();
+    for (int w = 0; w < kHeadWarps; ++w) {
+        if (wid == w) {
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int k = lane + 32 * j;
+                if (k < a.H)
+#pragma unroll
+                    for (int f = 0; f < F; ++f) sh[k * F + f] += accW[j][f];
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int f = 0; f < F; ++f) sh[nWF + f] += accB[f];
+                sh[nWF + F + 0] += lpde;
+                sh[nWF + F + 1] += lic;
+                sh[nWF + F + 2] += lbc;
+            }
+        }
+        __syncthreads();
+    }
+    double* hp = a.head_part + (int64_t)blockIdx.x * (nWF + F);
+    for (int i = threadIdx.x; i < nWF + F; i += blockDim.x) hp[i] += sh[i];
+    if (threadIdx.x < 3) a.loss_part[blockIdx.x * 3 + threadIdx.x] += sh[nWF + F + threadIdx.x];
+}
+
+// ---------------------------------------------------------------------------
+// finalize: fixed-order reduction of partials -> flat float32 gradient in
+// trainable() order (RWF: dV = dW*exp(s), ds = exp(s)*colsum(dW*V)), losses.
+// ---------------------------------------------------------------------------
+struct FinalArgs {
+    LayerTab t;
+    const double* part[kMaxLayers];  // per layer: [nsplit][K*N + N]
+    int nsplit[kMaxLayers];
+    const float* params;
+    float* grad;                     // flat
+    double* dWscratch;               // max(K*N + N) doubles
+};
+
+// reduce splits of layer l into dWscratch (double)
+__global__ void k_reduce_splits(const double* __restrict__ part, int nsplit, int64_t len,
+                                double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * len + i];
+        out[i] = s;
+    }
+}
+
+// write layer l's flat grads from the reduced dW (K*N) + db (N)
+__global__ void k_write_layer_grad(const double* __restrict__ red, const float* __restrict__ params,
+                                   int K, int N, int64_t offW, int64_t offS, int64_t offB, float scale,
+                                   float* __restrict__ grad) {
+    const int64_t total = (int64_t)K * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total + N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < total) {
+            const int n = (int)(i % N);
+            double v = red[i];
+            if (offS >= 0) v *= exp((double)params[offS + n]);
+            grad[offW + i] = (float)(v * scale);
+        } else {
+            const int n = (int)(i - total);
+            grad[offB + n] = (float)(red[total + n] * scale);
+            if (offS >= 0) {  // ds_n = exp(s_n) * sum_k dW[k][n] * V[k][n]
+                double acc = 0.0;
+                for (int k = 0; k < K; ++k) acc += red[(int64_t)k * N + n] * (double)params[offW + (int64_t)k * N + n];
+                grad[offS + n] = (float)(exp((double)params[offS + n]) * acc * scale);
+            }
+        }
+    }
+}
+
+__global__ void k_write_scalar_grads(const double* __restrict__ partP, int nblk, const int64_t* offs,
+                                     int naxes, float scale, float* __restrict__ grad,
+                                     const double* __restrict__ loss_part, int nloss_blk,
+                                     const double* inv_n, double* __restrict__ losses_out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        for (int ax = 0; ax < naxes; ++ax) {
+            if (offs[ax] < 0) continue;
+            double s = 0.0;
+            for (int b = 0; b < nblk; ++b) s += partP[b * kMaxAxes + ax];
+            grad[offs[ax]] = (float)(s * scale);
+        }
+        if (losses_out) {
+            for (int t = 0; t < 3; ++t) {
+                double s = 0.0;
+                for (int b = 0; b < nloss_blk; ++b) s += loss_part[b * 3 + t];
+                losses_out[t] = s * inv_n[t];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Adam (optim.cpp:7-41) fused with the 1/W average (trainer.cpp:278-280)
+// ---------------------------------------------------------------------------
+__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                       float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps,
+                       float bc1, float bc2, float gscale) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float gi = g[i] * gscale;
+        const float mi = b1 * m[i] + (1.0f - b1) * gi;
+        const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        p[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    }
+}
+
+__global__ void k_f64_to_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (float)a[i];
+}
+
+__global__ void k_any_nonfinite(const float* __restrict__ g, int64_t n, int* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(g[i])) atomicMin(flag, (int)i);
+}
+
+}  // namespace pnx

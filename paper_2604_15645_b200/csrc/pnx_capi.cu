@@ -1,0 +1,934 @@
+// pnx_capi.cu -- C ABI (include/pnx.h) and host orchestration of one worker
+// step on one B200. Replaces run_worker_epoch's graph build + nested reverse
+// sweeps (trainer.cpp:200-262) with a chunked pass of jet kernels:
+//
+//   prep -> [per chunk: input -> L fwd GEMMs -> head -> L rev GEMMs + dW]
+//        -> fixed-order reductions -> flat gradient (trainable() order)
+//
+// Rows of a step are laid out [bc_a | bc_b | ic | interior]; the small
+// replicated IC/BC sets (trainer.cpp:225-232) ride in the first chunk and carry
+// value-only seeds, interior rows carry residual seeds (losses.cpp:77-95).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pnx.h"
+#include "kernels_simt.cuh"
+#include "tc_gemm.cuh"
+
+using namespace pnx;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+}  // namespace
+
+struct pnx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    int engine = PNX_ENGINE_AUTO;
+
+    // model (ModelSpec)
+    int in_dim = 0, H = 0, depth = 0, F = 0, act = 0;
+    float w0 = 1.0f;
+    bool rwf = false;
+    int rff_w = 0, E = 0, K0 = 0;
+    int periodic[kMaxAxes] = {0, 0, 0, 0};
+    double period[kMaxAxes] = {0, 0, 0, 0};
+    int64_t period_off[kMaxAxes] = {-1, -1, -1, -1};
+    bool train_period = false;
+    // problem
+    int pde = 0, bc = 0, layout = 0, S = 1, Kres = 1;
+    PdeConst pc{};
+    // params
+    int64_t P = 0;
+    LayerTab tab{};
+    int64_t wsize = 0, bsize = 0;
+
+    // collocation (global rows: [bc_a | bc_b | ic | interior])
+    int64_t n_bca = 0, n_bcb = 0, n_ic = 0, n_int = 0;
+    std::vector<double> h_int, h_ic, h_bca, h_bcb;  // axis-major host copies
+    std::vector<float> h_ic_t, h_bc_t;
+    bool rows_dirty = true;
+    double* d_coords = nullptr;
+    int64_t ld = 0, coords_cap = 0, layout_T = -1, layout_chunk_override = -1;
+    float *d_ic_t = nullptr, *d_bc_t = nullptr;
+    double* d_rffB = nullptr;
+
+    // weights / grads
+    float *d_W = nullptr, *d_Wt = nullptr, *d_bias = nullptr;
+    float *d_params = nullptr, *d_grad = nullptr;
+    double* d_losses = nullptr;
+
+    // activations
+    int64_t chunk_rows = 0, chunk_override = 0, Rcap = 0;
+    float *d_Hin = nullptr, *d_Hinb = nullptr;
+    std::vector<float*> d_Z;
+    float* d_Zb[2] = {nullptr, nullptr};
+    // partials
+    std::vector<double*> d_part;
+    std::vector<int> nsplit;
+    double* d_head_part = nullptr;
+    int head_grid = 296;
+    double* d_loss_part = nullptr;
+    double* d_partP = nullptr;
+    int ibwd_grid = 148;
+    double* d_red = nullptr;
+    float* d_bc_vals = nullptr;
+    int* d_bad = nullptr;
+    float* d_resid = nullptr;
+    bool capture_resid = false;
+    TcWorkspace tc{};
+    // kernel-class timing with CUDA events on the launching stream (bench roofline)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<int> ev_cls;  // class per recorded pair
+    size_t ev_used = 0;
+    double prof_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t prof_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+
+namespace {
+
+int fail(pnx_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+#define CK(call)                                                                     \
+    do {                                                                             \
+        cudaError_t e_ = (call);                                                     \
+        if (e_ != cudaSuccess)                                                       \
+            return fail(ctx, PNX_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CKL()                                                                        \
+    do {                                                                             \
+        ++ctx->launches;                                                             \
+        cudaError_t e_ = cudaGetLastError();                                         \
+        if (e_ != cudaSuccess)                                                       \
+            return fail(ctx, PNX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+int dalloc(pnx_ctx* ctx, T** p, size_t n) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    if (n == 0) return PNX_OK;
+    CK(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+    return PNX_OK;
+}
+
+enum ProfClass { PC_INPUT = 0, PC_FWD = 1, PC_HEAD = 2, PC_BWD = 3, PC_WGRAD = 4, PC_FINAL = 5 };
+
+// Record an event before a kernel of class `cls`; returns the pair index.
+void prof_begin(pnx_ctx* c, int cls, cudaStream_t st) {
+    if (!c->prof) return;
+    if (c->ev_used + 2 > c->ev_pool.size()) {
+        for (int i = 0; i < 64; ++i) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            c->ev_pool.push_back(e);
+        }
+    }
+    cudaEventRecord(c->ev_pool[c->ev_used], st);
+    c->ev_cls.push_back(cls);
+}
+void prof_end(pnx_ctx* c, cudaStream_t st) {
+    if (!c->prof) return;
+    cudaEventRecord(c->ev_pool[c->ev_used + 1], st);
+    c->ev_used += 2;
+}
+void prof_collect(pnx_ctx* c) {
+    for (size_t i = 0; i < c->ev_cls.size(); ++i) {
+        float ms = 0.0f;
+        cudaEventSynchronize(c->ev_pool[2 * i + 1]);
+        cudaEventElapsedTime(&ms, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]);
+        c->prof_ms[c->ev_cls[i]] += ms;
+        c->prof_n[c->ev_cls[i]] += 1;
+    }
+    c->ev_cls.clear();
+    c->ev_used = 0;
+}
+
+int pde_layout(int pde) {
+    switch (pde) {
+        case PNX_PDE_ADVECTION:
+        case PNX_PDE_BURGERS: return LAY_XT;
+        case PNX_PDE_ALLEN_CAHN: return LAY_AC;
+        case PNX_PDE_MAXWELL_TE: return LAY_MX;
+        case PNX_PDE_NS_STEADY: return LAY_NS;
+    }
+    return -1;
+}
+
+// ---- template dispatch -----------------------------------------------------
+
+template <int L>
+void launch_input_t(const InputArgs& a, cudaStream_t st) {
+    const int per_row = a.rff_w > 0 ? a.rff_w : 1;
+    const int64_t total = (int64_t)a.Rpad * per_row;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    k_input<L><<<grid, 256, 0, st>>>(a);
+}
+void launch_input(int L, const InputArgs& a, cudaStream_t st) {
+    switch (L) {
+        case LAY_XT: launch_input_t<LAY_XT>(a, st); break;
+        case LAY_AC: launch_input_t<LAY_AC>(a, st); break;
+        case LAY_MX: launch_input_t<LAY_MX>(a, st); break;
+        case LAY_NS: launch_input_t<LAY_NS>(a, st); break;
+    }
+}
+void launch_input_bwd(int L, const InputArgs& a, const float* Hb, double* partP, int grid, cudaStream_t st) {
+    switch (L) {
+        case LAY_XT: k_input_bwd<LAY_XT><<<grid, 256, 0, st>>>(a, Hb, partP); break;
+        case LAY_AC: k_input_bwd<LAY_AC><<<grid, 256, 0, st>>>(a, Hb, partP); break;
+        case LAY_MX: k_input_bwd<LAY_MX><<<grid, 256, 0, st>>>(a, Hb, partP); break;
+        case LAY_NS: k_input_bwd<LAY_NS><<<grid, 256, 0, st>>>(a, Hb, partP); break;
+    }
+}
+
+template <int L, int PRO, int EPI>
+void launch_gemm_e(int eact, const GemmArgs& g, dim3 grid, cudaStream_t st) {
+    switch (eact) {
+        case ACT_TANH: k_gemm<L, PRO, EPI, ACT_TANH><<<grid, 256, 0, st>>>(g); break;
+        case ACT_SINE: k_gemm<L, PRO, EPI, ACT_SINE><<<grid, 256, 0, st>>>(g); break;
+        case ACT_SWISH: k_gemm<L, PRO, EPI, ACT_SWISH><<<grid, 256, 0, st>>>(g); break;
+        default: k_gemm<L, PRO, EPI, ACT_NONE><<<grid, 256, 0, st>>>(g); break;
+    }
+}
+template <int L, int PRO>
+void launch_gemm_p(int epi, int eact, const GemmArgs& g, dim3 grid, cudaStream_t st) {
+    switch (epi) {
+        case EPI_BIAS: k_gemm<L, PRO, EPI_BIAS, ACT_NONE><<<grid, 256, 0, st>>>(g); break;
+        case EPI_RAW: k_gemm<L, PRO, EPI_RAW, ACT_NONE><<<grid, 256, 0, st>>>(g); break;
+        default: launch_gemm_e<L, PRO, EPI_ACTT>(eact, g, grid, st); break;
+    }
+}
+template <int L>
+void launch_gemm_l(int pro, int epi, int eact, const GemmArgs& g, dim3 grid, cudaStream_t st) {
+    switch (pro) {
+        case ACT_TANH: launch_gemm_p<L, ACT_TANH>(epi, eact, g, grid, st); break;
+        case ACT_SINE: launch_gemm_p<L, ACT_SINE>(epi, eact, g, grid, st); break;
+        case ACT_SWISH: launch_gemm_p<L, ACT_SWISH>(epi, eact, g, grid, st); break;
+        default: launch_gemm_p<L, ACT_NONE>(epi, eact, g, grid, st); break;
+    }
+}
+void launch_gemm(int L, int pro, int epi, int eact, const GemmArgs& g, cudaStream_t st) {
+    dim3 grid((unsigned)(g.Rpad / GT_M), (unsigned)((g.N + GT_N - 1) / GT_N));
+    switch (L) {
+        case LAY_XT: launch_gemm_l<LAY_XT>(pro, epi, eact, g, grid, st); break;
+        case LAY_AC: launch_gemm_l<LAY_AC>(pro, epi, eact, g, grid, st); break;
+        case LAY_MX: launch_gemm_l<LAY_MX>(pro, epi, eact, g, grid, st); break;
+        case LAY_NS: launch_gemm_l<LAY_NS>(pro, epi, eact, g, grid, st); break;
+    }
+}
+
+template <int L>
+void launch_wgrad_l(int pro, const WgradArgs& w, dim3 grid, cudaStream_t st) {
+    switch (pro) {
+        case ACT_TANH: k_wgrad<L, ACT_TANH><<<grid, 256, 0, st>>>(w); break;
+        case ACT_SINE: k_wgrad<L, ACT_SINE><<<grid, 256, 0, st>>>(w); break;
+        case ACT_SWISH: k_wgrad<L, ACT_SWISH><<<grid, 256, 0, st>>>(w); break;
+        default: k_wgrad<L, ACT_NONE><<<grid, 256, 0, st>>>(w); break;
+    }
+}
+void launch_wgrad(int L, int pro, const WgradArgs& w, int nsplit, cudaStream_t st) {
+    dim3 grid((unsigned)((w.N + 63) / 64), (unsigned)((w.K + 63) / 64), (unsigned)nsplit);
+    switch (L) {
+        case LAY_XT: launch_wgrad_l<LAY_XT>(pro, w, grid, st); break;
+        case LAY_AC: launch_wgrad_l<LAY_AC>(pro, w, grid, st); break;
+        case LAY_MX: launch_wgrad_l<LAY_MX>(pro, w, grid, st); break;
+        case LAY_NS: launch_wgrad_l<LAY_NS>(pro, w, grid, st); break;
+    }
+}
+
+template <int P, int J>
+void launch_head_j(int act, const HeadArgs& h, int grid, cudaStream_t st) {
+    switch (act) {
+        case ACT_TANH: k_head<P, ACT_TANH, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
+        case ACT_SINE: k_head<P, ACT_SINE, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
+        default: k_head<P, ACT_SWISH, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
+    }
+}
+template <int P>
+void launch_head_p(int act, const HeadArgs& h, int grid, cudaStream_t st) {
+    if (h.H <= 32) launch_head_j<P, 1>(act, h, grid, st);
+    else if (h.H <= 64) launch_head_j<P, 2>(act, h, grid, st);
+    else if (h.H <= 128) launch_head_j<P, 4>(act, h, grid, st);
+    else if (h.H <= 256) launch_head_j<P, 8>(act, h, grid, st);
+    else launch_head_j<P, 16>(act, h, grid, st);
+}
+void launch_head(int pde, int act, const HeadArgs& h, int grid, cudaStream_t st) {
+    switch (pde) {
+        case PDE_ADVECTION: launch_head_p<PDE_ADVECTION>(act, h, grid, st); break;
+        case PDE_ALLEN_CAHN: launch_head_p<PDE_ALLEN_CAHN>(act, h, grid, st); break;
+        case PDE_BURGERS: launch_head_p<PDE_BURGERS>(act, h, grid, st); break;
+        case PDE_MAXWELL: launch_head_p<PDE_MAXWELL>(act, h, grid, st); break;
+        case PDE_NS: launch_head_p<PDE_NS>(act, h, grid, st); break;
+    }
+}
+
+// ---- buffers ---------------------------------------------------------------
+
+int64_t bytes_per_row(const pnx_ctx* c) {
+    int64_t f = (int64_t)c->S * (c->K0 + (int64_t)c->depth * c->H + 2LL * c->H + (c->train_period ? c->K0 : 0));
+    return f * 4;
+}
+
+int upload_rows(pnx_ctx* ctx) {
+    const int d = ctx->in_dim;
+    const int64_t T = ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_int;
+    ctx->ld = T;
+    std::vector<double> all((size_t)(d * T));
+    auto put = [&](const std::vector<double>& src, int64_t n, int64_t at) {
+        for (int a = 0; a < d; ++a)
+            for (int64_t i = 0; i < n; ++i) all[(size_t)(a * T + at + i)] = src[(size_t)(a * n + i)];
+    };
+    put(ctx->h_bca, ctx->n_bca, 0);
+    put(ctx->h_bcb, ctx->n_bcb, ctx->n_bca);
+    put(ctx->h_ic, ctx->n_ic, ctx->n_bca + ctx->n_bcb);
+    put(ctx->h_int, ctx->n_int, ctx->n_bca + ctx->n_bcb + ctx->n_ic);
+    if ((int64_t)all.size() > ctx->coords_cap) {
+        if (int r = dalloc(ctx, &ctx->d_coords, all.size())) return r;
+        ctx->coords_cap = (int64_t)all.size();
+    }
+    CK(cudaMemcpy(ctx->d_coords, all.data(), all.size() * 8, cudaMemcpyHostToDevice));
+    if (int r = dalloc(ctx, &ctx->d_ic_t, ctx->h_ic_t.size())) return r;
+    if (!ctx->h_ic_t.empty())
+        CK(cudaMemcpy(ctx->d_ic_t, ctx->h_ic_t.data(), ctx->h_ic_t.size() * 4, cudaMemcpyHostToDevice));
+    if (int r = dalloc(ctx, &ctx->d_bc_t, ctx->h_bc_t.size())) return r;
+    if (!ctx->h_bc_t.empty())
+        CK(cudaMemcpy(ctx->d_bc_t, ctx->h_bc_t.data(), ctx->h_bc_t.size() * 4, cudaMemcpyHostToDevice));
+    if (int r = dalloc(ctx, &ctx->d_bc_vals, (size_t)std::max<int64_t>(1, ctx->n_bca + ctx->n_bcb) * ctx->F)) return r;
+
+    if (T == ctx->layout_T && ctx->chunk_override == ctx->layout_chunk_override) {
+        ctx->rows_dirty = false;
+        return PNX_OK;  // same row count: keep chunking, activations and partials
+    }
+    ctx->layout_T = T;
+    ctx->layout_chunk_override = ctx->chunk_override;
+    // chunking: all small rows in chunk 0
+    const int64_t small = ctx->n_bca + ctx->n_bcb + ctx->n_ic;
+    int64_t ch = ctx->chunk_override;
+    if (ch <= 0) {
+        const int64_t budget = 48LL << 30;  // bytes of per-chunk activations
+        ch = std::max<int64_t>(65536, budget / std::max<int64_t>(1, bytes_per_row(ctx)));
+    }
+    ch = std::max<int64_t>(ch, small + 64);
+    ch = std::min<int64_t>(ch, T);
+    ctx->chunk_rows = ch;
+    const int64_t Rp = roundup(ch, 64);
+    if (Rp > ctx->Rcap) {
+        ctx->Rcap = Rp;
+        const size_t SR = (size_t)ctx->S * Rp;
+        if (int r = dalloc(ctx, &ctx->d_Hin, SR * ctx->K0)) return r;
+        if (ctx->train_period)
+            if (int r = dalloc(ctx, &ctx->d_Hinb, SR * ctx->K0)) return r;
+        ctx->d_Z.assign(ctx->depth, nullptr);
+        for (int l = 0; l < ctx->depth; ++l)
+            if (int r = dalloc(ctx, &ctx->d_Z[l], SR * ctx->H)) return r;
+        for (int i = 0; i < 2; ++i)
+            if (int r = dalloc(ctx, &ctx->d_Zb[i], SR * ctx->H)) return r;
+        CK(cudaMemset(ctx->d_Hin, 0, SR * ctx->K0 * 4));
+        if (int r = tc_workspace_alloc(ctx->tc, (int)ctx->S, Rp, ctx->H, ctx->K0)) return fail(ctx, r, "tc workspace alloc");
+    }
+    // wgrad splits per layer (fill ~4 waves of 148 SMs)
+    const int L = ctx->tab.n;
+    ctx->d_part.resize(L, nullptr);
+    ctx->nsplit.assign(L, 1);
+    for (int l = 0; l < L - 1; ++l) {
+        const int tiles = (int)(((ctx->tab.N[l] + 63) / 64) * ((ctx->tab.K[l] + 63) / 64));
+        int ns = std::max(1, std::min(256, (4 * 148 + tiles - 1) / tiles));
+        ns = (int)std::min<int64_t>(ns, std::max<int64_t>(1, ch / 256));
+        ctx->nsplit[l] = ns;
+        if (int r = dalloc(ctx, &ctx->d_part[l], (size_t)ns * (ctx->tab.K[l] * (size_t)ctx->tab.N[l] + ctx->tab.N[l]))) return r;
+    }
+    ctx->rows_dirty = false;
+    return PNX_OK;
+}
+
+int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_grad, double* d_losses,
+             cudaStream_t st) {
+    if (ctx->n_int <= 0) return fail(ctx, PNX_ERR_STATE, "pnx_step: no interior points (call pnx_set_points)");
+    if (ctx->rows_dirty)
+        if (int r = upload_rows(ctx)) return r;
+    ctx->launches = 0;
+    const LayerTab& t = ctx->tab;
+    const int Lw = t.n;  // linear layers
+    const int S = ctx->S;
+    const int L = ctx->layout;
+    const int act = ctx->act;
+
+    {
+        dim3 grid(64, Lw);
+        k_prep<<<grid, 256, 0, st>>>(d_params, t, ctx->d_W, ctx->d_Wt, ctx->d_bias);
+        CKL();
+    }
+    for (int l = 0; l < Lw - 1; ++l)
+        CK(cudaMemsetAsync(ctx->d_part[l], 0,
+                           (size_t)ctx->nsplit[l] * (t.K[l] * (size_t)t.N[l] + t.N[l]) * 8, st));
+    CK(cudaMemsetAsync(ctx->d_head_part, 0, (size_t)ctx->head_grid * (ctx->H * ctx->F + ctx->F) * 8, st));
+    CK(cudaMemsetAsync(ctx->d_loss_part, 0, (size_t)ctx->head_grid * 3 * 8, st));
+    CK(cudaMemsetAsync(ctx->d_partP, 0, (size_t)ctx->ibwd_grid * kMaxAxes * 8, st));
+    CK(cudaMemsetAsync(ctx->d_bad, 0x7f, 3 * sizeof(int), st));
+
+    const int64_t T = ctx->ld;
+    const int64_t bca0 = 0, bca1 = ctx->n_bca, bcb0 = bca1, bcb1 = bcb0 + ctx->n_bcb;
+    const int64_t ic0 = bcb1, ic1 = ic0 + ctx->n_ic, int0 = ic1, int1 = int0 + ctx->n_int;
+
+    InputArgs ia{};
+    ia.coords = ctx->d_coords;
+    ia.ld = T;
+    ia.in_dim = ctx->in_dim;
+    for (int a = 0; a < kMaxAxes; ++a) {
+        ia.periodic[a] = ctx->periodic[a];
+        ia.period[a] = ctx->period[a];
+        ia.period_off[a] = ctx->period_off[a];
+    }
+    ia.params = d_params;
+    ia.E = ctx->E;
+    ia.rff_w = ctx->rff_w;
+    ia.rffB = ctx->d_rffB;
+    ia.K0 = ctx->K0;
+    ia.Hin = ctx->d_Hin;
+
+    const bool use_tc = tc_enabled(ctx->engine, ctx->H, S);
+
+    for (int64_t c0 = 0; c0 < T; c0 += ctx->chunk_rows) {
+        const int nrows = (int)std::min<int64_t>(ctx->chunk_rows, T - c0);
+        const int Rpad = (int)roundup(nrows, 64);
+        ia.row0 = c0;
+        ia.nrows = nrows;
+        ia.Rpad = Rpad;
+        prof_begin(ctx, PC_INPUT, st);
+        launch_input(L, ia, st);
+        prof_end(ctx, st);
+        CKL();
+        // forward layers
+        for (int l = 0; l < ctx->depth; ++l) {
+            GemmArgs g{};
+            g.A = l == 0 ? ctx->d_Hin : ctx->d_Z[l - 1];
+            g.B = ctx->d_W + t.dW[l];
+            g.bias = ctx->d_bias + t.dB[l];
+            g.out = ctx->d_Z[l];
+            g.Rpad = Rpad;
+            g.K = t.K[l];
+            g.N = t.N[l];
+            g.w0 = ctx->w0;
+            const int pro = l == 0 ? ACT_NONE : act;
+            prof_begin(ctx, PC_FWD, st);
+            if (use_tc && l > 0) {
+                if (int r = tc_forward(ctx->tc, L, pro, g, st, &ctx->launches)) return fail(ctx, PNX_ERR_CUDA, "tc_forward failed");
+            } else {
+                launch_gemm(L, pro, EPI_BIAS, ACT_NONE, g, st);
+                CKL();
+            }
+            prof_end(ctx, st);
+        }
+        // head
+        HeadArgs h{};
+        h.Z = ctx->d_Z[ctx->depth - 1];
+        h.Zb = ctx->d_Zb[0];
+        h.W = ctx->d_W + t.dW[Lw - 1];
+        h.b = ctx->d_bias + t.dB[Lw - 1];
+        h.H = ctx->H;
+        h.Rpad = Rpad;
+        h.nrows = nrows;
+        h.row0 = c0;
+        h.bca0 = bca0; h.bca1 = bca1; h.bcb0 = bcb0; h.bcb1 = bcb1;
+        h.ic0 = ic0; h.ic1 = ic1; h.int0 = int0; h.int1 = int1;
+        h.bc_mode = ctx->bc;
+        h.ic_t = ctx->d_ic_t;
+        h.bc_t = ctx->d_bc_t;
+        h.bc_vals = ctx->d_bc_vals;
+        h.w_pde = (float)(2.0 * lam[0] / (double)ctx->n_int);
+        h.w_ic = ctx->n_ic ? (float)(2.0 * lam[1] / (double)ctx->n_ic) : 0.0f;
+        h.w_bc = ctx->n_bca ? (float)(2.0 * lam[2] / (double)ctx->n_bca) : 0.0f;
+        h.pc = ctx->pc;
+        h.w0 = ctx->w0;
+        h.loss_part = ctx->d_loss_part;
+        h.head_part = ctx->d_head_part;
+        h.bad = ctx->d_bad;
+        h.resid_out = ctx->capture_resid ? ctx->d_resid : nullptr;
+        if (ctx->bc == PNX_BC_SOFT_PERIODIC && c0 == 0) {
+            HeadArgs hv = h;
+            hv.values_only = 1;
+            hv.vals_out = ctx->d_bc_vals;
+            hv.nrows = (int)std::min<int64_t>(nrows, bcb1);
+            launch_head(ctx->pde, act, hv, ctx->head_grid, st);
+            CKL();
+        }
+        prof_begin(ctx, PC_HEAD, st);
+        launch_head(ctx->pde, act, h, ctx->head_grid, st);
+        prof_end(ctx, st);
+        CKL();
+        // reverse layers
+        int cur = 0;
+        for (int l = ctx->depth - 1; l >= 0; --l) {
+            WgradArgs w{};
+            w.A = l == 0 ? ctx->d_Hin : ctx->d_Z[l - 1];
+            w.Bm = ctx->d_Zb[cur];
+            w.part = ctx->d_part[l];
+            w.Rpad = Rpad;
+            w.nrows_valid = nrows;
+            w.K = t.K[l];
+            w.N = t.N[l];
+            w.rows_per_split = (int)roundup((nrows + ctx->nsplit[l] - 1) / ctx->nsplit[l], WT_R);
+            w.w0 = ctx->w0;
+            const int pro = l == 0 ? ACT_NONE : act;
+            prof_begin(ctx, PC_WGRAD, st);
+            if (use_tc && l > 0) {
+                if (int r = tc_wgrad(ctx->tc, L, pro, w, ctx->nsplit[l], st, &ctx->launches)) return fail(ctx, PNX_ERR_CUDA, "tc_wgrad failed");
+            } else {
+                launch_wgrad(L, pro, w, ctx->nsplit[l], st);
+                CKL();
+            }
+            prof_end(ctx, st);
+            if (l > 0 || ctx->train_period) {
+                GemmArgs g{};
+                g.A = ctx->d_Zb[cur];
+                g.B = ctx->d_Wt + t.dW[l];  // [N_l][K_l]
+                g.Rpad = Rpad;
+                g.K = t.N[l];
+                g.N = t.K[l];
+                g.w0 = ctx->w0;
+                if (l > 0) {
+                    g.Zlow = ctx->d_Z[l - 1];
+                    g.out = ctx->d_Zb[cur ^ 1];
+                    prof_begin(ctx, PC_BWD, st);
+                    if (use_tc) {
+                        if (int r = tc_backward(ctx->tc, L, act, g, st, &ctx->launches)) return fail(ctx, PNX_ERR_CUDA, "tc_backward failed");
+                    } else {
+                        launch_gemm(L, ACT_NONE, EPI_ACTT, act, g, st);
+                        CKL();
+                    }
+                    prof_end(ctx, st);
+                    cur ^= 1;
+                } else {
+                    g.out = ctx->d_Hinb;
+                    launch_gemm(L, ACT_NONE, EPI_RAW, ACT_NONE, g, st);
+                    CKL();
+                    launch_input_bwd(L, ia, ctx->d_Hinb, ctx->d_partP, ctx->ibwd_grid, st);
+                    CKL();
+                }
+            }
+        }
+    }
+    // finalize: fixed-order reductions, trainable() order
+    for (int l = 0; l < Lw; ++l) {
+        const double* part = l < Lw - 1 ? ctx->d_part[l] : ctx->d_head_part;
+        const int ns = l < Lw - 1 ? ctx->nsplit[l] : ctx->head_grid;
+        const int64_t len = (int64_t)t.K[l] * t.N[l] + t.N[l];
+        k_reduce_splits<<<(unsigned)std::min<int64_t>((len + 255) / 256, 1024), 256, 0, st>>>(part, ns, len, ctx->d_red);
+        CKL();
+        k_write_layer_grad<<<(unsigned)std::min<int64_t>((len + 255) / 256, 1024), 256, 0, st>>>(
+            ctx->d_red, d_params, t.K[l], t.N[l], t.offW[l], t.offS[l], t.offB[l], 1.0f, d_grad);
+        CKL();
+    }
+    {
+        double inv[3] = {1.0 / (double)ctx->n_int, ctx->n_ic ? 1.0 / (double)ctx->n_ic : 0.0,
+                         ctx->n_bca ? 1.0 / (double)ctx->n_bca : 0.0};
+        // small constant args via a device scratch (last 8 doubles of d_losses area)
+        CK(cudaMemcpyAsync(ctx->d_losses + 3, inv, sizeof(inv), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->d_losses + 8), ctx->period_off, sizeof(ctx->period_off),
+                           cudaMemcpyHostToDevice, st));
+        k_write_scalar_grads<<<1, 32, 0, st>>>(ctx->d_partP, ctx->ibwd_grid,
+                                               reinterpret_cast<const int64_t*>(ctx->d_losses + 8), ctx->in_dim,
+                                               1.0f, d_grad, ctx->d_loss_part, ctx->head_grid, ctx->d_losses + 3,
+                                               d_losses ? d_losses : ctx->d_losses);
+        CKL();
+    }
+    return PNX_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* pnx_create_error(void) { return g_create_error.c_str(); }
+
+int pnx_create(const pnx_model_desc* m, const pnx_problem_desc* p, int device, pnx_ctx** out) {
+    g_create_error.clear();
+    if (!m || !p || !out) {
+        g_create_error = "pnx_create: null argument";
+        return PNX_ERR_ARG;
+    }
+    *out = nullptr;
+    // ModelSpec::validate (model.cpp:25-33)
+    if (m->in_dim <= 0 || m->hidden_dim <= 0 || m->depth <= 0 || m->out_dim <= 0) {
+        g_create_error = "ModelSpec: dimensions must be positive";
+        return PNX_ERR_ARG;
+    }
+    if (m->n_periodic_axes != 0 && m->n_periodic_axes != m->in_dim) {
+        g_create_error = "ModelSpec: periodic_axes must have one entry per input axis";
+        return PNX_ERR_ARG;
+    }
+    if (m->in_dim > kMaxAxes || m->depth + 1 > kMaxLayers) {
+        g_create_error = "pnx_create: in_dim <= 4 and depth <= 15 supported";
+        return PNX_ERR_ARG;
+    }
+    if (m->hidden_dim > 512) {
+        g_create_error = "pnx_create: hidden_dim <= 512 supported";
+        return PNX_ERR_ARG;
+    }
+    const int layout = pde_layout(p->pde);
+    if (layout < 0) {
+        g_create_error = "unknown pde";
+        return PNX_ERR_ARG;
+    }
+    const int fields = (p->pde == PNX_PDE_MAXWELL_TE || p->pde == PNX_PDE_NS_STEADY) ? 3 : 1;
+    const int coords = (p->pde == PNX_PDE_MAXWELL_TE) ? 3 : 2;
+    if (m->out_dim != fields) {  // losses.cpp:31-32
+        g_create_error = "residual: model field count does not match the equation";
+        return PNX_ERR_ARG;
+    }
+    if (m->in_dim != coords) {  // losses.cpp:29-30
+        g_create_error = "residual: coordinate count mismatch";
+        return PNX_ERR_ARG;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        g_create_error = "pnx_create: no CUDA device (the B200 path has no CPU fallback)";
+        return PNX_ERR_CUDA;
+    }
+    if (device < 0 || device >= ndev) {
+        g_create_error = "pnx_create: bad device index";
+        return PNX_ERR_ARG;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) {
+        g_create_error = "pnx_create: cudaSetDevice failed";
+        return PNX_ERR_CUDA;
+    }
+    pnx_ctx* ctx = new pnx_ctx();
+    ctx->device = device;
+    ctx->in_dim = m->in_dim;
+    ctx->H = m->hidden_dim;
+    ctx->depth = m->depth;
+    ctx->F = m->out_dim;
+    ctx->act = m->activation;
+    ctx->w0 = (float)m->sine_w0;
+    ctx->rwf = m->rwf != 0;
+    ctx->rff_w = m->rff_width;
+    int E = 0;
+    for (int a = 0; a < m->in_dim; ++a) {
+        const bool per = m->n_periodic_axes && m->periodic[a];
+        ctx->periodic[a] = per;
+        if (per) {
+            if (!(m->period[a] > 0.0)) {
+                g_create_error = "ModelSpec: periodic axis needs a positive period";
+                delete ctx;
+                return PNX_ERR_ARG;
+            }
+            ctx->period[a] = m->period[a];
+        }
+        E += per ? 2 : 1;
+    }
+    ctx->E = E;
+    ctx->K0 = ctx->rff_w > 0 ? 2 * ctx->rff_w : E;
+    ctx->pde = p->pde;
+    ctx->bc = p->bc;
+    ctx->layout = layout;
+    ctx->pc.c = (float)p->advection_c;
+    ctx->pc.eps = (float)p->epsilon;
+    ctx->pc.mu = (float)p->mu;
+    ctx->pc.inv_re = p->reynolds > 0 ? (float)(1.0 / p->reynolds) : 0.0f;
+    switch (layout) {
+        case LAY_XT: ctx->S = 3; break;
+        case LAY_AC: ctx->S = 4; break;
+        case LAY_MX: ctx->S = 4; break;
+        case LAY_NS: ctx->S = 5; break;
+    }
+    ctx->Kres = fields;
+    // parameter layout (model.cpp:64-101)
+    LayerTab& t = ctx->tab;
+    t.n = m->depth + 1;
+    int64_t off = 0, dw = 0, db = 0;
+    for (int l = 0; l < t.n; ++l) {
+        const int K = l == 0 ? ctx->K0 : ctx->H;
+        const int N = l == m->depth ? ctx->F : ctx->H;
+        t.K[l] = K;
+        t.N[l] = N;
+        t.offW[l] = off;
+        off += (int64_t)K * N;
+        if (ctx->rwf) {
+            t.offS[l] = off;
+            off += N;
+        } else {
+            t.offS[l] = -1;
+        }
+        t.offB[l] = off;
+        off += N;
+        t.dW[l] = dw;
+        dw += (int64_t)K * N;
+        t.dB[l] = db;
+        db += N;
+    }
+    for (int a = 0; a < m->in_dim; ++a) {
+        if (ctx->periodic[a] && m->period_trainable && m->period_trainable[a]) {
+            ctx->period_off[a] = off++;
+            ctx->train_period = true;
+        }
+    }
+    ctx->P = off;
+    ctx->wsize = dw;
+    ctx->bsize = db;
+    int rc = PNX_OK;
+    cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if ((rc = dalloc(ctx, &ctx->d_W, dw)) || (rc = dalloc(ctx, &ctx->d_Wt, dw)) ||
+        (rc = dalloc(ctx, &ctx->d_bias, db)) || (rc = dalloc(ctx, &ctx->d_params, ctx->P)) ||
+        (rc = dalloc(ctx, &ctx->d_grad, ctx->P)) || (rc = dalloc(ctx, &ctx->d_losses, 16)) ||
+        (rc = dalloc(ctx, &ctx->d_head_part, (size_t)ctx->head_grid * (ctx->H * ctx->F + ctx->F))) ||
+        (rc = dalloc(ctx, &ctx->d_loss_part, (size_t)ctx->head_grid * 3)) ||
+        (rc = dalloc(ctx, &ctx->d_partP, (size_t)ctx->ibwd_grid * kMaxAxes)) ||
+        (rc = dalloc(ctx, &ctx->d_bad, 4))) {
+        g_create_error = ctx->err;
+        pnx_destroy(ctx);
+        return rc;
+    }
+    int64_t redmax = 0;
+    for (int l = 0; l < t.n; ++l) redmax = std::max<int64_t>(redmax, (int64_t)t.K[l] * t.N[l] + t.N[l]);
+    if ((rc = dalloc(ctx, &ctx->d_red, redmax))) {
+        g_create_error = ctx->err;
+        pnx_destroy(ctx);
+        return rc;
+    }
+    if (ctx->rff_w > 0) {
+        if (!m->rff_B) {
+            g_create_error = "pnx_create: rff_B required when rff_width > 0";
+            pnx_destroy(ctx);
+            return PNX_ERR_ARG;
+        }
+        const size_t nB = (size_t)E * ctx->rff_w;
+        if ((rc = dalloc(ctx, &ctx->d_rffB, nB)) ||
+            cudaMemcpy(ctx->d_rffB, m->rff_B, nB * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+            g_create_error = "pnx_create: rff_B upload failed";
+            pnx_destroy(ctx);
+            return PNX_ERR_CUDA;
+        }
+    }
+    *out = ctx;
+    return PNX_OK;
+}
+
+void pnx_destroy(pnx_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaFree(ctx->d_coords);
+    cudaFree(ctx->d_ic_t);
+    cudaFree(ctx->d_bc_t);
+    cudaFree(ctx->d_rffB);
+    cudaFree(ctx->d_W);
+    cudaFree(ctx->d_Wt);
+    cudaFree(ctx->d_bias);
+    cudaFree(ctx->d_params);
+    cudaFree(ctx->d_grad);
+    cudaFree(ctx->d_losses);
+    cudaFree(ctx->d_Hin);
+    cudaFree(ctx->d_Hinb);
+    for (float* z : ctx->d_Z) cudaFree(z);
+    cudaFree(ctx->d_Zb[0]);
+    cudaFree(ctx->d_Zb[1]);
+    for (double* p : ctx->d_part) cudaFree(p);
+    cudaFree(ctx->d_head_part);
+    cudaFree(ctx->d_loss_part);
+    cudaFree(ctx->d_partP);
+    cudaFree(ctx->d_red);
+    cudaFree(ctx->d_bc_vals);
+    cudaFree(ctx->d_bad);
+    cudaFree(ctx->d_resid);
+    tc_workspace_free(ctx->tc);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* pnx_last_error(const pnx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int pnx_param_count(const pnx_ctx* ctx, int64_t* n) {
+    if (!ctx || !n) return PNX_ERR_ARG;
+    *n = ctx->P;
+    return PNX_OK;
+}
+
+int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes) {
+    if (!ctx) return PNX_ERR_ARG;
+    if (n_axes != ctx->in_dim) return fail(ctx, PNX_ERR_ARG, "residual: coordinate count mismatch");
+    if (n <= 0 || !coords) return fail(ctx, PNX_ERR_ARG, "residual_loss: empty point set");
+    ctx->h_int.assign(coords, coords + n * n_axes);
+    ctx->n_int = n;
+    ctx->rows_dirty = true;
+    cudaSetDevice(ctx->device);
+    if (int r = dalloc(ctx, &ctx->d_resid, (size_t)n * ctx->Kres)) return r;
+    return PNX_OK;
+}
+
+int pnx_set_ic(pnx_ctx* ctx, const double* coords, const double* targets, int64_t n) {
+    if (!ctx) return PNX_ERR_ARG;
+    if (n < 0 || (n > 0 && (!coords || !targets))) return fail(ctx, PNX_ERR_ARG, "ic_loss: empty point set");
+    ctx->h_ic.assign(coords, coords + n * ctx->in_dim);
+    ctx->h_ic_t.resize((size_t)(n * ctx->F));
+    for (int64_t i = 0; i < n * ctx->F; ++i) ctx->h_ic_t[(size_t)i] = (float)targets[i];
+    ctx->n_ic = n;
+    ctx->rows_dirty = true;
+    return PNX_OK;
+}
+
+int pnx_set_bc(pnx_ctx* ctx, const double* a, const double* b, const double* targets, int64_t n) {
+    if (!ctx) return PNX_ERR_ARG;
+    if (ctx->bc == PNX_BC_HARD) {
+        if (n != 0) return fail(ctx, PNX_ERR_ARG, "pnx_set_bc: problem has hard (architectural) BC");
+        return PNX_OK;
+    }
+    if (n <= 0 || !a) return fail(ctx, PNX_ERR_ARG, "bc_loss: empty point set");
+    ctx->h_bca.assign(a, a + n * ctx->in_dim);
+    ctx->n_bca = n;
+    if (ctx->bc == PNX_BC_SOFT_PERIODIC) {
+        if (!b) return fail(ctx, PNX_ERR_ARG, "bc_loss: boundary traces must pair up");
+        ctx->h_bcb.assign(b, b + n * ctx->in_dim);
+        ctx->n_bcb = n;
+        ctx->h_bc_t.clear();
+    } else {
+        if (!targets) return fail(ctx, PNX_ERR_ARG, "loss: field/target count mismatch");
+        ctx->h_bcb.clear();
+        ctx->n_bcb = 0;
+        ctx->h_bc_t.resize((size_t)(n * ctx->F));
+        for (int64_t i = 0; i < n * ctx->F; ++i) ctx->h_bc_t[(size_t)i] = (float)targets[i];
+    }
+    ctx->rows_dirty = true;
+    return PNX_OK;
+}
+
+int pnx_set_engine(pnx_ctx* ctx, int engine) {
+    if (!ctx || engine < 0 || engine > 2) return PNX_ERR_ARG;
+    ctx->engine = engine;
+    return PNX_OK;
+}
+
+int pnx_set_chunk_rows(pnx_ctx* ctx, int64_t rows) {
+    if (!ctx || rows < 0) return PNX_ERR_ARG;
+    ctx->chunk_override = rows;
+    ctx->rows_dirty = true;
+    return PNX_OK;
+}
+
+int pnx_profile(pnx_ctx* ctx, int on) {
+    if (!ctx) return PNX_ERR_ARG;
+    ctx->prof = on != 0;
+    prof_collect(ctx);
+    for (int i = 0; i < 8; ++i) {
+        ctx->prof_ms[i] = 0.0;
+        ctx->prof_n[i] = 0;
+    }
+    return PNX_OK;
+}
+
+int pnx_profile_read(pnx_ctx* ctx, double* ms, int64_t* counts, int n) {
+    if (!ctx || !ms || !counts || n <= 0) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    prof_collect(ctx);
+    for (int i = 0; i < n && i < 8; ++i) {
+        ms[i] = ctx->prof_ms[i];
+        counts[i] = ctx->prof_n[i];
+    }
+    return PNX_OK;
+}
+
+int pnx_last_launch_count(const pnx_ctx* ctx, int64_t* n) {
+    if (!ctx || !n) return PNX_ERR_ARG;
+    *n = ctx->launches;
+    return PNX_OK;
+}
+
+int pnx_step_device(pnx_ctx* ctx, const float* d_params, const double lambdas[3], float* d_grad,
+                    double* d_losses, void* stream) {
+    if (!ctx || !d_params || !d_grad || !lambdas) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    return run_step(ctx, d_params, lambdas, d_grad, d_losses, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pnx_check(pnx_ctx* ctx) {
+    if (!ctx) return PNX_ERR_ARG;
+    int bad[3];
+    CK(cudaMemcpy(bad, ctx->d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < ctx->Kres; ++k)
+        if (bad[k] != 0x7f7f7f7f)
+            return fail(ctx, PNX_ERR_NONFINITE,
+                        "residual_loss: non-finite residual at point index " + std::to_string(bad[k]));
+    return PNX_OK;
+}
+
+int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double* grad_out,
+             double losses_out[3]) {
+    if (!ctx || !params || !lambdas) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    std::vector<float> p32((size_t)ctx->P);
+    for (int64_t i = 0; i < ctx->P; ++i) p32[(size_t)i] = (float)params[i];
+    CK(cudaMemcpyAsync(ctx->d_params, p32.data(), p32.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (int r = run_step(ctx, ctx->d_params, lambdas, ctx->d_grad, ctx->d_losses, ctx->stream)) return r;
+    std::vector<float> g32((size_t)ctx->P);
+    double losses[3];
+    CK(cudaMemcpyAsync(g32.data(), ctx->d_grad, g32.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(losses, ctx->d_losses, sizeof(losses), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (int r = pnx_check(ctx)) return r;
+    for (int t = 0; t < 3; ++t)
+        if (!std::isfinite(losses[t])) return fail(ctx, PNX_ERR_NONFINITE, "non-finite loss in worker step");
+    if (grad_out)
+        for (int64_t i = 0; i < ctx->P; ++i) {
+            if (!std::isfinite(g32[(size_t)i]))
+                return fail(ctx, PNX_ERR_NONFINITE, "non-finite gradient entry " + std::to_string(i));
+            grad_out[i] = (double)g32[(size_t)i];
+        }
+    if (losses_out)
+        for (int t = 0; t < 3; ++t) losses_out[t] = losses[t];
+    return PNX_OK;
+}
+
+int pnx_adam_step_device(pnx_ctx* ctx, float* d_params, const float* d_grad, float* d_m, float* d_v,
+                         int64_t n, double lr, double beta1, double beta2, double eps, int64_t t,
+                         double grad_scale, void* stream) {
+    if (!ctx || !d_params || !d_grad || !d_m || !d_v || n <= 0 || t <= 0) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    const float bc1 = (float)(1.0 - std::pow(beta1, (double)t));
+    const float bc2 = (float)(1.0 - std::pow(beta2, (double)t));
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_adam<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        d_params, d_grad, d_m, d_v, n, (float)lr, (float)beta1, (float)beta2, (float)eps, bc1, bc2,
+        (float)grad_scale);
+    CKL();
+    return PNX_OK;
+}
+
+// Diagnostics (residual_components, losses.hpp:51-53): interior residuals of
+// the last pnx_step, component-major [K][n_int] float64.
+int pnx_capture_residuals(pnx_ctx* ctx, int on) {
+    if (!ctx) return PNX_ERR_ARG;
+    ctx->capture_resid = on != 0;
+    return PNX_OK;
+}
+
+int pnx_copy_residuals(pnx_ctx* ctx, double* out) {
+    if (!ctx || !out || !ctx->d_resid) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    std::vector<float> r((size_t)(ctx->n_int * ctx->Kres));
+    CK(cudaMemcpy(r.data(), ctx->d_resid, r.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < r.size(); ++i) out[i] = r[i];
+    return PNX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C ABI, libpnx.so) against the
+reference's golden vectors and the FP64 oracle.
+
+Tolerances (FP32 device arithmetic vs FP64 reference):
+  gradients  ||g - g_ref||_2 / ||g_ref||_2 <= GRAD_RTOL (north_star: ~1e-5)
+  losses     |l - l_ref| <= LOSS_RTOL * |l_ref| + 1e-12
+  residuals  max |r - r_ref| <= RES_ATOL * (1 + max |r_ref|)
+"""
+import numpy as np
+import pytest
+
+import golden_io as gi
+from oracle import pinn_oracle as po
+
+pytestmark = pytest.mark.gpu
+
+GRAD_RTOL = 1e-5
+LOSS_RTOL = 1e-5
+RES_ATOL = 1e-5
+
+
+def _pkg():
+    import paper_2604_15645_b200 as pk
+    return pk
+
+
+def _spec(case):
+    return _pkg().ModelSpec.from_json(case["model"])
+
+
+def _res(case):
+    p = case["pde"]
+    return _pkg().ResidualSpec(p["id"], p.get("advection_c", 1.0), p.get("epsilon", 1.0), p.get("mu", 1.0))
+
+
+def _col_args(g):
+    col = g["col"]
+    return dict(interior=col.interior, ic_points=col.ic_points, ic_targets=col.ic_targets,
+                bc_a=col.bc_a, bc_b=col.bc_b, bc_targets=col.bc_targets)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("engine", ["ffma", "auto"])
+@pytest.mark.parametrize("name", gi.CASE_NAMES)
+def test_golden_gradients_and_losses(name, engine):
+    pk = _pkg()
+    g = gi.load(name)
+    case = g["case"]
+    for w in g["meta"]["workers"]:
+        grad, losses = pk.data_parallel_gradient(_spec(case), _res(case), g["bc"], g["params"], g["rffB"],
+                                                 workers=w, engine=engine, **_col_args(g))
+        ref = g[f"grad_w{w}"]
+        assert rel_l2(grad, ref) <= GRAD_RTOL, (name, w, rel_l2(grad, ref))
+        for o, r in zip(losses, g["meta"]["worker_losses"][str(w)]):
+            for k in ("pde", "ic", "bc"):
+                assert abs(o[k] - r[k]) <= LOSS_RTOL * abs(r[k]) + 1e-12, (name, w, k, o[k], r[k])
+
+
+@pytest.mark.parametrize("name", gi.CASE_NAMES)
+def test_golden_residuals(name):
+    pk = _pkg()
+    g = gi.load(name)
+    case = g["case"]
+    a = _col_args(g)
+    w = pk.make_worker(_spec(case), _res(case), g["bc"], g["rffB"], **a)
+    w.capture_residuals(True)
+    w.step(g["params"])
+    r = w.residuals(len(a["interior"]))
+    ref = g["residuals"]
+    assert np.max(np.abs(r - ref)) <= RES_ATOL * (1.0 + np.max(np.abs(ref)))
+
+
+def _workload_case(cfg, dims):
+    """A BASELINE config's model at full width on a reduced grid, FP64 oracle
+    vs GPU (params from numpy init; the oracle is pinned to the reference)."""
+    pk = _pkg()
+    from paper_2604_15645_b200 import configs
+    wl = configs.get_config(cfg)
+    col = configs.collocation(wl, dims)
+    flat, rffB = pk.init_params(wl.spec, seed=1)
+    ospec = gi.spec_from_json(_spec_json(wl.spec))
+    ores = po.ResidualSpec(wl.res.id, wl.res.advection_c, wl.res.epsilon, wl.res.mu, wl.res.reynolds)
+    ocol = po.Collocation(col["interior"], col["ic_points"], col["ic_targets"], col["bc_a"], col["bc_b"],
+                          col["bc_targets"])
+    return wl, col, flat, rffB, ospec, ores, ocol
+
+
+def _spec_json(s):
+    import dataclasses
+    j = {"in_dim": s.in_dim, "hidden_dim": s.hidden_dim, "depth": s.depth, "out_dim": s.out_dim,
+         "activation": s.activation, "sine_w0": s.sine_w0}
+    if s.periodic_axes:
+        j["periodic_axes"] = [dataclasses.asdict(a) for a in s.periodic_axes]
+    if s.rff:
+        j["rff"] = dataclasses.asdict(s.rff)
+    if s.rwf:
+        j["rwf"] = dataclasses.asdict(s.rwf)
+    return j
+
+
+@pytest.mark.parametrize("engine", ["ffma", "auto"])
+@pytest.mark.parametrize("cfg,dims,workers", [
+    ("c1", [40, 30], 1), ("c1", [40, 30], 3),
+    ("c2", [32, 24], 1),
+    ("c3", [24, 20], 2),
+    ("c4", [12, 10, 8], 1), ("c4", [12, 10, 8], 4),
+])
+def test_config_shapes_vs_oracle(cfg, dims, workers, engine):
+    pk = _pkg()
+    wl, col, flat, rffB, ospec, ores, ocol = _workload_case(cfg, dims)
+    ref, outs = po.data_parallel_gradient(ospec, flat, rffB, ores, ocol, wl.bc, workers)
+    grad, losses = pk.data_parallel_gradient(wl.spec, wl.res, wl.bc, flat, rffB, workers=workers,
+                                             engine=engine, **col)
+    assert rel_l2(grad, ref) <= GRAD_RTOL, rel_l2(grad, ref)
+    for o, r in zip(losses, outs):
+        for k in ("pde", "ic", "bc"):
+            assert abs(o[k] - r[k]) <= LOSS_RTOL * abs(r[k]) + 1e-12
+
+
+def test_chunking_is_invisible():
+    """Rows split into several chunks (the 64M-point path) give the same step."""
+    pk = _pkg()
+    wl, col, flat, rffB, *_ = _workload_case("c4", [16, 16, 12])
+    w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, **col)
+    g1, l1 = w.step(flat)
+    w.set_chunk_rows(700)
+    g2, l2 = w.step(flat)
+    assert rel_l2(g2, g1) <= 1e-6
+    for k in l1:
+        assert abs(l1[k] - l2[k]) <= 1e-6 * abs(l1[k]) + 1e-12
+
+
+def test_step_is_deterministic():
+    pk = _pkg()
+    wl, col, flat, rffB, *_ = _workload_case("c1", [50, 40])
+    w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, **col)
+    g1, l1 = w.step(flat)
+    g2, l2 = w.step(flat)
+    assert np.array_equal(g1, g2) and l1 == l2
+
+
+def test_nonfinite_residual_reports_point_index():
+    """losses.cpp:86-90: TensorError naming the first bad point."""
+    pk = _pkg()
+    g = gi.load("burgers_tanh")
+    a = _col_args(g)
+    pts = a["interior"].copy()
+    pts[7, 0] = np.nan
+    a["interior"] = pts
+    w = pk.make_worker(_spec(g["case"]), _res(g["case"]), g["bc"], None, **a)
+    with pytest.raises(pk.TensorError, match="non-finite residual at point index 7"):
+        w.step(g["params"])
+
+
+def test_argument_errors_match_reference_text():
+    pk = _pkg()
+    with pytest.raises(pk.TensorError, match="field count does not match"):
+        pk.Worker(pk.ModelSpec(2, 8, 2, 3), pk.ResidualSpec("burgers"))
+    with pytest.raises(pk.TensorError, match="fewer interior points than workers"):
+        pk.shard_interior(3, 4)
+
+
+@pytest.mark.parametrize("name", gi.TRAJ_NAMES)
+def test_adam_trajectory_on_device(name):
+    """N device-Adam steps (pnx_adam_step_device) track the reference train()
+    loss trajectory (trainer.cpp:419-555, balancing off). Tolerance: 1e-3
+    relative per step (FP32 drift grows with N)."""
+    import torch
+    pk = _pkg()
+    g = gi.load(name)
+    case = g["case"]
+    t = case["train"]
+    W = case["workers"]
+    a = _col_args(g)
+    shards = pk.shard_interior(len(a["interior"]), W)
+    workers = []
+    for lo, hi in shards:
+        aa = dict(a, interior=a["interior"][lo:hi])
+        workers.append(pk.make_worker(_spec(case), _res(case), g["bc"], g["rffB"], **aa))
+    dev = torch.device("cuda:0")
+    p = torch.tensor(g["params"], dtype=torch.float32, device=dev)
+    m = torch.zeros_like(p)
+    v = torch.zeros_like(p)
+    grads = [torch.zeros_like(p) for _ in workers]
+    losses = [torch.zeros(3, dtype=torch.float64, device=dev) for _ in workers]
+    st = torch.cuda.current_stream().cuda_stream
+    metrics = g["metrics"]
+    for ep in range(t["epochs"]):
+        for w, gr, lo in zip(workers, grads, losses):
+            w.step_device(p, gr, losses=lo, stream=st)
+        gsum = torch.stack(grads).sum(0)
+        lr = t["lr"] * t["gamma"] ** ep
+        workers[0].adam_step_device(p, gsum, m, v, ep + 1, lr, grad_scale=1.0 / W, stream=st)
+        lm = torch.stack(losses).mean(0).cpu().numpy()
+        for k in range(3):
+            ref = metrics[ep, 1 + k]
+            assert abs(lm[k] - ref) <= 1e-3 * abs(ref) + 1e-9, (ep, k, lm[k], ref)
+    for w in workers:
+        w.check()

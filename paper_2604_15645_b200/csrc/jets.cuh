@@ -57,10 +57,15 @@ template <> struct Streams<LAY_NS> {
 
 enum Act : int { ACT_TANH = 0, ACT_SINE = 1, ACT_SWISH = 2, ACT_NONE = 3 };
 
-__device__ __forceinline__ float fast_tanh_acc(float z) {
-    // accurate tanh (the hardware tanh.approx has ~2^-11 error: too coarse for
-    // 1e-5 gradient parity)
-    return tanhf(z);
+// Storage convention of a hidden layer's jets Z[s]: for tanh layers the value
+// stream holds t = tanh(z0) (applied once, in the producing epilogue), the
+// other streams hold the pre-activation jets z_a, z_aa. Every consumer (next
+// layer's prologue, the reverse epilogue, the weight gradient, the head) needs
+// exactly t and z_a, z_aa. sine/swish layers store z0 itself.
+template <int ACT>
+__device__ __forceinline__ float store_value(float z0) {
+    if constexpr (ACT == ACT_TANH) return tanhf(z0);
+    return z0;
 }
 
 // h = act(z) on all S streams of one (point, feature) element.
@@ -72,7 +77,7 @@ __device__ __forceinline__ void act_fwd(const float* z, float* h, float w0) {
 #pragma unroll
         for (int s = 0; s < S; ++s) h[s] = z[s];
     } else if constexpr (ACT == ACT_TANH) {
-        const float t = fast_tanh_acc(z[0]);
+        const float t = z[0];  // stored as tanh(z0)
         const float d = 1.0f - t * t;
         h[0] = t;
 #pragma unroll
@@ -125,7 +130,7 @@ __device__ __forceinline__ void act_bwd(const float* z, const float* hb, float* 
 #pragma unroll
         for (int s = 0; s < S; ++s) zb[s] = hb[s];
     } else if constexpr (ACT == ACT_TANH) {
-        const float t = fast_tanh_acc(z[0]);
+        const float t = z[0];  // stored as tanh(z0)
         const float d = 1.0f - t * t;
         float tbar = hb[0], dbar = 0.0f;
 #pragma unroll

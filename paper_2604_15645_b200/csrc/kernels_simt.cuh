@@ -39,7 +39,7 @@ struct LayerTab {
     int64_t dB[kMaxLayers];      // offset into the bias arena
 };
 
-__global__ void k_prep(const float* __restrict__ params, LayerTab t, float* __restrict__ W,
+static __global__ void k_prep(const float* __restrict__ params, LayerTab t, float* __restrict__ W,
                        float* __restrict__ Wt, float* __restrict__ bias) {
     const int l = blockIdx.y;
     if (l >= t.n) return;
@@ -130,7 +130,7 @@ __device__ __forceinline__ void embed_row(const InputArgs& a, int64_t g, double 
 }
 
 template <int L>
-__global__ void k_input(InputArgs a) {
+static __global__ void k_input(InputArgs a) {
     using St = Streams<L>;
     constexpr int S = St::S;
     const int per_row = a.rff_w > 0 ? a.rff_w : 1;
@@ -195,7 +195,7 @@ __global__ void k_input(InputArgs a) {
 // features), back through RFF (B frozen) and the embedding to each trainable
 // period: d phi/dP = -phi/P, d kappa/dP = -kappa/P.
 template <int L>
-__global__ void k_input_bwd(InputArgs a, const float* __restrict__ Hb, double* __restrict__ partP) {
+static __global__ void k_input_bwd(InputArgs a, const float* __restrict__ Hb, double* __restrict__ partP) {
     using St = Streams<L>;
     constexpr int S = St::S;
     double accP[kMaxAxes] = {0.0, 0.0, 0.0, 0.0};
@@ -384,9 +384,10 @@ __global__ void __launch_bounds__(256) k_gemm(GemmArgs g) {
             const int n = n0 + tx * 4 + j;
             if (n >= g.N) continue;
             const int64_t o = (int64_t)r * g.N + n;
-            if constexpr (EPI == EPI_BIAS) {
+            if constexpr (EPI == EPI_BIAS) {  // EACT: activation of this layer's output
+                g.out[o] = store_value<EACT>(acc[0][i][j] + g.bias[n]);
 #pragma unroll
-                for (int s = 0; s < S; ++s) g.out[s * RN + o] = acc[s][i][j] + (s == 0 ? g.bias[n] : 0.0f);
+                for (int s = 1; s < S; ++s) g.out[s * RN + o] = acc[s][i][j];
             } else if constexpr (EPI == EPI_RAW) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) g.out[s * RN + o] = acc[s][i][j];
@@ -749,7 +750,7 @@ struct FinalArgs {
 };
 
 // reduce splits of layer l into dWscratch (double)
-__global__ void k_reduce_splits(const double* __restrict__ part, int nsplit, int64_t len,
+static __global__ void k_reduce_splits(const double* __restrict__ part, int nsplit, int64_t len,
                                 double* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -759,7 +760,7 @@ __global__ void k_reduce_splits(const double* __restrict__ part, int nsplit, int
 }
 
 // write layer l's flat grads from the reduced dW (K*N) + db (N)
-__global__ void k_write_layer_grad(const double* __restrict__ red, const float* __restrict__ params,
+static __global__ void k_write_layer_grad(const double* __restrict__ red, const float* __restrict__ params,
                                    int K, int N, int64_t offW, int64_t offS, int64_t offB, float scale,
                                    float* __restrict__ grad) {
     const int64_t total = (int64_t)K * N;
@@ -782,7 +783,7 @@ __global__ void k_write_layer_grad(const double* __restrict__ red, const float* 
     }
 }
 
-__global__ void k_write_scalar_grads(const double* __restrict__ partP, int nblk, const int64_t* offs,
+static __global__ void k_write_scalar_grads(const double* __restrict__ partP, int nblk, const int64_t* offs,
                                      int naxes, float scale, float* __restrict__ grad,
                                      const double* __restrict__ loss_part, int nloss_blk,
                                      const double* inv_n, double* __restrict__ losses_out) {
@@ -806,7 +807,7 @@ __global__ void k_write_scalar_grads(const double* __restrict__ partP, int nblk,
 // ---------------------------------------------------------------------------
 // Adam (optim.cpp:7-41) fused with the 1/W average (trainer.cpp:278-280)
 // ---------------------------------------------------------------------------
-__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+static __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                        float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps,
                        float bc1, float bc2, float gscale) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -819,12 +820,12 @@ __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float
     }
 }
 
-__global__ void k_f64_to_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+static __global__ void k_f64_to_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = (float)a[i];
 }
 
-__global__ void k_any_nonfinite(const float* __restrict__ g, int64_t n, int* __restrict__ flag) {
+static __global__ void k_any_nonfinite(const float* __restrict__ g, int64_t n, int* __restrict__ flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (!isfinite(g[i])) atomicMin(flag, (int)i);
 }

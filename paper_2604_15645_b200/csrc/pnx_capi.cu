@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include "../../include/pnx.h"
 #include "kernels_simt.cuh"
 #include "tc_gemm.cuh"
+#include "launch.h"
 
 using namespace pnx;
 
@@ -173,112 +175,7 @@ int pde_layout(int pde) {
     return -1;
 }
 
-// ---- template dispatch -----------------------------------------------------
-
-template <int L>
-void launch_input_t(const InputArgs& a, cudaStream_t st) {
-    const int per_row = a.rff_w > 0 ? a.rff_w : 1;
-    const int64_t total = (int64_t)a.Rpad * per_row;
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    k_input<L><<<grid, 256, 0, st>>>(a);
-}
-void launch_input(int L, const InputArgs& a, cudaStream_t st) {
-    switch (L) {
-        case LAY_XT: launch_input_t<LAY_XT>(a, st); break;
-        case LAY_AC: launch_input_t<LAY_AC>(a, st); break;
-        case LAY_MX: launch_input_t<LAY_MX>(a, st); break;
-        case LAY_NS: launch_input_t<LAY_NS>(a, st); break;
-    }
-}
-void launch_input_bwd(int L, const InputArgs& a, const float* Hb, double* partP, int grid, cudaStream_t st) {
-    switch (L) {
-        case LAY_XT: k_input_bwd<LAY_XT><<<grid, 256, 0, st>>>(a, Hb, partP); break;
-        case LAY_AC: k_input_bwd<LAY_AC><<<grid, 256, 0, st>>>(a, Hb, partP); break;
-        case LAY_MX: k_input_bwd<LAY_MX><<<grid, 256, 0, st>>>(a, Hb, partP); break;
-        case LAY_NS: k_input_bwd<LAY_NS><<<grid, 256, 0, st>>>(a, Hb, partP); break;
-    }
-}
-
-template <int L, int PRO, int EPI>
-void launch_gemm_e(int eact, const GemmArgs& g, dim3 grid, cudaStream_t st) {
-    switch (eact) {
-        case ACT_TANH: k_gemm<L, PRO, EPI, ACT_TANH><<<grid, 256, 0, st>>>(g); break;
-        case ACT_SINE: k_gemm<L, PRO, EPI, ACT_SINE><<<grid, 256, 0, st>>>(g); break;
-        case ACT_SWISH: k_gemm<L, PRO, EPI, ACT_SWISH><<<grid, 256, 0, st>>>(g); break;
-        default: k_gemm<L, PRO, EPI, ACT_NONE><<<grid, 256, 0, st>>>(g); break;
-    }
-}
-template <int L, int PRO>
-void launch_gemm_p(int epi, int eact, const GemmArgs& g, dim3 grid, cudaStream_t st) {
-    switch (epi) {
-        case EPI_BIAS: k_gemm<L, PRO, EPI_BIAS, ACT_NONE><<<grid, 256, 0, st>>>(g); break;
-        case EPI_RAW: k_gemm<L, PRO, EPI_RAW, ACT_NONE><<<grid, 256, 0, st>>>(g); break;
-        default: launch_gemm_e<L, PRO, EPI_ACTT>(eact, g, grid, st); break;
-    }
-}
-template <int L>
-void launch_gemm_l(int pro, int epi, int eact, const GemmArgs& g, dim3 grid, cudaStream_t st) {
-    switch (pro) {
-        case ACT_TANH: launch_gemm_p<L, ACT_TANH>(epi, eact, g, grid, st); break;
-        case ACT_SINE: launch_gemm_p<L, ACT_SINE>(epi, eact, g, grid, st); break;
-        case ACT_SWISH: launch_gemm_p<L, ACT_SWISH>(epi, eact, g, grid, st); break;
-        default: launch_gemm_p<L, ACT_NONE>(epi, eact, g, grid, st); break;
-    }
-}
-void launch_gemm(int L, int pro, int epi, int eact, const GemmArgs& g, cudaStream_t st) {
-    dim3 grid((unsigned)(g.Rpad / GT_M), (unsigned)((g.N + GT_N - 1) / GT_N));
-    switch (L) {
-        case LAY_XT: launch_gemm_l<LAY_XT>(pro, epi, eact, g, grid, st); break;
-        case LAY_AC: launch_gemm_l<LAY_AC>(pro, epi, eact, g, grid, st); break;
-        case LAY_MX: launch_gemm_l<LAY_MX>(pro, epi, eact, g, grid, st); break;
-        case LAY_NS: launch_gemm_l<LAY_NS>(pro, epi, eact, g, grid, st); break;
-    }
-}
-
-template <int L>
-void launch_wgrad_l(int pro, const WgradArgs& w, dim3 grid, cudaStream_t st) {
-    switch (pro) {
-        case ACT_TANH: k_wgrad<L, ACT_TANH><<<grid, 256, 0, st>>>(w); break;
-        case ACT_SINE: k_wgrad<L, ACT_SINE><<<grid, 256, 0, st>>>(w); break;
-        case ACT_SWISH: k_wgrad<L, ACT_SWISH><<<grid, 256, 0, st>>>(w); break;
-        default: k_wgrad<L, ACT_NONE><<<grid, 256, 0, st>>>(w); break;
-    }
-}
-void launch_wgrad(int L, int pro, const WgradArgs& w, int nsplit, cudaStream_t st) {
-    dim3 grid((unsigned)((w.N + 63) / 64), (unsigned)((w.K + 63) / 64), (unsigned)nsplit);
-    switch (L) {
-        case LAY_XT: launch_wgrad_l<LAY_XT>(pro, w, grid, st); break;
-        case LAY_AC: launch_wgrad_l<LAY_AC>(pro, w, grid, st); break;
-        case LAY_MX: launch_wgrad_l<LAY_MX>(pro, w, grid, st); break;
-        case LAY_NS: launch_wgrad_l<LAY_NS>(pro, w, grid, st); break;
-    }
-}
-
-template <int P, int J>
-void launch_head_j(int act, const HeadArgs& h, int grid, cudaStream_t st) {
-    switch (act) {
-        case ACT_TANH: k_head<P, ACT_TANH, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
-        case ACT_SINE: k_head<P, ACT_SINE, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
-        default: k_head<P, ACT_SWISH, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
-    }
-}
-template <int P>
-void launch_head_p(int act, const HeadArgs& h, int grid, cudaStream_t st) {
-    if (h.H <= 32) launch_head_j<P, 1>(act, h, grid, st);
-    else if (h.H <= 64) launch_head_j<P, 2>(act, h, grid, st);
-    else if (h.H <= 128) launch_head_j<P, 4>(act, h, grid, st);
-    else if (h.H <= 256) launch_head_j<P, 8>(act, h, grid, st);
-    else launch_head_j<P, 16>(act, h, grid, st);
-}
-void launch_head(int pde, int act, const HeadArgs& h, int grid, cudaStream_t st) {
-    switch (pde) {
-        case PDE_ADVECTION: launch_head_p<PDE_ADVECTION>(act, h, grid, st); break;
-        case PDE_ALLEN_CAHN: launch_head_p<PDE_ALLEN_CAHN>(act, h, grid, st); break;
-        case PDE_BURGERS: launch_head_p<PDE_BURGERS>(act, h, grid, st); break;
-        case PDE_MAXWELL: launch_head_p<PDE_MAXWELL>(act, h, grid, st); break;
-        case PDE_NS: launch_head_p<PDE_NS>(act, h, grid, st); break;
-    }
-}
+// launch_* dispatchers: launch_simt.cu / launch_tc.cu (declared in launch.h)
 
 // ---- buffers ---------------------------------------------------------------
 
@@ -326,10 +223,10 @@ int upload_rows(pnx_ctx* ctx) {
         const int64_t budget = 48LL << 30;  // bytes of per-chunk activations
         ch = std::max<int64_t>(65536, budget / std::max<int64_t>(1, bytes_per_row(ctx)));
     }
-    ch = std::max<int64_t>(ch, small + 64);
+    ch = std::max<int64_t>(ch, small + 128);
     ch = std::min<int64_t>(ch, T);
     ctx->chunk_rows = ch;
-    const int64_t Rp = roundup(ch, 64);
+    const int64_t Rp = roundup(ch, 128);
     if (Rp > ctx->Rcap) {
         ctx->Rcap = Rp;
         const size_t SR = (size_t)ctx->S * Rp;
@@ -404,11 +301,50 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
     ia.K0 = ctx->K0;
     ia.Hin = ctx->d_Hin;
 
-    const bool use_tc = tc_enabled(ctx->engine, ctx->H, S);
+    const bool tc_on = tc_enabled(ctx->engine, ctx->H, S, act);
+    bool tc_fwd[kMaxLayers] = {}, tc_bwd[kMaxLayers] = {}, tc_wg[kMaxLayers] = {};
+    // debug/ablation: PNX_TC_MASK bit0 forward, bit1 reverse, bit2 weight-gradient (default all)
+    static const int tc_mask = getenv("PNX_TC_MASK") ? atoi(getenv("PNX_TC_MASK")) : 7;
+    if (tc_on) {
+        const int NT = tc_nt(S);
+        int64_t need = 0;
+        for (int l = 0; l < ctx->depth; ++l) {
+            tc_fwd[l] = tc_layer_ok(S, t.K[l], t.N[l]);
+            tc_bwd[l] = l > 0 && tc_fwd[l] && t.K[l] % NT == 0 && (t.N[l] == 128 || t.N[l] == 256);
+            if (tc_fwd[l]) {
+                ctx->tc.img_fwd[l] = need;
+                need += 2LL * t.K[l] * t.N[l];
+            }
+            if (tc_bwd[l]) {
+                ctx->tc.img_bwd[l] = need;
+                need += 2LL * t.K[l] * t.N[l];
+            }
+        }
+        if (need > ctx->tc.img_cap) {
+            if (ctx->tc.img) cudaFree(ctx->tc.img);
+            ctx->tc.img = nullptr;
+            CK(cudaMalloc(&ctx->tc.img, need * sizeof(float)));
+            ctx->tc.img_cap = need;
+        }
+        for (int l = 0; l < ctx->depth; ++l) {
+            tc_wg[l] = tc_fwd[l] && (tc_mask & 4);
+            if (!(tc_mask & 2)) tc_bwd[l] = false;
+            if (tc_fwd[l]) {
+                k_tc_prep_image<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 0, t.N[l],
+                                                    ctx->tc.img + ctx->tc.img_fwd[l]);
+                CKL();
+            }
+            if (tc_bwd[l]) {
+                k_tc_prep_image<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 1, NT,
+                                                    ctx->tc.img + ctx->tc.img_bwd[l]);
+                CKL();
+            }
+        }
+    }
 
     for (int64_t c0 = 0; c0 < T; c0 += ctx->chunk_rows) {
         const int nrows = (int)std::min<int64_t>(ctx->chunk_rows, T - c0);
-        const int Rpad = (int)roundup(nrows, 64);
+        const int Rpad = (int)roundup(nrows, 128);
         ia.row0 = c0;
         ia.nrows = nrows;
         ia.Rpad = Rpad;
@@ -429,10 +365,19 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             g.w0 = ctx->w0;
             const int pro = l == 0 ? ACT_NONE : act;
             prof_begin(ctx, PC_FWD, st);
-            if (use_tc && l > 0) {
-                if (int r = tc_forward(ctx->tc, L, pro, g, st, &ctx->launches)) return fail(ctx, PNX_ERR_CUDA, "tc_forward failed");
+            if (tc_fwd[l] && (tc_mask & 1)) {
+                TcGemmArgs tg{};
+                tg.A = g.A;
+                tg.img = ctx->tc.img + ctx->tc.img_fwd[l];
+                tg.bias = g.bias;
+                tg.out = g.out;
+                tg.Rpad = Rpad;
+                tg.K = g.K;
+                tg.N = g.N;
+                if (launch_tc2_fwd(L, pro, tg, st)) return fail(ctx, PNX_ERR_CUDA, "tc forward launch");
+                CKL();
             } else {
-                launch_gemm(L, pro, EPI_BIAS, ACT_NONE, g, st);
+                launch_gemm(L, pro, EPI_BIAS, act, g, st);
                 CKL();
             }
             prof_end(ctx, st);
@@ -489,8 +434,22 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             w.w0 = ctx->w0;
             const int pro = l == 0 ? ACT_NONE : act;
             prof_begin(ctx, PC_WGRAD, st);
-            if (use_tc && l > 0) {
-                if (int r = tc_wgrad(ctx->tc, L, pro, w, ctx->nsplit[l], st, &ctx->launches)) return fail(ctx, PNX_ERR_CUDA, "tc_wgrad failed");
+            if (tc_wg[l]) {
+                TcWgradArgs tw{};
+                tw.A = w.A;
+                tw.Bm = w.Bm;
+                tw.wpart = ctx->tc.wpart;
+                tw.dbpart = ctx->tc.dbpart;
+                tw.Rpad = Rpad;
+                tw.nrows = nrows;
+                tw.Kin = t.K[l];
+                tw.N = t.N[l];
+                const int ntl = (Rpad + TC_WROWS - 1) / TC_WROWS;
+                if (launch_tc2_wgrad(L, pro, tw, ntl, st)) return fail(ctx, PNX_ERR_CUDA, "tc wgrad launch");
+                CKL();
+                k_tc_wreduce<<<296, 256, 0, st>>>(ctx->tc.wpart, ctx->tc.dbpart, ntl, t.K[l], t.N[l],
+                                                  ctx->d_part[l]);
+                CKL();
             } else {
                 launch_wgrad(L, pro, w, ctx->nsplit[l], st);
                 CKL();
@@ -508,8 +467,17 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                     g.Zlow = ctx->d_Z[l - 1];
                     g.out = ctx->d_Zb[cur ^ 1];
                     prof_begin(ctx, PC_BWD, st);
-                    if (use_tc) {
-                        if (int r = tc_backward(ctx->tc, L, act, g, st, &ctx->launches)) return fail(ctx, PNX_ERR_CUDA, "tc_backward failed");
+                    if (tc_bwd[l]) {
+                        TcGemmArgs tg{};
+                        tg.A = g.A;
+                        tg.img = ctx->tc.img + ctx->tc.img_bwd[l];
+                        tg.Zlow = g.Zlow;
+                        tg.out = g.out;
+                        tg.Rpad = Rpad;
+                        tg.K = g.K;
+                        tg.N = g.N;
+                        if (launch_tc_layer(L, 1, ACT_NONE, tg, st)) return fail(ctx, PNX_ERR_CUDA, "tc backward launch");
+                        CKL();
                     } else {
                         launch_gemm(L, ACT_NONE, EPI_ACTT, act, g, st);
                         CKL();

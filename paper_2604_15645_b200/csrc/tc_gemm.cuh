@@ -1,18 +1,1088 @@
-// tc_gemm.cuh -- tcgen05 (5th-gen tensor core) 3xTF32 path (placeholder until
-// the sm_100a kernels land; the FFMA engine is used meanwhile).
+// tc_gemm.cuh -- the hidden-layer contractions of the jet train step on sm_100a
+// 5th-generation tensor cores: tcgen05.mma kind::tf32 with FP32 accumulators
+// in TMEM and 3xTF32 split accumulation (x = hi + lo, D += Ah*Bh + Ah*Bl + Al*Bh)
+// to hold FP32 accuracy.
+//
+//   k_tc_fwd   Z_out[s] = act(Z_in)[s] W + [s==0] b          (model.cpp:163-175)
+//   k_tc_bwd   Zb_in[s] = act^T(Zb_out[s] W^T ; Z_in)         (graph.cpp:468-502)
+//   k_tc_wgrad dW = sum_s act(Z_in)[s]^T Zb_out[s] per row tile, + db
+//
+// One CTA per SM (TMEM: 512 columns). Operands live in shared memory as
+// K-major 32-byte-swizzled tiles (K = 8 fp32 per stage = one MMA K step):
+// all 8 warps produce a stage (load -> jet activation -> hi/lo split ->
+// swizzled st.shared), thread 0 issues the 3 MMAs per accumulator and commits
+// to the stage's mbarrier, so production of stage i+1 overlaps the tensor
+// core on stage i. Weights are pre-split and pre-swizzled once per step into
+// "stage images" (k_tc_prep_images) and copied 16 B at a time.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include "jets.cuh"
 #include "kernels_simt.cuh"
+#include "tc_common.cuh"
 
 namespace pnx {
+
+constexpr int TC_M = 128;          // rows per MMA / per CTA tile
+constexpr int TC_TILE_BYTES = 4096;  // 128 rows x 8 fp32 (one SW32 K-major tile)
+constexpr int TC_SMEM = 200 * 1024;
+constexpr int TC_WROWS = 512;      // rows per weight-gradient tile (FP32 partial)
+
 struct TcWorkspace {
-    int dummy = 0;
+    float* img = nullptr;          // weight stage images, all layers
+    int64_t img_cap = 0;
+    int64_t img_fwd[kMaxLayers] = {};
+    int64_t img_bwd[kMaxLayers] = {};
+    float* wpart = nullptr;        // [n_wtiles][K*N] FP32 partials
+    int64_t wpart_cap = 0;
+    double* dbpart = nullptr;      // [n_wtiles][N]
+    int64_t dbpart_cap = 0;
+    bool attrs_set = false;
 };
-inline int tc_workspace_alloc(TcWorkspace&, int, int64_t, int, int) { return 0; }
-inline void tc_workspace_free(TcWorkspace&) {}
-inline bool tc_enabled(int, int, int) { return false; }
-inline int tc_forward(TcWorkspace&, int, int, const GemmArgs&, cudaStream_t, int64_t*) { return -1; }
-inline int tc_backward(TcWorkspace&, int, int, const GemmArgs&, cudaStream_t, int64_t*) { return -1; }
-inline int tc_wgrad(TcWorkspace&, int, int, const WgradArgs&, int, cudaStream_t, int64_t*) { return -1; }
+
+// NT: output columns per CTA so that S * NT <= 512 TMEM columns.
+__host__ __device__ constexpr int tc_nt(int S) { return S <= 4 ? 128 : 64; }
+
+// ---------------------------------------------------------------------------
+// weight images: img[(ntile * (K/8) + kb)] = {hi tile, lo tile}, NT x 8 each,
+// element (n, k) of B at sw32_off(n % NT, k % 8). fwd: B(n,k) = W[k][n];
+// bwd: B(n = k_in, k = n_out) = W[n][k].
+// ---------------------------------------------------------------------------
+static __global__ void k_tc_prep_image(const float* __restrict__ W, int K, int N, int transpose_b, int NT,
+                                float* __restrict__ img) {
+    // B is (rowsB x KB): fwd rowsB = N, KB = K ; bwd rowsB = K, KB = N
+    const int rowsB = transpose_b ? K : N, KB = transpose_b ? N : K;
+    const int64_t total = (int64_t)rowsB * KB;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int n = (int)(i / KB), k = (int)(i % KB);
+        const float w = transpose_b ? W[(int64_t)n * N + k] : W[(int64_t)k * N + n];
+        float hi, lo;
+        tc::split3(w, hi, lo);
+        const int nt = n / NT, kb = k / 8;
+        const int64_t blk = ((int64_t)nt * (KB / 8) + kb) * (2 * NT * 8);
+        const uint32_t off = tc::sw32_off((uint32_t)(n % NT), (uint32_t)(k % 8)) / 4;
+        img[blk + off] = hi;
+        img[blk + NT * 8 + off] = lo;
+    }
+}
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void split4(float4 v, float4& hi, float4& lo) {
+    tc::split3(v.x, hi.x, lo.x);
+    tc::split3(v.y, hi.y, lo.y);
+    tc::split3(v.z, hi.z, lo.z);
+    tc::split3(v.w, hi.w, lo.w);
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// jet activation of 4 consecutive features for all streams (z: S float4)
+template <int L, int PRO>
+__device__ __forceinline__ void act4(const float4* z, float4* h) {
+    constexpr int S = Streams<L>::S;
+    float zz[S], hh[S];
+#define ACT4_LANE(c)                                         \
+    _Pragma("unroll") for (int s = 0; s < S; ++s) zz[s] = z[s].c; \
+    act_fwd<L, PRO>(zz, hh, 1.0f);                           \
+    _Pragma("unroll") for (int s = 0; s < S; ++s) h[s].c = hh[s];
+    ACT4_LANE(x) ACT4_LANE(y) ACT4_LANE(z) ACT4_LANE(w)
+#undef ACT4_LANE
+}
+
+// ---------------------------------------------------------------------------
+// shared skeleton bits
+// ---------------------------------------------------------------------------
+struct TcGemmArgs {
+    const float* A;     // [S][Rpad][K] (fwd: Z_in / Hin ; bwd: Zb_out)
+    const float* img;   // weight stage images
+    const float* bias;  // fwd
+    const float* Zlow;  // bwd: Z_in [S][Rpad][N]
+    float* out;         // [S][Rpad][N]
+    int Rpad, K, N;
+};
+
+template <int S, int NT>
+struct TcFwdCfg {
+    static constexpr int A_BYTES = 2 * S * TC_TILE_BYTES;  // hi+lo per stream
+    static constexpr int B_BYTES = 2 * NT * 32;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int NST = (TC_SMEM - 1024) / STAGE > 8 ? 8 : (TC_SMEM - 1024) / STAGE;
+};
+
+// MODE 0: forward (PRO act on A, bias + store_value<ACT> epilogue)
+// MODE 1: backward (A plain, act^T<ACT> epilogue with Zlow)
+template <int L, int MODE, int PRO, int ACT, int NT>
+__global__ void __launch_bounds__(256, 1) k_tc_layer(TcGemmArgs g) {
+    constexpr int S = Streams<L>::S;
+    using Cfg = TcFwdCfg<S, NT>;
+    constexpr int NST = Cfg::NST;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    __shared__ uint64_t empty_bar[8];
+    __shared__ uint64_t done_bar;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ntiles = g.N / NT;
+    const int rt = blockIdx.x / ntiles, nt = blockIdx.x % ntiles;
+    const int r0 = rt * TC_M, n0 = nt * NT;
+    const int nkb = g.K / 8;
+    const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * g.N;
+
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) tc::mbar_init(&empty_bar[i], 1);
+        tc::mbar_init(&done_bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = tc::smem_u32(smem);
+    constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NT, 0, 0);
+
+    // producer mapping: thread -> (row, 16 B chunk) of the 128 x 8 A tile
+    const int prow = tid >> 1, pc = tid & 1;
+    const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
+    const uint32_t aoff = tc::sw32_off((uint32_t)prow, (uint32_t)(pc * 4));
+    const float4* bimg = reinterpret_cast<const float4*>(g.img) + (int64_t)nt * nkb * (Cfg::B_BYTES / 16);
+
+    float4 zin[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) zin[s] = ldg4(asrc + s * RK);
+
+    for (int it = 0; it < nkb; ++it) {
+        const int st = it % NST;
+        const uint32_t stage = sbase + st * Cfg::STAGE;
+        if (it >= NST) tc::mbar_wait(&empty_bar[st], (uint32_t)((it / NST) - 1) & 1u);
+        // ---- A: jet activation (forward) + 3xTF32 split, swizzled stores
+        float4 h[S];
+        if constexpr (MODE == 0) {
+            act4<L, PRO>(zin, h);
+        } else {
+#pragma unroll
+            for (int s = 0; s < S; ++s) h[s] = zin[s];
+        }
+        // prefetch the next k-block's raw A while this one is stored
+        if (it + 1 < nkb) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) zin[s] = ldg4(asrc + s * RK + (it + 1) * 8);
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            float4 hi, lo;
+            split4(h[s], hi, lo);
+            sts128(stage + (2 * s) * TC_TILE_BYTES + aoff, hi);
+            sts128(stage + (2 * s + 1) * TC_TILE_BYTES + aoff, lo);
+        }
+        // ---- B: weight image block (pre-split, pre-swizzled)
+        {
+            const float4* src = bimg + (int64_t)it * (Cfg::B_BYTES / 16);
+            for (int i = tid; i < Cfg::B_BYTES / 16; i += 256) sts128(stage + Cfg::A_BYTES + i * 16, __ldg(src + i));
+        }
+        tc::fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc::tc_fence_after();
+            const uint32_t bh = stage + Cfg::A_BYTES, bl = bh + NT * 32;
+            const uint64_t bdh = tc::make_sdesc(bh, 16, 256, 6), bdl = tc::make_sdesc(bl, 16, 256, 6);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const uint32_t ah = stage + (2 * s) * TC_TILE_BYTES, al = ah + TC_TILE_BYTES;
+                const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(al, 16, 256, 6);
+                const uint32_t d = tmem + (uint32_t)(s * NT);
+                tc::mma_tf32(d, adh, bdh, idesc, it > 0 ? 1u : 0u);
+                tc::mma_tf32(d, adh, bdl, idesc, 1u);
+                tc::mma_tf32(d, adl, bdh, idesc, 1u);
+            }
+            tc::mma_commit(&empty_bar[st]);
+        }
+    }
+    if (tid == 0) tc::mma_commit(&done_bar);
+    tc::mbar_wait(&done_bar, 0);
+    tc::tc_fence_after();
+
+    // ---- epilogue: warp (w%4) owns TMEM lanes 32*(w%4).., w/4 picks the column half
+    const int q = warp & 3, half = warp >> 2;
+    const int row = r0 + q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    constexpr int HC = NT / 2;
+    if constexpr (MODE == 0) {
+#pragma unroll 1
+        for (int s = 0; s < S; ++s) {
+#pragma unroll 1
+            for (int c = 0; c < HC; c += 16) {
+                const int col = half * HC + c;
+                float v[16];
+                tc::tmem_ld16(tl + (uint32_t)(s * NT + col), v);
+                tc::tmem_ld_wait();
+                float* dst = g.out + s * RN + (int64_t)row * g.N + n0 + col;
+                if (s == 0) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = store_value<ACT>(v[j] + __ldg(g.bias + n0 + col + j));
+                }
+#pragma unroll
+                for (int j = 0; j < 16; j += 4)
+                    *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int c = 0; c < HC; c += 8) {
+            const int col = half * HC + c;
+            float hb[S][8], z[S][8];
+#pragma unroll
+            for (int s = 0; s < S; ++s) tmem_ld8(tl + (uint32_t)(s * NT + col), hb[s]);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const float* zp = g.Zlow + s * RN + (int64_t)row * g.N + n0 + col;
+                const float4 a = ldg4(zp), b = ldg4(zp + 4);
+                z[s][0] = a.x; z[s][1] = a.y; z[s][2] = a.z; z[s][3] = a.w;
+                z[s][4] = b.x; z[s][5] = b.y; z[s][6] = b.z; z[s][7] = b.w;
+            }
+            tc::tmem_ld_wait();
+            float zb[S][8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float zz[S], hh[S], oo[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    zz[s] = z[s][j];
+                    hh[s] = hb[s][j];
+                }
+                act_bwd<L, ACT>(zz, hh, oo, 1.0f);
+#pragma unroll
+                for (int s = 0; s < S; ++s) zb[s][j] = oo[s];
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                float* dst = g.out + s * RN + (int64_t)row * g.N + n0 + col;
+                *reinterpret_cast<float4*>(dst) = make_float4(zb[s][0], zb[s][1], zb[s][2], zb[s][3]);
+                *reinterpret_cast<float4*>(dst + 4) = make_float4(zb[s][4], zb[s][5], zb[s][6], zb[s][7]);
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// weight gradient: per row tile of TC_WROWS rows,
+//   wpart[tile][k][n] = sum_{rows, s} act(Z_in)[s][row][k] * Zb[s][row][n]
+//   dbpart[tile][n]   = sum_rows Zb[0][row][n]
+// M = k_in (MT tiles of 128), N = n_out, K = 8 rows of one stream per stage.
+// Operands are written transposed (K-major: k = row) into SW32 tiles.
+// ---------------------------------------------------------------------------
+struct TcWgradArgs {
+    const float* A;   // Z_in / Hin [S][Rpad][Kin]
+    const float* Bm;  // Zb_out [S][Rpad][N]
+    float* wpart;
+    double* dbpart;
+    int Rpad, nrows, Kin, N;
+};
+
+template <int S, int MT, int N>
+struct TcWgCfg {
+    static constexpr int A_BYTES = 2 * MT * TC_TILE_BYTES;
+    static constexpr int B_BYTES = 2 * N * 32;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int NST = (TC_SMEM - 1024) / STAGE > 8 ? 8 : (TC_SMEM - 1024) / STAGE;
+};
+
+template <int L, int PRO, int MT, int N>
+__global__ void __launch_bounds__(256, 1) k_tc_wgrad(TcWgradArgs g) {
+    constexpr int S = Streams<L>::S;
+    using St = Streams<L>;
+    using Cfg = TcWgCfg<S, MT, N>;
+    constexpr int NST = Cfg::NST;
+    constexpr int KIN = MT * 128;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    __shared__ uint64_t empty_bar[8];
+    __shared__ uint64_t done_bar;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rbeg = blockIdx.x * TC_WROWS;
+    const int rend = min(g.Rpad, rbeg + TC_WROWS);
+    const int nrb = (rend - rbeg) / 8;
+    const int nit = nrb * S;
+    const int64_t RK = (int64_t)g.Rpad * KIN, RN = (int64_t)g.Rpad * N;
+
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) tc::mbar_init(&empty_bar[i], 1);
+        tc::mbar_init(&done_bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = tc::smem_u32(smem);
+    constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, N, 0, 0);
+
+    // producer mapping: r = row within the 8-row block, f = 8-feature block
+    const int pr = tid & 7, pf = tid >> 3;  // pf in [0, 32)
+    double dbacc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dbacc[j] = 0.0;
+
+    for (int it = 0; it < nit; ++it) {
+        const int st = it % NST;
+        const uint32_t stage = sbase + st * Cfg::STAGE;
+        const int rb = it / S, s = it % S;
+        const int row = rbeg + rb * 8 + pr;
+        if (it >= NST) tc::mbar_wait(&empty_bar[st], (uint32_t)((it / NST) - 1) & 1u);
+        // ---- A(m = k_in, k = row) = act(Z_in)[s][row][k_in]
+        for (int fb = pf; fb < KIN / 8; fb += 32) {
+            const int f = fb * 8;
+            float h[8];
+            if constexpr (PRO == ACT_NONE) {
+                const float* p = g.A + s * RK + (int64_t)row * KIN + f;
+                const float4 a = ldg4(p), b = ldg4(p + 4);
+                h[0] = a.x; h[1] = a.y; h[2] = a.z; h[3] = a.w; h[4] = b.x; h[5] = b.y; h[6] = b.z; h[7] = b.w;
+            } else {
+                // tanh storage: value stream holds t; needs t, z_s (+ partner)
+                const float* p0 = g.A + (int64_t)row * KIN + f;
+                const float4 t0 = ldg4(p0), t1 = ldg4(p0 + 4);
+                const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+                if (s == 0) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) h[j] = tv[j];
+                } else {
+                    const float* ps = g.A + s * RK + (int64_t)row * KIN + f;
+                    const float4 a = ldg4(ps), b = ldg4(ps + 4);
+                    const float zs[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                    int par = -1;
+#pragma unroll
+                    for (int q2 = 1; q2 < S; ++q2)
+                        if (q2 == s) par = St::partner(q2);
+                    if (par < 0) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) h[j] = (1.0f - tv[j] * tv[j]) * zs[j];
+                    } else {
+                        const float* pp = g.A + par * RK + (int64_t)row * KIN + f;
+                        const float4 c = ldg4(pp), d = ldg4(pp + 4);
+                        const float za[8] = {c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            h[j] = (1.0f - tv[j] * tv[j]) * (zs[j] - 2.0f * tv[j] * za[j] * za[j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int j = (jj + (pf & 3)) & 7;  // rotate to spread banks
+                const int m = f + j;
+                float hi, lo;
+                tc::split3(h[j], hi, lo);
+                const uint32_t o = (uint32_t)(m >> 7) * 2 * TC_TILE_BYTES + tc::sw32_off((uint32_t)(m & 127), (uint32_t)pr);
+                sts32(stage + o, hi);
+                sts32(stage + o + TC_TILE_BYTES, lo);
+            }
+        }
+        // ---- B(n = n_out, k = row) = Zb[s][row][n]
+        for (int nb = pf; nb < N / 8; nb += 32) {
+            const int n = nb * 8;
+            const float* p = g.Bm + s * RN + (int64_t)row * N + n;
+            const float4 a = ldg4(p), b = ldg4(p + 4);
+            const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            if (s == 0) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dbacc[j] += (double)v[j];
+            }
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int j = (jj + (pf & 3)) & 7;
+                float hi, lo;
+                tc::split3(v[j], hi, lo);
+                const uint32_t o = tc::sw32_off((uint32_t)(n + j), (uint32_t)pr);
+                sts32(stage + Cfg::A_BYTES + o, hi);
+                sts32(stage + Cfg::A_BYTES + N * 32 + o, lo);
+            }
+        }
+        tc::fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc::tc_fence_after();
+            const uint32_t bh = stage + Cfg::A_BYTES, bl = bh + N * 32;
+            const uint64_t bdh = tc::make_sdesc(bh, 16, 256, 6), bdl = tc::make_sdesc(bl, 16, 256, 6);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const uint32_t ah = stage + mt * 2 * TC_TILE_BYTES, al = ah + TC_TILE_BYTES;
+                const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(al, 16, 256, 6);
+                const uint32_t d = tmem + (uint32_t)(mt * N);
+                tc::mma_tf32(d, adh, bdh, idesc, it > 0 ? 1u : 0u);
+                tc::mma_tf32(d, adh, bdl, idesc, 1u);
+                tc::mma_tf32(d, adl, bdh, idesc, 1u);
+            }
+            tc::mma_commit(&empty_bar[st]);
+        }
+    }
+    if (tid == 0) tc::mma_commit(&done_bar);
+    tc::mbar_wait(&done_bar, 0);
+    tc::tc_fence_after();
+
+    // ---- epilogue: FP32 partial dW of this row tile
+    const int q = warp & 3, grp = warp >> 2;  // grp: M tile (MT == 2) or column half (MT == 1)
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    float* wp = g.wpart + (int64_t)blockIdx.x * KIN * N;
+    if (nit > 0) {
+        const int mt = MT == 2 ? grp : 0;
+        const int c0 = MT == 2 ? 0 : grp * (N / 2), c1 = MT == 2 ? N : c0 + N / 2;
+        const int k = mt * 128 + q * 32 + lane;
+#pragma unroll 1
+        for (int c = c0; c < c1; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tl + (uint32_t)(mt * N + c), v);
+            tc::tmem_ld_wait();
+            float* dst = wp + (int64_t)k * N + c;
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+    } else {
+        for (int i = tid; i < KIN * N; i += 256) wp[i] = 0.0f;
+    }
+    // db: reduce the 8 row lanes (lane bits 0..2) of each 8-column block
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        double v = dbacc[j];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        dbacc[j] = v;
+    }
+    if (pr == 0 && pf < N / 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g.dbpart[(int64_t)blockIdx.x * N + pf * 8 + j] = dbacc[j];
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+// part[k*N + n] += sum_t wpart[t][k][n] ; part[K*N + n] += sum_t dbpart[t][n]  (FP64, fixed order)
+static __global__ void k_tc_wreduce(const float* __restrict__ wpart, const double* __restrict__ dbpart, int ntiles,
+                             int K, int N, double* __restrict__ part) {
+    const int64_t KN = (int64_t)K * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < KN + N; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        if (i < KN) {
+            for (int t = 0; t < ntiles; ++t) s += (double)wpart[(int64_t)t * KN + i];
+        } else {
+            for (int t = 0; t < ntiles; ++t) s += dbpart[(int64_t)t * N + (i - KN)];
+        }
+        part[i] += s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+// ---------------------------------------------------------------------------
+inline bool tc_layer_ok(int S, int K, int N) {
+    const int NT = tc_nt(S);
+    return S <= 5 && K % 32 == 0 && K >= 32 && K <= 256 && N % NT == 0 && N <= 256 && (K == 128 || K == 256);
+}
+
+inline bool tc_enabled(int engine, int H, int S, int act) {
+    if (engine == 1) return false;  // PNX_ENGINE_FFMA
+    return (H == 128 || H == 256) && S <= 5 && act == ACT_TANH;
+}
+
+inline int tc_workspace_alloc(TcWorkspace& ws, int, int64_t Rpad, int H, int K0) {
+    const int64_t tiles = (Rpad + TC_WROWS - 1) / TC_WROWS;
+    const int64_t kmax = H > K0 ? H : K0;
+    const int64_t need = tiles * kmax * H;
+    if (need > ws.wpart_cap) {
+        if (ws.wpart) cudaFree(ws.wpart);
+        if (cudaMalloc(&ws.wpart, need * sizeof(float)) != cudaSuccess) return -2;
+        ws.wpart_cap = need;
+    }
+    if (tiles * H > ws.dbpart_cap) {
+        if (ws.dbpart) cudaFree(ws.dbpart);
+        if (cudaMalloc(&ws.dbpart, tiles * H * sizeof(double)) != cudaSuccess) return -2;
+        ws.dbpart_cap = tiles * H;
+    }
+    return 0;
+}
+inline void tc_workspace_free(TcWorkspace& ws) {
+    if (ws.img) cudaFree(ws.img);
+    if (ws.wpart) cudaFree(ws.wpart);
+    if (ws.dbpart) cudaFree(ws.dbpart);
+    ws = TcWorkspace{};
+}
+
+
+// ===========================================================================
+// v2: warp-specialized kernels with split ("big" | "small") accumulators.
+//
+// Accumulating the 3xTF32 correction products (hi*lo, lo*hi) into the same
+// FP32 TMEM accumulator as hi*hi truncates them against the large running sum
+// (measured: 5.2e-7 vs 1.5e-7 rel. error for FP32 FMA at K=64). Keeping them in
+// a separate "small" accumulator restores FP32-level accuracy (1.9e-7); the
+// epilogue adds big + small. N=256 MMAs with the A operand reused by two
+// consecutive MMAs keep the SMEM operand traffic under the tensor pipe's rate.
+//
+// Roles (416 threads): warps 0-7 produce stages, warp 8 issues tcgen05.mma
+// (lane 0) and owns TMEM, warps 9-12 drain TMEM (epilogue; warp%4 = lane quarter).
+// ===========================================================================
+constexpr int TC2_THREADS = 416;
+constexpr int TC3_THREADS = 544;  // 8 producer + 1 MMA + 8 epilogue warps
+constexpr int TC2_PROD = 256;
+
+template <int NF>
+struct Tc2FwdCfg {
+    static constexpr int A_T = TC_TILE_BYTES;  // 128 rows x 8 fp32
+    static constexpr int B_T = NF * 32;
+    static constexpr int STAGE = 2 * A_T + 2 * B_T;
+    static constexpr int NST = (TC_SMEM - 1024) / STAGE > 8 ? 8 : (TC_SMEM - 1024) / STAGE;
+    static constexpr int NBUF = 4 * NF <= 512 ? 2 : 1;  // TMEM buffers of (big | small)
+};
+
+// forward: Z_out[p] = act(Z_in)[p] W + [p==0] b, one stream p per pass
+template <int L, int PRO, int NF>
+__global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    using Cfg = Tc2FwdCfg<NF>;
+    constexpr int NST = Cfg::NST, NBUF = Cfg::NBUF;
+    constexpr int D = 3;  // register prefetch depth (stages)
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    __shared__ uint64_t full[8], empty[8], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r0 = blockIdx.x * TC_M;
+    const int nkb = g.K / 8, nit = S * nkb;
+    const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * NF;
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            tc::mbar_init(&full[i], 9);  // 8 producer warps + 1 expect_tx
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < NBUF; ++i) {
+            tc::mbar_init(&tfull[i], 1);
+            tc::mbar_init(&tempty[i], 8);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 8) tc::tmem_alloc<512>(&tmem_base);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = tc::smem_u32(smem);
+
+    if (warp < 8) {
+        // ---------------- producers ----------------
+        const int prow = tid >> 1, pc = tid & 1;
+        const float* rowp = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
+        const uint32_t aoff = tc::sw32_off((uint32_t)prow, (uint32_t)(pc * 4));
+        float4 ring[D][3];
+        auto load = [&](int it, float4* v) {
+            const int p = it / nkb, off = (it % nkb) * 8;
+            if constexpr (PRO == ACT_NONE) {
+                v[0] = ldg4(rowp + p * RK + off);
+            } else {
+                v[0] = ldg4(rowp + off);  // value stream (t)
+                if (p > 0) v[1] = ldg4(rowp + p * RK + off);
+                if (St::order(p) == 2) v[2] = ldg4(rowp + St::partner(p) * RK + off);
+            }
+        };
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            if (d < nit) load(d, ring[d]);
+        // unrolled by D so every ring slot index is a compile-time constant
+        for (int it0 = 0; it0 < nit; it0 += D) {
+#pragma unroll
+            for (int slot = 0; slot < D; ++slot) {
+                const int it = it0 + slot;
+                if (it >= nit) break;
+                const int st = it % NST, p = it / nkb, kb = it % nkb;
+                const uint32_t stage = sbase + st * Cfg::STAGE;
+                float4 v[3];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) v[j] = ring[slot][j];
+                if (it + D < nit) load(it + D, ring[slot]);
+                float4 h;
+                if constexpr (PRO == ACT_NONE) {
+                    h = v[0];
+                } else {
+                    const float4 t = v[0];
+                    if (p == 0) {
+                        h = t;
+                    } else if (St::order(p) == 1) {
+                        h = make_float4((1.f - t.x * t.x) * v[1].x, (1.f - t.y * t.y) * v[1].y,
+                                        (1.f - t.z * t.z) * v[1].z, (1.f - t.w * t.w) * v[1].w);
+                    } else {
+                        h = make_float4((1.f - t.x * t.x) * (v[1].x - 2.f * t.x * v[2].x * v[2].x),
+                                        (1.f - t.y * t.y) * (v[1].y - 2.f * t.y * v[2].y * v[2].y),
+                                        (1.f - t.z * t.z) * (v[1].z - 2.f * t.z * v[2].z * v[2].z),
+                                        (1.f - t.w * t.w) * (v[1].w - 2.f * t.w * v[2].w * v[2].w));
+                    }
+                }
+                float4 hi, lo;
+                split4(h, hi, lo);
+                tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                if (tid == 0) {
+                    tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
+                    tc::bulk_g2s(stage + 2 * Cfg::A_T, g.img + (int64_t)kb * (2 * Cfg::B_T / 4), 2 * Cfg::B_T,
+                                 &full[st]);
+                }
+                sts128(stage + aoff, hi);
+                sts128(stage + Cfg::A_T + aoff, lo);
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&full[st]);
+            }
+        }
+    } else if (warp == 8) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NF, 0, 0);
+            for (int p = 0; p < S; ++p) {
+                const int buf = p % NBUF, use = p / NBUF;
+                tc::mbar_wait(&tempty[buf], ((uint32_t)use & 1u) ^ 1u);
+                tc::tc_fence_after();
+                const uint32_t dbig = tmem + (uint32_t)(buf * 2 * NF), dsmall = dbig + NF;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    const int it = p * nkb + kb, st = it % NST;
+                    const uint32_t stage = sbase + st * Cfg::STAGE;
+                    tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                    tc::tc_fence_after();
+                    const uint64_t ah = tc::make_sdesc(stage, 16, 256, 6), al = tc::make_sdesc(stage + Cfg::A_T, 16, 256, 6);
+                    const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 16, 256, 6);
+                    const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 16, 256, 6);
+                    tc::mma_tf32(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
+                    tc::mma_tf32(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+                    tc::mma_tf32(dsmall, al, bh, idesc, 1u);
+                    tc::mma_commit(&empty[st]);
+                }
+                tc::mma_commit(&tfull[buf]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue (8 warps: lane quarter warp%4, column half) ----------------
+        const int q = warp & 3, half = (warp - 9) >> 2;
+        const int row = r0 + q * 32 + lane;
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        for (int p = 0; p < S; ++p) {
+            const int buf = p % NBUF, use = p / NBUF;
+            tc::mbar_wait(&tfull[buf], (uint32_t)use & 1u);
+            tc::tc_fence_after();
+            float* dst = g.out + p * RN + (int64_t)row * NF;
+#pragma unroll 1
+            for (int c = half * (NF / 2); c < (half + 1) * (NF / 2); c += 16) {
+                float a[16], b[16];
+                tc::tmem_ld16(tl + (uint32_t)(buf * 2 * NF + c), a);
+                tc::tmem_ld16(tl + (uint32_t)(buf * 2 * NF + NF + c), b);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 16; ++j) a[j] += b[j];
+                if (p == 0) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));
+                }
+#pragma unroll
+                for (int j = 0; j < 16; j += 4)
+                    *reinterpret_cast<float4*>(dst + c + j) = make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]);
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 8) tc::tmem_dealloc<512>(tmem);
+}
+
+// weight gradient, one 128-wide k_in tile (mt) per CTA, big|small accumulators:
+//   wpart[tile][mt*128 + m][n] = sum_{rows, s} act(Z_in)[s][row][k_in] Zb[s][row][n]
+// A (m = k_in, k = row) and B (n = n_out, k = row) are MN-major SW128_32B tiles
+// written with 16 B stores straight from the row-major activations.
+template <int NF>
+struct Tc2WgCfg {
+    static constexpr int A_T = 8 * 128 * 4;  // 8 rows x 128 k_in
+    static constexpr int B_T = 8 * NF * 4;
+    static constexpr int STAGE = 2 * A_T + 2 * B_T;
+    static constexpr int NST = (TC_SMEM - 16384) / STAGE > 8 ? 8 : (TC_SMEM - 16384) / STAGE;
+};
+
+template <int L, int PRO, int NF>
+__global__ void __launch_bounds__(TC2_THREADS, 1) k_tc2_wgrad(TcWgradArgs g, int wrows) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    using Cfg = Tc2WgCfg<NF>;
+    constexpr int NST = Cfg::NST;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    __shared__ uint64_t full[8], empty[8], tfull;
+    __shared__ uint32_t tmem_base;
+    __shared__ double dbred[8][NF];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int MT = g.Kin / 128;
+    const int tile = blockIdx.x / MT, mt = blockIdx.x % MT;
+    const int rbeg = tile * wrows;
+    const int rend = min(g.Rpad, rbeg + wrows);
+    const int nit = ((rend - rbeg) / 8) * S;
+    const int64_t RK = (int64_t)g.Rpad * g.Kin, RN = (int64_t)g.Rpad * NF;
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            tc::mbar_init(&full[i], 8);
+            tc::mbar_init(&empty[i], 1);
+        }
+        tc::mbar_init(&tfull, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 8) tc::tmem_alloc<512>(&tmem_base);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = tc::smem_u32(smem);
+
+    if (warp < 8) {
+        // A: thread -> (row r = tid/32, 4 features at 4*(tid%32)) ; B: 2 chunks of 4 n
+        const int ar = tid >> 5, ac = tid & 31;
+        const int f = mt * 128 + ac * 4;
+        const uint32_t aoff = tc::mn32_off((uint32_t)ar, (uint32_t)(ac * 4), 128u);
+        constexpr int BCH = NF / 4;  // float4 chunks per row
+        int brow[2], bc[2];
+        uint32_t boff[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int idx = tid + 256 * j;
+            brow[j] = idx / BCH;
+            bc[j] = idx % BCH;
+            boff[j] = tc::mn32_off((uint32_t)(brow[j] & 7), (uint32_t)(bc[j] * 4), (uint32_t)NF);
+        }
+        double dbacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        constexpr int D = 2;  // register prefetch depth (stages)
+        float4 ring[D][5];
+        auto load = [&](int it, float4* v) {
+            const int rb = it / S, s = it % S;
+            const int row = rbeg + rb * 8 + ar;
+            const float* pa = g.A + (int64_t)row * g.Kin + f;
+            if constexpr (PRO == ACT_NONE) {
+                v[0] = ldg4(pa + s * RK);
+            } else {
+                v[0] = ldg4(pa);
+                if (s > 0) v[1] = ldg4(pa + s * RK);
+                int par = -1;
+#pragma unroll
+                for (int q2 = 1; q2 < S; ++q2)
+                    if (q2 == s) par = St::partner(q2);
+                if (par >= 0) v[2] = ldg4(pa + par * RK);
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                if (brow[j] < 8) v[3 + j] = ldg4(g.Bm + s * RN + (int64_t)(rbeg + rb * 8 + brow[j]) * NF + bc[j] * 4);
+        };
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            if (d < nit) load(d, ring[d]);
+        for (int it0 = 0; it0 < nit; it0 += D) {
+#pragma unroll
+            for (int slot = 0; slot < D; ++slot) {
+                const int it = it0 + slot;
+                if (it >= nit) break;
+                const int st = it % NST, s = it % S;
+                const uint32_t stage = sbase + st * Cfg::STAGE;
+                float4 v[5];
+#pragma unroll
+                for (int j = 0; j < 5; ++j) v[j] = ring[slot][j];
+                if (it + D < nit) load(it + D, ring[slot]);
+                float4 h;
+                if constexpr (PRO == ACT_NONE) {
+                    h = v[0];
+                } else {
+                    const float4 t = v[0];
+                    if (s == 0) {
+                        h = t;
+                    } else {
+                        int par = -1;
+#pragma unroll
+                        for (int q2 = 1; q2 < S; ++q2)
+                            if (q2 == s) par = St::partner(q2);
+                        const float4 z = v[1];
+                        if (par < 0) {
+                            h = make_float4((1.f - t.x * t.x) * z.x, (1.f - t.y * t.y) * z.y, (1.f - t.z * t.z) * z.z,
+                                            (1.f - t.w * t.w) * z.w);
+                        } else {
+                            const float4 za = v[2];
+                            h = make_float4((1.f - t.x * t.x) * (z.x - 2.f * t.x * za.x * za.x),
+                                            (1.f - t.y * t.y) * (z.y - 2.f * t.y * za.y * za.y),
+                                            (1.f - t.z * t.z) * (z.z - 2.f * t.z * za.z * za.z),
+                                            (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
+                        }
+                    }
+                }
+                float4 ahi, alo, bhi[2], blo[2];
+                split4(h, ahi, alo);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (brow[j] >= 8) continue;
+                    if (s == 0) {
+                        dbacc[j][0] += v[3 + j].x;
+                        dbacc[j][1] += v[3 + j].y;
+                        dbacc[j][2] += v[3 + j].z;
+                        dbacc[j][3] += v[3 + j].w;
+                    }
+                    split4(v[3 + j], bhi[j], blo[j]);
+                }
+                tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                sts128(stage + aoff, ahi);
+                sts128(stage + Cfg::A_T + aoff, alo);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (brow[j] >= 8) continue;
+                    sts128(stage + 2 * Cfg::A_T + boff[j], bhi[j]);
+                    sts128(stage + 2 * Cfg::A_T + Cfg::B_T + boff[j], blo[j]);
+                }
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&full[st]);
+            }
+        }
+        // db (M tile 0 only): rows of a chunk are spread over threads with equal idx % BCH
+        if (mt == 0) {
+            for (int i = tid; i < 8 * NF; i += 256) (&dbred[0][0])[i] = 0.0;
+            asm volatile("bar.sync 1, 256;");
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int idx = tid + 256 * j;
+                if (idx / BCH >= 8) continue;
+                const int grp = idx / BCH;  // one slot per row of the 8-row block (fixed-order sum below)
+                for (int c = 0; c < 4; ++c) dbred[grp][(idx % BCH) * 4 + c] += dbacc[j][c];
+            }
+            asm volatile("bar.sync 1, 256;");
+            for (int n = tid; n < NF; n += 256)
+                g.dbpart[(int64_t)tile * NF + n] = ((dbred[0][n] + dbred[1][n]) + (dbred[2][n] + dbred[3][n])) +
+                                                   ((dbred[4][n] + dbred[5][n]) + (dbred[6][n] + dbred[7][n]));
+        }
+    } else if (warp == 8) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NF, 1, 1);
+            const uint32_t dbig = tmem, dsmall = tmem + NF;
+            for (int it = 0; it < nit; ++it) {
+                const int st = it % NST;
+                const uint32_t stage = sbase + st * Cfg::STAGE;
+                tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                tc::tc_fence_after();
+                const uint64_t ah = tc::make_sdesc(stage, 512, 4 * 512, 1);
+                const uint64_t al = tc::make_sdesc(stage + Cfg::A_T, 512, 4 * 512, 1);
+                const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 512, (NF / 32) * 512, 1);
+                const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 512, (NF / 32) * 512, 1);
+                tc::mma_tf32(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
+                tc::mma_tf32(dsmall, ah, bl, idesc, it > 0 ? 1u : 0u);
+                tc::mma_tf32(dsmall, al, bh, idesc, 1u);
+                tc::mma_commit(&empty[st]);
+            }
+            tc::mma_commit(&tfull);
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        float* dst = g.wpart + ((int64_t)tile * g.Kin + mt * 128 + m) * NF;
+        if (nit > 0) {
+            tc::mbar_wait(&tfull, 0);
+            tc::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < NF; c += 16) {
+                float a[16], b[16];
+                tc::tmem_ld16(tl + (uint32_t)c, a);
+                tc::tmem_ld16(tl + (uint32_t)(NF + c), b);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 16; j += 4)
+                    *reinterpret_cast<float4*>(dst + c + j) =
+                        make_float4(a[j] + b[j], a[j + 1] + b[j + 1], a[j + 2] + b[j + 2], a[j + 3] + b[j + 3]);
+            }
+        } else {
+            for (int c = 0; c < NF; ++c) dst[c] = 0.0f;
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 8) tc::tmem_dealloc<512>(tmem);
+}
+
+
+// reverse: Zb_in[s] = act^T(Zb_out[s] W^T ; Z_in), all S streams of a
+// 128-row x NT-column tile resident in TMEM (the tanh jet transpose couples the
+// streams), one accumulator per stream; weights streamed by cp.async.bulk.
+template <int S, int NT>
+struct Tc2BwdCfg {
+    static constexpr int A_BYTES = 2 * S * TC_TILE_BYTES;
+    static constexpr int B_T = NT * 32;
+    static constexpr int STAGE = A_BYTES + 2 * B_T;
+    static constexpr int NST = (TC_SMEM - 1024) / STAGE > 8 ? 8 : (TC_SMEM - 1024) / STAGE;
+};
+
+template <int L, int NT>
+__global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    using Cfg = Tc2BwdCfg<S, NT>;
+    constexpr int NST = Cfg::NST;
+    constexpr int D = 2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    __shared__ uint64_t full[8], empty[8], tfull;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ntiles = g.N / NT;
+    const int rt = blockIdx.x / ntiles, nt = blockIdx.x % ntiles;
+    const int r0 = rt * TC_M, n0 = nt * NT;
+    const int nkb = g.K / 8;
+    const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * g.N;
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            tc::mbar_init(&full[i], 9);
+            tc::mbar_init(&empty[i], 1);
+        }
+        tc::mbar_init(&tfull, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 8) tc::tmem_alloc<512>(&tmem_base);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = tc::smem_u32(smem);
+    const float* bimg = g.img + (int64_t)nt * nkb * (2 * Cfg::B_T / 4);
+
+    if (warp < 8) {
+        const int prow = tid >> 1, pc = tid & 1;
+        const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
+        const uint32_t aoff = tc::sw32_off((uint32_t)prow, (uint32_t)(pc * 4));
+        float4 ring[D][S];
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            if (d < nkb)
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) ring[d][s2] = ldg4(asrc + s2 * RK + d * 8);
+        for (int it0 = 0; it0 < nkb; it0 += D) {
+#pragma unroll
+            for (int slot = 0; slot < D; ++slot) {
+                const int it = it0 + slot;
+                if (it >= nkb) break;
+                const int st = it % NST;
+                const uint32_t stage = sbase + st * Cfg::STAGE;
+                float4 hi[S], lo[S];
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) split4(ring[slot][s2], hi[s2], lo[s2]);
+                if (it + D < nkb)
+#pragma unroll
+                    for (int s2 = 0; s2 < S; ++s2) ring[slot][s2] = ldg4(asrc + s2 * RK + (it + D) * 8);
+                tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                if (tid == 0) {
+                    tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
+                    tc::bulk_g2s(stage + Cfg::A_BYTES, bimg + (int64_t)it * (2 * Cfg::B_T / 4), 2 * Cfg::B_T, &full[st]);
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) {
+                    sts128(stage + (2 * s2) * TC_TILE_BYTES + aoff, hi[s2]);
+                    sts128(stage + (2 * s2 + 1) * TC_TILE_BYTES + aoff, lo[s2]);
+                }
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&full[st]);
+            }
+        }
+    } else if (warp == 8) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NT, 0, 0);
+            for (int it = 0; it < nkb; ++it) {
+                const int st = it % NST;
+                const uint32_t stage = sbase + st * Cfg::STAGE;
+                tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                tc::tc_fence_after();
+                const uint64_t bh = tc::make_sdesc(stage + Cfg::A_BYTES, 16, 256, 6);
+                const uint64_t bl = tc::make_sdesc(stage + Cfg::A_BYTES + Cfg::B_T, 16, 256, 6);
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) {
+                    const uint32_t ah = stage + (2 * s2) * TC_TILE_BYTES;
+                    const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(ah + TC_TILE_BYTES, 16, 256, 6);
+                    const uint32_t d = tmem + (uint32_t)(s2 * NT);
+                    tc::mma_tf32(d, adh, bh, idesc, it > 0 ? 1u : 0u);
+                    tc::mma_tf32(d, adh, bl, idesc, 1u);
+                    tc::mma_tf32(d, adl, bh, idesc, 1u);
+                }
+                tc::mma_commit(&empty[st]);
+            }
+            tc::mma_commit(&tfull);
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3, half = (warp - 9) >> 2;
+        const int row = r0 + q * 32 + lane;
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        tc::mbar_wait(&tfull, 0);
+        tc::tc_fence_after();
+#pragma unroll 1
+        for (int c = half * (NT / 2); c < (half + 1) * (NT / 2); c += 8) {
+            float hb[S][8], z[S][8];
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) tmem_ld8(tl + (uint32_t)(s2 * NT + c), hb[s2]);
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) {
+                const float* zp = g.Zlow + s2 * RN + (int64_t)row * g.N + n0 + c;
+                const float4 a = ldg4(zp), b = ldg4(zp + 4);
+                z[s2][0] = a.x; z[s2][1] = a.y; z[s2][2] = a.z; z[s2][3] = a.w;
+                z[s2][4] = b.x; z[s2][5] = b.y; z[s2][6] = b.z; z[s2][7] = b.w;
+            }
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float zz[S], hh[S], oo[S];
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) {
+                    zz[s2] = z[s2][j];
+                    hh[s2] = hb[s2][j];
+                }
+                act_bwd<L, ACT_TANH>(zz, hh, oo, 1.0f);
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) hb[s2][j] = oo[s2];
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) {
+                float* dst = g.out + s2 * RN + (int64_t)row * g.N + n0 + c;
+                *reinterpret_cast<float4*>(dst) = make_float4(hb[s2][0], hb[s2][1], hb[s2][2], hb[s2][3]);
+                *reinterpret_cast<float4*>(dst + 4) = make_float4(hb[s2][4], hb[s2][5], hb[s2][6], hb[s2][7]);
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 8) tc::tmem_dealloc<512>(tmem);
+}
+
 }  // namespace pnx

@@ -52,8 +52,8 @@ int launch_tc_layer(int L, int mode, int pro, const TcGemmArgs& g, cudaStream_t 
 
 template <int L, int PRO, int NF>
 int launch_tc2_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
-    using Cfg = Tc2FwdCfg<NF>;
-    const int smem = Cfg::NST * Cfg::STAGE + 1024;
+    using Cfg = Tc3FwdCfg<NF>;
+    const int smem = Cfg::SMEM;
     auto kern = k_tc2_fwd<L, PRO, NF>;
     static bool attr = false;
     if (!attr) {

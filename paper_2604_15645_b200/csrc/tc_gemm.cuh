@@ -546,6 +546,17 @@ inline void tc_workspace_free(TcWorkspace& ws) {
 // Roles (416 threads): warps 0-7 produce stages, warp 8 issues tcgen05.mma
 // (lane 0) and owns TMEM, warps 9-12 drain TMEM (epilogue; warp%4 = lane quarter).
 // ===========================================================================
+// Optional role-timing instrumentation (compile with -DPNX_TC_TRACE): per CTA,
+// [0] MMA waits on full stages, [1] MMA waits on TMEM-empty, [2] producer waits
+// on empty stages (warp 0), [3] epilogue busy cycles (warp 9), [4] kernel cycles.
+#ifdef PNX_TC_TRACE
+__device__ unsigned long long g_tc_trace[8];
+#define TC_T0() long long _t0 = clock64()
+#define TC_ACC(i) atomicAdd(&g_tc_trace[i], (unsigned long long)(clock64() - _t0))
+#else
+#define TC_T0()
+#define TC_ACC(i)
+#endif
 constexpr int TC2_THREADS = 416;
 constexpr int TC3_THREADS = 544;  // 8 producer + 1 MMA + 8 epilogue warps
 constexpr int TC2_PROD = 256;
@@ -559,14 +570,34 @@ struct Tc2FwdCfg {
     static constexpr int NBUF = 4 * NF <= 512 ? 2 : 1;  // TMEM buffers of (big | small)
 };
 
-// forward: Z_out[p] = act(Z_in)[p] W + [p==0] b, one stream p per pass
+// forward: Z_out[p] = act(Z_in)[p] W + [p==0] b, one stream p per pass.
+//
+// Memory access is organised around 128 B lines (the L1 request rate, not DRAM
+// bandwidth, bounded the first version): producers read a 32-feature group
+// (4 MMA k-steps) per row with 8 lanes per line and write it into four stages;
+// the epilogue transposes each warp's 32 rows x 32 columns through a padded
+// smem tile so global stores are full-line as well.
+template <int NF>
+struct Tc3FwdCfg {
+    static constexpr int A_T = TC_TILE_BYTES;
+    static constexpr int B_T = NF * 32;
+    static constexpr int STAGE = 2 * A_T + 2 * B_T;
+    static constexpr int EPI_ROW = 144;                     // 128 B + 16 B pad
+    static constexpr int EPI_BYTES = 8 * 32 * EPI_ROW;      // 8 epilogue warps
+    static constexpr int NST = (TC_SMEM + 20 * 1024 - 1024 - EPI_BYTES) / STAGE > 8
+                                   ? 8
+                                   : (TC_SMEM + 20 * 1024 - 1024 - EPI_BYTES) / STAGE;
+    static constexpr int NBUF = 4 * NF <= 512 ? 2 : 1;
+    static constexpr int SMEM = NST * STAGE + EPI_BYTES + 1024;
+};
+
 template <int L, int PRO, int NF>
 __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
     using St = Streams<L>;
     constexpr int S = St::S;
-    using Cfg = Tc2FwdCfg<NF>;
+    using Cfg = Tc3FwdCfg<NF>;
     constexpr int NST = Cfg::NST, NBUF = Cfg::NBUF;
-    constexpr int D = 3;  // register prefetch depth (stages)
+    constexpr bool SECOND = (St::order(S - 1) == 2);  // layout has order-2 streams
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     __shared__ uint64_t full[8], empty[8], tfull[2], tempty[2];
@@ -574,7 +605,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int r0 = blockIdx.x * TC_M;
-    const int nkb = g.K / 8, nit = S * nkb;
+    const int nkb = g.K / 8, ngrp = g.K / 32, nit = S * nkb;
     const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * NF;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
@@ -596,62 +627,100 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
 
     if (warp < 8) {
         // ---------------- producers ----------------
-        const int prow = tid >> 1, pc = tid & 1;
-        const float* rowp = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
-        const uint32_t aoff = tc::sw32_off((uint32_t)prow, (uint32_t)(pc * 4));
-        float4 ring[D][3];
-        auto load = [&](int it, float4* v) {
-            const int p = it / nkb, off = (it % nkb) * 8;
-            if constexpr (PRO == ACT_NONE) {
-                v[0] = ldg4(rowp + p * RK + off);
-            } else {
-                v[0] = ldg4(rowp + off);  // value stream (t)
-                if (p > 0) v[1] = ldg4(rowp + p * RK + off);
-                if (St::order(p) == 2) v[2] = ldg4(rowp + St::partner(p) * RK + off);
+        // lane -> (row quad offset rq = lane/8, 16 B chunk c = lane%8 of a 128 B
+        // group line); warp w covers rows 16w .. 16w+15 as rq + 4i, i = 0..3.
+        const int rq = lane >> 3, c = lane & 7;
+        const int j_own = c >> 1;           // k-step of the group this lane feeds
+        const int kc = (c & 1) * 4;         // feature offset inside the k-step
+        const float* base = g.A + (int64_t)(r0 + warp * 16 + rq) * g.K + c * 4;
+        uint32_t aoff[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) aoff[i] = tc::sw32_off((uint32_t)(warp * 16 + rq + 4 * i), (uint32_t)kc);
+        float4 t4[4], z4[4], p4[SECOND ? 4 : 1];
+        auto load = [&](int grp, float4* tt, float4* zz, float4* pp) {
+#ifdef PNX_EXP_NOLOAD
+#pragma unroll
+            for (int i = 0; i < 4; ++i) tt[i] = zz[i] = pp[SECOND ? i : 0] = make_float4(0.1f * grp, 0.2f, 0.3f, 0.4f);
+            return;
+#endif
+            const int p = grp / ngrp, off = (grp % ngrp) * 32;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float* q = base + (int64_t)(4 * i) * g.K + off;
+                if constexpr (PRO == ACT_NONE) {
+                    tt[i] = ldg4(q + p * RK);
+                } else {
+                    tt[i] = ldg4(q);
+                    if (p > 0) zz[i] = ldg4(q + p * RK);
+                    if constexpr (SECOND) {
+                        if (St::order(p) == 2) pp[i] = ldg4(q + St::partner(p) * RK);
+                    }
+                }
             }
         };
+        const int ngt = S * ngrp;
+        load(0, t4, z4, p4);
+        for (int gi = 0; gi < ngt; ++gi) {
+            float4 tc4[4], zc4[4], pc4[SECOND ? 4 : 1];
 #pragma unroll
-        for (int d = 0; d < D; ++d)
-            if (d < nit) load(d, ring[d]);
-        // unrolled by D so every ring slot index is a compile-time constant
-        for (int it0 = 0; it0 < nit; it0 += D) {
+            for (int i = 0; i < 4; ++i) {
+                tc4[i] = t4[i];
+                zc4[i] = z4[i];
+                if constexpr (SECOND) pc4[i] = p4[i];
+            }
+            if (gi + 1 < ngt) load(gi + 1, t4, z4, p4);  // prefetch one group (4 stages) ahead
+            const int p = gi / ngrp;
+            // activation + split for this lane's 4 rows (used at stage j_own)
+            float4 hi[4], lo[4];
 #pragma unroll
-            for (int slot = 0; slot < D; ++slot) {
-                const int it = it0 + slot;
-                if (it >= nit) break;
-                const int st = it % NST, p = it / nkb, kb = it % nkb;
-                const uint32_t stage = sbase + st * Cfg::STAGE;
-                float4 v[3];
-#pragma unroll
-                for (int j = 0; j < 3; ++j) v[j] = ring[slot][j];
-                if (it + D < nit) load(it + D, ring[slot]);
+            for (int i = 0; i < 4; ++i) {
                 float4 h;
                 if constexpr (PRO == ACT_NONE) {
-                    h = v[0];
+                    h = tc4[i];
                 } else {
-                    const float4 t = v[0];
+                    const float4 t = tc4[i], z = zc4[i];
                     if (p == 0) {
                         h = t;
                     } else if (St::order(p) == 1) {
-                        h = make_float4((1.f - t.x * t.x) * v[1].x, (1.f - t.y * t.y) * v[1].y,
-                                        (1.f - t.z * t.z) * v[1].z, (1.f - t.w * t.w) * v[1].w);
+                        h = make_float4((1.f - t.x * t.x) * z.x, (1.f - t.y * t.y) * z.y, (1.f - t.z * t.z) * z.z,
+                                        (1.f - t.w * t.w) * z.w);
                     } else {
-                        h = make_float4((1.f - t.x * t.x) * (v[1].x - 2.f * t.x * v[2].x * v[2].x),
-                                        (1.f - t.y * t.y) * (v[1].y - 2.f * t.y * v[2].y * v[2].y),
-                                        (1.f - t.z * t.z) * (v[1].z - 2.f * t.z * v[2].z * v[2].z),
-                                        (1.f - t.w * t.w) * (v[1].w - 2.f * t.w * v[2].w * v[2].w));
+                        float4 za = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if constexpr (SECOND) za = pc4[i];
+                        h = make_float4((1.f - t.x * t.x) * (z.x - 2.f * t.x * za.x * za.x),
+                                        (1.f - t.y * t.y) * (z.y - 2.f * t.y * za.y * za.y),
+                                        (1.f - t.z * t.z) * (z.z - 2.f * t.z * za.z * za.z),
+                                        (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
                     }
                 }
-                float4 hi, lo;
-                split4(h, hi, lo);
-                tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                split4(h, hi[i], lo[i]);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int it = gi * 4 + j, st = it % NST, kb = it % nkb;
+                const uint32_t stage = sbase + st * Cfg::STAGE;
+                {
+                    TC_T0();
+                    tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                    if (tid == 0) TC_ACC(2);
+                }
                 if (tid == 0) {
+#ifdef PNX_EXP_NOB
+                    tc::mbar_arrive(&full[st]);
+                    (void)kb;
+#else
                     tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
                     tc::bulk_g2s(stage + 2 * Cfg::A_T, g.img + (int64_t)kb * (2 * Cfg::B_T / 4), 2 * Cfg::B_T,
                                  &full[st]);
+#endif
                 }
-                sts128(stage + aoff, hi);
-                sts128(stage + Cfg::A_T + aoff, lo);
+                if (j == j_own) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        sts128(stage + aoff[i], hi[i]);
+                        sts128(stage + Cfg::A_T + aoff[i], lo[i]);
+                    }
+                }
                 tc::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&full[st]);
@@ -663,13 +732,21 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
             constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NF, 0, 0);
             for (int p = 0; p < S; ++p) {
                 const int buf = p % NBUF, use = p / NBUF;
-                tc::mbar_wait(&tempty[buf], ((uint32_t)use & 1u) ^ 1u);
+                {
+                    TC_T0();
+                    tc::mbar_wait(&tempty[buf], ((uint32_t)use & 1u) ^ 1u);
+                    TC_ACC(1);
+                }
                 tc::tc_fence_after();
                 const uint32_t dbig = tmem + (uint32_t)(buf * 2 * NF), dsmall = dbig + NF;
                 for (int kb = 0; kb < nkb; ++kb) {
                     const int it = p * nkb + kb, st = it % NST;
                     const uint32_t stage = sbase + st * Cfg::STAGE;
-                    tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                    {
+                        TC_T0();
+                        tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                        TC_ACC(0);
+                    }
                     tc::tc_fence_after();
                     const uint64_t ah = tc::make_sdesc(stage, 16, 256, 6), al = tc::make_sdesc(stage + Cfg::A_T, 16, 256, 6);
                     const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 16, 256, 6);
@@ -686,31 +763,51 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
     } else {
         // ---------------- epilogue (8 warps: lane quarter warp%4, column half) ----------------
         const int q = warp & 3, half = (warp - 9) >> 2;
-        const int row = r0 + q * 32 + lane;
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t stg = sbase + NST * Cfg::STAGE + (uint32_t)(warp - 9) * 32 * Cfg::EPI_ROW;
         for (int p = 0; p < S; ++p) {
             const int buf = p % NBUF, use = p / NBUF;
             tc::mbar_wait(&tfull[buf], (uint32_t)use & 1u);
             tc::tc_fence_after();
-            float* dst = g.out + p * RN + (int64_t)row * NF;
+            TC_T0();
 #pragma unroll 1
-            for (int c = half * (NF / 2); c < (half + 1) * (NF / 2); c += 16) {
-                float a[16], b[16];
+            for (int c = half * (NF / 2); c < (half + 1) * (NF / 2); c += 32) {
+                float a[32], b[32];
                 tc::tmem_ld16(tl + (uint32_t)(buf * 2 * NF + c), a);
+                tc::tmem_ld16(tl + (uint32_t)(buf * 2 * NF + c + 16), a + 16);
                 tc::tmem_ld16(tl + (uint32_t)(buf * 2 * NF + NF + c), b);
+                tc::tmem_ld16(tl + (uint32_t)(buf * 2 * NF + NF + c + 16), b + 16);
                 tc::tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 16; ++j) a[j] += b[j];
+                for (int j = 0; j < 32; ++j) a[j] += b[j];
                 if (p == 0) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));
+                    for (int j = 0; j < 32; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));
                 }
+                // row `lane` of this warp's 32 x 32 block -> padded smem
 #pragma unroll
-                for (int j = 0; j < 16; j += 4)
-                    *reinterpret_cast<float4*>(dst + c + j) = make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]);
+                for (int j = 0; j < 32; j += 4)
+                    sts128(stg + lane * Cfg::EPI_ROW + j * 4, make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]));
+                __syncwarp();
+                // full-line stores: instruction k writes rows 4k .. 4k+3 (8 lanes x 16 B each)
+                float* dst = g.out + p * RN + (int64_t)(r0 + q * 32) * NF + c;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int rr = 4 * k + (lane >> 3), cc = (lane & 7) * 4;
+                    float4 v;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                 : "r"(stg + rr * Cfg::EPI_ROW + cc * 4));
+#ifdef PNX_EXP_NOSTORE
+                    if (v.x == 12345.f)
+#endif
+                    *reinterpret_cast<float4*>(dst + (int64_t)rr * NF + cc) = v;
+                }
+                __syncwarp();
             }
             tc::tc_fence_before();
             __syncwarp();
+            if (warp == 9 && lane == 0) TC_ACC(3);
             if (lane == 0) tc::mbar_arrive(&tempty[buf]);
         }
     }

@@ -274,28 +274,20 @@ def main():
     worker = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, shard, col["ic_points"], col["ic_targets"],
                             col["bc_a"], col["bc_b"], col["bc_targets"], device=local, engine=args.engine)
     P = worker.n_params
-    params = torch.tensor(flat, dtype=torch.float32, device=dev)
-    grad = torch.zeros(P, dtype=torch.float32, device=dev)
-    m = torch.zeros_like(params)
-    v = torch.zeros_like(params)
-    losses = torch.zeros(3, dtype=torch.float64, device=dev)
+    from paper_2604_15645_b200.dist import DataParallelTrainer
+    trainer = DataParallelTrainer(worker, flat, world=world, lr=1e-3, device=dev)
     stream = torch.cuda.current_stream(dev)
     st = stream.cuda_stream
     lam = (1.0, 1.0, 1.0)
-    t_adam = [0]
 
-    def step():
-        worker.step_device(params, grad, lam, losses, stream=st)
-        if world > 1:
-            dist.all_reduce(grad, op=dist.ReduceOp.SUM)
-        t_adam[0] += 1
-        worker.adam_step_device(params, grad, m, v, t_adam[0], 1e-3, grad_scale=1.0 / world, stream=st)
+    def step():  # device step -> NCCL all-reduce of the flat gradient -> fused Adam(1/W)
+        trainer.step(lam, stream=st)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     worker.check()
-    launches_per_step = worker.launch_count() + 1
+    launches_per_step = worker.launch_count() + 1  # + the fused Adam kernel
 
     # ---- timed region (device-resident inputs) ----
     clk = ClockSampler(local)
@@ -372,23 +364,42 @@ def main():
             peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         except Exception:
             pass
-        # roofline of the dominant kernel class (CUDA events on the launching stream)
+        # roofline of the dominant kernel class (CUDA events on the launching stream):
+        # algorithmic flops of that class per step (2*S*rows*sum K*N over its
+        # layers) / its measured ms per step.
         S = wl.streams()
         H = wl.spec.hidden_dim
         rows = hi - lo
-        hidden_gemms = wl.spec.depth - 1  # H x H layers per pass
-        flops_cls = {"fwd_gemm": 2.0 * S * rows * (H * H * hidden_gemms + wl.spec.first_layer_width() * H),
-                     "bwd_gemm": 2.0 * S * rows * H * H * hidden_gemms,
-                     "wgrad_gemm": 2.0 * S * rows * (H * H * hidden_gemms + wl.spec.first_layer_width() * H)}
+        K0 = wl.spec.first_layer_width()
+        sum_fwd = K0 * H + H * H * (wl.spec.depth - 1)      # layers 0..depth-1 (head excluded)
+        sum_bwd = H * H * (wl.spec.depth - 1)               # reverse GEMMs of layers 1..depth-1
+        flops_cls = {"fwd_gemm": 2.0 * S * rows * sum_fwd, "bwd_gemm": 2.0 * S * rows * sum_bwd,
+                     "wgrad_gemm": 2.0 * S * rows * sum_fwd}
         dom = max(flops_cls, key=lambda k: prof[k][0])
         tms, nl = prof[dom]
-        per_launch_flops = flops_cls[dom] / max(1, nl / args.steps)
-        avg_launch_s = tms / max(nl, 1) / 1e3
-        achieved = per_launch_flops / avg_launch_s / 1e12
-        use_tc = args.engine == "tc3xtf32" or (args.engine == "auto" and H >= 128)
+        achieved = flops_cls[dom] * args.steps / (tms / 1e3) / 1e12
+        use_tc = args.engine != "ffma" and H in (128, 256) and wl.spec.activation == "tanh"
+        bf16 = float(peaks.get("bf16_tflops_sustained", 1366.2))
         fp32_peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
-        peak = fp32_peak
-        peak_note = "FP32 FFMA peak 148 SM x 128 x 2 x sm_max_mhz (derived from MEASURED_PEAKS.json clocks)"
+        if use_tc:
+            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                    "frac": achieved / bf16,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense bf16, of measured)",
+                    "effective_peak": bf16 / 6.0, "frac_effective": achieved / (bf16 / 6.0),
+                    "effective_note": "3xTF32: tensor-pipe work = 3 x algorithmic flops at the TF32 rate "
+                                      "(= bf16/2), so FP32-accurate peak = bf16/6 (derived)"}
+        else:
+            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp32_peak,
+                    "peak_source": "FP32 FFMA pipe: 148 SM x 128 lanes x 2 x sm_max_mhz (derived)"}
+        traffic_db = {}
+        try:
+            traffic_db = json.load(open(os.path.join(ROOT, "profiles", "kernel_traffic.json")))
+        except Exception:
+            pass
+        key = f"{name}:{dom}"
+        roof["traffic"] = traffic_db.get(key)
+        roof["launches_per_step"] = nl / args.steps
         step_flops = wl.flops_per_point() * n_total
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -400,10 +411,7 @@ def main():
                        "params": P, "engine": args.engine, "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (per-step activations >> 126 MB)"},
             "tflops_step": step_flops / (ms_step / 1e3) / 1e12,
-            "roofline": {"bound": "tensor" if use_tc else "fp32", "kernel": dom, "achieved": achieved,
-                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                         "peak_source": peak_note,
-                         "per_launch_flops": per_launch_flops, "avg_launch_ms": avg_launch_s * 1e3},
+            "roofline": roof,
             "kernel_ms_per_step": {k: prof[k][0] / args.steps for k in prof},
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clocks,

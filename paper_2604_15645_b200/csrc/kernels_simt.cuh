@@ -191,6 +191,145 @@ static __global__ void k_input(InputArgs a) {
     }
 }
 
+// Layer 0 for narrow embeddings (no RFF, K0 <= 8) fused with the input jets:
+// Z0[s] = e[s] W0 + [s==0] b0 with e recomputed in float64 per row; no Hin in HBM.
+constexpr int L0_ROWS = 32;
+
+template <int L, int ACT>
+__global__ void __launch_bounds__(256) k_layer0_fwd(InputArgs a, const float* __restrict__ W0,
+                                                   const float* __restrict__ b0, float* __restrict__ Z0, int H) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    __shared__ float E[L0_ROWS][S][2 * kMaxAxes];
+    __shared__ float Ws[2 * kMaxAxes * 512];
+    const int K0 = a.E;
+    for (int i = threadIdx.x; i < K0 * H; i += blockDim.x) Ws[i] = W0[i];
+    const int64_t RH = (int64_t)a.Rpad * H;
+    for (int rb = blockIdx.x * L0_ROWS; rb < a.Rpad; rb += gridDim.x * L0_ROWS) {
+        __syncthreads();
+        if (threadIdx.x < L0_ROWS) {
+            const int r = rb + threadIdx.x;
+            if (r < a.nrows) {
+                double e[S][2 * kMaxAxes];
+                embed_row<L>(a, a.row0 + r, e);
+                for (int s = 0; s < S; ++s)
+                    for (int k = 0; k < K0; ++k) E[threadIdx.x][s][k] = (float)e[s][k];
+            } else {
+                for (int s = 0; s < S; ++s)
+                    for (int k = 0; k < K0; ++k) E[threadIdx.x][s][k] = 0.0f;
+            }
+        }
+        __syncthreads();
+        const int nch = H / 4;
+        for (int item = threadIdx.x; item < L0_ROWS * nch; item += blockDim.x) {
+            const int rr = item / nch, n = (item % nch) * 4;
+            float z[S][4];
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) z[s][j] = 0.0f;
+            for (int k = 0; k < K0; ++k) {
+                const float4 w = *reinterpret_cast<const float4*>(&Ws[k * H + n]);
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const float e = E[rr][s][k];
+                    z[s][0] = fmaf(e, w.x, z[s][0]);
+                    z[s][1] = fmaf(e, w.y, z[s][1]);
+                    z[s][2] = fmaf(e, w.z, z[s][2]);
+                    z[s][3] = fmaf(e, w.w, z[s][3]);
+                }
+            }
+            const float4 bb = *reinterpret_cast<const float4*>(b0 + n);
+            z[0][0] = store_value<ACT>(z[0][0] + bb.x);
+            z[0][1] = store_value<ACT>(z[0][1] + bb.y);
+            z[0][2] = store_value<ACT>(z[0][2] + bb.z);
+            z[0][3] = store_value<ACT>(z[0][3] + bb.w);
+            float* dst = Z0 + (int64_t)(rb + rr) * H + n;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                *reinterpret_cast<float4*>(dst + s * RH) = make_float4(z[s][0], z[s][1], z[s][2], z[s][3]);
+        }
+    }
+}
+
+// Layer-0 weight gradient for narrow embeddings: part[blk][k*H + n] +=
+// sum_rows sum_s e[s][row][k] Zb0[s][row][n], part[blk][K0*H + n] += sum_rows Zb0[0][row][n].
+// Streams Zb0 once (coalesced), recomputes e; FP32 per 32-row tile, FP64 across tiles.
+template <int L>
+__global__ void __launch_bounds__(256) k_layer0_wgrad(InputArgs a, const float* __restrict__ Zb0, int H,
+                                                     double* __restrict__ part) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    constexpr int KM = 2 * kMaxAxes;
+    __shared__ float E[L0_ROWS][S][KM];
+    __shared__ double red[KM + 1][512];
+    const int K0 = a.E;
+    const int nch = H / 4;           // <= 128 chunks (H <= 512)
+    const int lanes = 256 / nch;     // row lanes per block (H=256: 4)
+    const int rl = threadIdx.x / nch, c = threadIdx.x % nch, n = c * 4;
+    const bool active = rl < lanes && c < nch;
+    double acc[KM + 1][4];
+#pragma unroll
+    for (int k = 0; k <= KM; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[k][j] = 0.0;
+    const int64_t RH = (int64_t)a.Rpad * H;
+    for (int rb = blockIdx.x * L0_ROWS; rb < a.nrows; rb += gridDim.x * L0_ROWS) {
+        __syncthreads();
+        if (threadIdx.x < L0_ROWS) {
+            const int r = rb + threadIdx.x;
+            double e[S][2 * kMaxAxes];
+            if (r < a.nrows) embed_row<L>(a, a.row0 + r, e);
+            for (int s = 0; s < S; ++s)
+                for (int k = 0; k < K0; ++k) E[threadIdx.x][s][k] = r < a.nrows ? (float)e[s][k] : 0.0f;
+        }
+        __syncthreads();
+        if (!active) continue;
+        float t32[KM + 1][4];
+#pragma unroll
+        for (int k = 0; k <= KM; ++k)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) t32[k][j] = 0.0f;
+        for (int rr = rl; rr < L0_ROWS; rr += lanes) {
+            const int r = rb + rr;
+            if (r >= a.nrows) break;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const float4 z = *reinterpret_cast<const float4*>(Zb0 + s * RH + (int64_t)r * H + n);
+                if (s == 0) {
+                    t32[KM][0] += z.x; t32[KM][1] += z.y; t32[KM][2] += z.z; t32[KM][3] += z.w;
+                }
+#pragma unroll
+                for (int k = 0; k < KM; ++k) {
+                    if (k >= K0) break;
+                    const float e = E[rr][s][k];
+                    t32[k][0] = fmaf(e, z.x, t32[k][0]);
+                    t32[k][1] = fmaf(e, z.y, t32[k][1]);
+                    t32[k][2] = fmaf(e, z.z, t32[k][2]);
+                    t32[k][3] = fmaf(e, z.w, t32[k][3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k <= KM; ++k)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[k][j] += (double)t32[k][j];
+    }
+    // fixed-order reduction over the row lanes (lane 0 first), then one partial per block
+    for (int l2 = 0; l2 < lanes; ++l2) {
+        __syncthreads();
+        if (active && rl == l2)
+            for (int k = 0; k <= KM; ++k)
+                for (int j = 0; j < 4; ++j) red[k][c * 4 + j] = (l2 == 0 ? 0.0 : red[k][c * 4 + j]) + acc[k][j];
+    }
+    __syncthreads();
+    double* dst = part + (int64_t)blockIdx.x * ((int64_t)K0 * H + H);
+    for (int i = threadIdx.x; i < (K0 + 1) * H; i += blockDim.x) {
+        const int k = i / H, nn = i % H;
+        dst[(int64_t)k * H + nn] += red[k < K0 ? k : KM][nn];
+    }
+}
+
 // Trainable-period gradient: given Hbar_in [S][Rpad][K0] (adjoint of the input
 // features), back through RFF (B frozen) and the embedding to each trainable
 // period: d phi/dP = -phi/P, d kappa/dP = -kappa/P.

@@ -1,4 +1,6 @@
 // launch_simt.cu -- dispatch of the FP32 CUDA-core (FFMA) kernels.
+#include <algorithm>
+
 #include "launch.h"
 
 namespace pnx {
@@ -106,6 +108,34 @@ void launch_head(int pde, int act, const HeadArgs& h, int grid, cudaStream_t st)
         case PDE_BURGERS: launch_head_p<PDE_BURGERS>(act, h, grid, st); break;
         case PDE_MAXWELL: launch_head_p<PDE_MAXWELL>(act, h, grid, st); break;
         case PDE_NS: launch_head_p<PDE_NS>(act, h, grid, st); break;
+    }
+}
+
+template <int L>
+void launch_layer0_fwd_l(int act, const InputArgs& a, const float* W0, const float* b0, float* Z0, int H,
+                         cudaStream_t st) {
+    const int grid = std::min(148 * 8, (a.Rpad + L0_ROWS - 1) / L0_ROWS);
+    switch (act) {
+        case ACT_TANH: k_layer0_fwd<L, ACT_TANH><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H); break;
+        case ACT_SINE: k_layer0_fwd<L, ACT_SINE><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H); break;
+        default: k_layer0_fwd<L, ACT_SWISH><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H); break;
+    }
+}
+void launch_layer0_fwd(int L, int act, const InputArgs& a, const float* W0, const float* b0, float* Z0, int H,
+                       cudaStream_t st) {
+    switch (L) {
+        case LAY_XT: launch_layer0_fwd_l<LAY_XT>(act, a, W0, b0, Z0, H, st); break;
+        case LAY_AC: launch_layer0_fwd_l<LAY_AC>(act, a, W0, b0, Z0, H, st); break;
+        case LAY_MX: launch_layer0_fwd_l<LAY_MX>(act, a, W0, b0, Z0, H, st); break;
+        case LAY_NS: launch_layer0_fwd_l<LAY_NS>(act, a, W0, b0, Z0, H, st); break;
+    }
+}
+void launch_layer0_wgrad(int L, const InputArgs& a, const float* Zb0, int H, double* part, int grid, cudaStream_t st) {
+    switch (L) {
+        case LAY_XT: k_layer0_wgrad<LAY_XT><<<grid, 256, 0, st>>>(a, Zb0, H, part); break;
+        case LAY_AC: k_layer0_wgrad<LAY_AC><<<grid, 256, 0, st>>>(a, Zb0, H, part); break;
+        case LAY_MX: k_layer0_wgrad<LAY_MX><<<grid, 256, 0, st>>>(a, Zb0, H, part); break;
+        case LAY_NS: k_layer0_wgrad<LAY_NS><<<grid, 256, 0, st>>>(a, Zb0, H, part); break;
     }
 }
 

@@ -179,6 +179,10 @@ int pde_layout(int pde) {
 
 // ---- buffers ---------------------------------------------------------------
 
+constexpr int kL0Blocks = 296;
+// layer 0 fused with the input jets (narrow embedding: no RFF, K0 <= 8, H % 4 == 0)
+bool layer0_fused(const pnx_ctx* c) { return c->rff_w == 0 && c->K0 <= 8 && c->H % 4 == 0 && c->H <= 512; }
+
 int64_t bytes_per_row(const pnx_ctx* c) {
     int64_t f = (int64_t)c->S * (c->K0 + (int64_t)c->depth * c->H + 2LL * c->H + (c->train_period ? c->K0 : 0));
     return f * 4;
@@ -249,6 +253,7 @@ int upload_rows(pnx_ctx* ctx) {
         const int tiles = (int)(((ctx->tab.N[l] + 63) / 64) * ((ctx->tab.K[l] + 63) / 64));
         int ns = std::max(1, std::min(256, (4 * 148 + tiles - 1) / tiles));
         ns = (int)std::min<int64_t>(ns, std::max<int64_t>(1, ch / 256));
+        if (l == 0 && layer0_fused(ctx)) ns = kL0Blocks;
         ctx->nsplit[l] = ns;
         if (int r = dalloc(ctx, &ctx->d_part[l], (size_t)ns * (ctx->tab.K[l] * (size_t)ctx->tab.N[l] + ctx->tab.N[l]))) return r;
     }
@@ -348,10 +353,13 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         ia.row0 = c0;
         ia.nrows = nrows;
         ia.Rpad = Rpad;
-        prof_begin(ctx, PC_INPUT, st);
-        launch_input(L, ia, st);
-        prof_end(ctx, st);
-        CKL();
+        const bool fuse0 = layer0_fused(ctx);
+        if (!fuse0) {
+            prof_begin(ctx, PC_INPUT, st);
+            launch_input(L, ia, st);
+            prof_end(ctx, st);
+            CKL();
+        }
         // forward layers
         for (int l = 0; l < ctx->depth; ++l) {
             GemmArgs g{};
@@ -365,7 +373,10 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             g.w0 = ctx->w0;
             const int pro = l == 0 ? ACT_NONE : act;
             prof_begin(ctx, PC_FWD, st);
-            if (tc_fwd[l] && (tc_mask & 1)) {
+            if (l == 0 && fuse0) {
+                launch_layer0_fwd(L, act, ia, g.B, g.bias, g.out, g.N, st);
+                CKL();
+            } else if (tc_fwd[l] && (tc_mask & 1)) {
                 TcGemmArgs tg{};
                 tg.A = g.A;
                 tg.img = ctx->tc.img + ctx->tc.img_fwd[l];
@@ -434,7 +445,10 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             w.w0 = ctx->w0;
             const int pro = l == 0 ? ACT_NONE : act;
             prof_begin(ctx, PC_WGRAD, st);
-            if (tc_wg[l]) {
+            if (l == 0 && fuse0) {
+                launch_layer0_wgrad(L, ia, w.Bm, t.N[0], ctx->d_part[0], kL0Blocks, st);
+                CKL();
+            } else if (tc_wg[l]) {
                 TcWgradArgs tw{};
                 tw.A = w.A;
                 tw.Bm = w.Bm;

@@ -323,14 +323,14 @@ def main():
         host_params = flat.copy()
         opt_m = np.zeros_like(host_params)
         opt_v = np.zeros_like(host_params)
-        shard_pinned = torch.from_numpy(np.ascontiguousarray(shard)).pin_memory()
+        shard_pinned = torch.from_numpy(np.ascontiguousarray(shard.T)).pin_memory()  # axis-major [d, N]
         g_dev = torch.zeros(P, dtype=torch.float64, device=dev)
         h2d = d2h = 0
 
         def e2e_step(k):
             nonlocal h2d, d2h
             pts = shard_pinned.numpy()
-            worker.set_points(pts)                      # H2D of this step's collocation batch
+            worker.set_points(pts, axis_major=True)     # H2D of this step's collocation batch
             g_host, l = worker.step(host_params, lam)   # H2D params, D2H grad + losses
             if world > 1:
                 g_dev.copy_(torch.from_numpy(g_host))

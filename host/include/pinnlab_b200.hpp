@@ -1,0 +1,184 @@
+// pinnlab_b200.hpp -- C++ host API mirroring the reference pinnlab core
+// (/root/reference/proj/core/include/pinnlab) for the train-step path, with the
+// per-worker step executed by libpnx (include/pnx.h) on B200s.
+//
+// Same names, argument meaning and error behaviour as the reference:
+//   ModelSpec / AxisPeriodic / RFFSpec / RWFSpec      model.hpp:14-57
+//   Model (init draws, trainable() order)             model.cpp:52-102
+//   ResidualSpec / PdeId                              losses.hpp:14-30
+//   Domain, linspace, sample_uniform                  sampling.hpp:13-36
+//   TrainingProblem, CollocationConfig, TrainConfig   trainer.hpp:17-86
+//   build_collocation (uniform mode)                  trainer.cpp:47-128
+//   data_parallel_gradient                            trainer.hpp:118-119
+//   train (Adam phase, balancing off)                 trainer.cpp:332-555
+//   param_hash                                        trainer.cpp:22-35
+// Errors are thrown as pinnlab_b200::TensorError with the reference's text.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace pinnlab_b200 {
+
+class TensorError : public std::runtime_error {
+public:
+    explicit TensorError(const std::string& what) : std::runtime_error(what) {}
+};
+
+enum class Activation { tanh, sine, swish };
+
+struct RFFSpec {
+    std::size_t width = 64;
+    double sigma = 10.0;
+    double mean = 0.0;
+};
+struct RWFSpec {
+    double mean = 1.0;
+    double stddev = 0.1;
+};
+struct AxisPeriodic {
+    bool periodic = false;
+    double period = 0.0;
+    bool trainable = false;
+};
+
+struct ModelSpec {
+    std::size_t in_dim = 2;
+    std::size_t hidden_dim = 64;
+    std::size_t depth = 3;
+    std::size_t out_dim = 1;
+    Activation activation = Activation::tanh;
+    double sine_w0 = 1.0;
+    std::vector<AxisPeriodic> periodic_axes;
+    std::optional<RFFSpec> rff;
+    std::optional<RWFSpec> rwf;
+
+    std::size_t embedded_width() const;
+    std::size_t first_layer_width() const;
+    void validate() const;
+};
+
+// Row-major float64 tensor of rank 0..2 (tensor.hpp:19-109, reduced to storage).
+struct Tensor {
+    std::vector<std::size_t> shape;
+    std::vector<double> data;
+    std::size_t size() const { return data.size(); }
+};
+
+struct NamedTensor {
+    std::string name;
+    Tensor value;
+};
+
+class Model {
+public:
+    Model(ModelSpec spec, std::uint64_t seed);
+    const ModelSpec& spec() const { return spec_; }
+    std::vector<NamedTensor>& trainable() { return params_; }
+    const std::vector<NamedTensor>& trainable() const { return params_; }
+    const Tensor& rff_matrix() const { return rff_B_; }
+    std::size_t trainable_count() const;
+
+private:
+    ModelSpec spec_;
+    std::vector<NamedTensor> params_;
+    Tensor rff_B_;
+};
+
+enum class PdeId { advection, allen_cahn, burgers, maxwell_te, ns_steady };
+
+struct ResidualSpec {
+    PdeId id = PdeId::advection;
+    double advection_c = 1.0;
+    double epsilon = 1.0;
+    double mu = 1.0;
+    double reynolds = 100.0;  // ns_steady extension
+
+    std::size_t field_count() const { return (id == PdeId::maxwell_te || id == PdeId::ns_steady) ? 3 : 1; }
+    std::size_t coord_count() const { return id == PdeId::maxwell_te ? 3 : 2; }
+};
+
+struct Points {
+    std::vector<std::vector<double>> coords;  // one column per axis
+    std::size_t count() const { return coords.empty() ? 0 : coords[0].size(); }
+};
+
+struct Domain {
+    std::vector<std::array<double, 2>> bounds;
+    std::size_t dim() const { return bounds.size(); }
+};
+
+std::vector<double> linspace(double lo, double hi, std::size_t n);
+Points sample_uniform(const Domain& dom, std::span<const std::size_t> dims);
+
+struct TrainingProblem {
+    ResidualSpec residual;
+    Domain domain;
+    std::function<std::vector<double>(std::span<const double>)> initial;
+    enum class Bc { hard, soft_periodic, dirichlet_zero };
+    Bc bc = Bc::hard;
+};
+
+struct CollocationConfig {
+    std::vector<std::size_t> dims;  // uniform grid
+    std::size_t n_ic = 128;
+    std::size_t n_bc = 64;
+};
+
+struct CollocationData {
+    Points interior;
+    Points ic_points;
+    std::vector<std::vector<double>> ic_targets;  // one column per field
+    Points bc_a, bc_b;
+    std::vector<std::vector<double>> bc_targets;
+};
+CollocationData build_collocation(const TrainingProblem& prob, const CollocationConfig& cc, std::uint64_t seed);
+
+struct AdamConfig {
+    double lr = 1e-3;
+    double beta1 = 0.9;
+    double beta2 = 0.999;
+    double eps = 1e-8;
+};
+
+struct TrainConfig {
+    long epochs = 1000;
+    std::uint64_t seed = 0;
+    int workers = 1;
+    AdamConfig adam;
+    double scheduler_gamma = 1.0;
+    CollocationConfig collocation;
+    std::array<double, 3> lambdas{1.0, 1.0, 1.0};  // fixed weights (balancing off)
+    int device = 0;                                 // first CUDA device; worker w uses device + w % ndev
+    std::function<void(long epoch, std::span<const std::uint64_t>)> on_sync;
+};
+
+struct MetricsRecord {
+    long epoch = 0;
+    double l_pde = 0.0, l_ic = 0.0, l_bc = 0.0;
+    double lr = 0.0;
+};
+struct TrainResult {
+    std::vector<MetricsRecord> metrics;
+    long epochs_run = 0;
+    bool aborted = false;
+    std::string abort_reason;
+};
+
+// One data-parallel gradient evaluation (shard, per-worker step, rank-ordered
+// average), returned aligned with Model::trainable().
+std::vector<Tensor> data_parallel_gradient(Model& model, const TrainingProblem& prob, const TrainConfig& cfg,
+                                           int workers);
+
+// Adam training loop with fixed loss weights; the per-worker step runs on the GPU.
+TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& cfg);
+
+std::uint64_t param_hash(const std::vector<NamedTensor>& params);
+
+}  // namespace pinnlab_b200

@@ -1,0 +1,413 @@
+// pinnlab_b200.cpp -- C++ host mirror of the reference pinnlab API over libpnx.
+// See host/include/pinnlab_b200.hpp for the reference file:line map.
+#include "pinnlab_b200.hpp"
+
+#include <cmath>
+#include <memory>
+#include <numbers>
+#include <random>
+#include <thread>
+
+#include "../../include/pnx.h"
+
+namespace pinnlab_b200 {
+
+// ---------------------------------------------------------------------------
+// ModelSpec / Model (model.cpp:14-108)
+// ---------------------------------------------------------------------------
+
+std::size_t ModelSpec::embedded_width() const {
+    if (periodic_axes.empty()) return in_dim;
+    std::size_t w = 0;
+    for (const auto& ax : periodic_axes) w += ax.periodic ? 2 : 1;
+    return w;
+}
+
+std::size_t ModelSpec::first_layer_width() const { return rff ? 2 * rff->width : embedded_width(); }
+
+void ModelSpec::validate() const {
+    if (in_dim == 0 || hidden_dim == 0 || depth == 0 || out_dim == 0)
+        throw TensorError("ModelSpec: dimensions must be positive");
+    if (!periodic_axes.empty() && periodic_axes.size() != in_dim)
+        throw TensorError("ModelSpec: periodic_axes must have one entry per input axis");
+    for (const auto& ax : periodic_axes)
+        if (ax.periodic && !(ax.period > 0.0)) throw TensorError("ModelSpec: periodic axis needs a positive period");
+    if (rff && rff->width == 0) throw TensorError("ModelSpec: rff width must be positive");
+}
+
+namespace {
+
+// Same engine and distributions as the reference Rng (rng.hpp:10-27): one
+// fresh std::normal_distribution per draw, so libstdc++ reproduces its values.
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed) : engine_(seed) {}
+    double normal(double mean, double stddev) { return std::normal_distribution<double>(mean, stddev)(engine_); }
+
+private:
+    std::mt19937_64 engine_;
+};
+
+}  // namespace
+
+Model::Model(ModelSpec spec, std::uint64_t seed) : spec_(std::move(spec)) {
+    spec_.validate();
+    Rng rng(seed);
+    if (spec_.rff) {  // frozen RFF frequencies drawn first (model.cpp:58-62)
+        rff_B_.shape = {spec_.embedded_width(), spec_.rff->width};
+        rff_B_.data.resize(spec_.embedded_width() * spec_.rff->width);
+        for (auto& v : rff_B_.data) v = rng.normal(spec_.rff->mean, spec_.rff->sigma);
+    }
+    auto make_layer = [&](std::size_t in, std::size_t out, std::size_t index) {
+        const double xavier = std::sqrt(2.0 / static_cast<double>(in + out));
+        Tensor W{{in, out}, std::vector<double>(in * out)};
+        for (auto& v : W.data) v = rng.normal(0.0, xavier);
+        const std::string base = "layer" + std::to_string(index) + ".";
+        if (spec_.rwf) {
+            params_.push_back({base + "V", std::move(W)});
+            Tensor s{{1, out}, std::vector<double>(out)};
+            for (auto& v : s.data) v = rng.normal(spec_.rwf->mean, spec_.rwf->stddev);
+            params_.push_back({base + "s", std::move(s)});
+        } else {
+            params_.push_back({base + "W", std::move(W)});
+        }
+        params_.push_back({base + "b", Tensor{{1, out}, std::vector<double>(out, 0.0)}});
+    };
+    std::size_t in = spec_.first_layer_width();
+    for (std::size_t l = 0; l < spec_.depth; ++l) {
+        make_layer(in, spec_.hidden_dim, l);
+        in = spec_.hidden_dim;
+    }
+    make_layer(in, spec_.out_dim, spec_.depth);
+    for (std::size_t a = 0; a < spec_.periodic_axes.size(); ++a) {
+        const auto& ax = spec_.periodic_axes[a];
+        if (ax.periodic && ax.trainable)
+            params_.push_back({"periodic.P" + std::to_string(a), Tensor{{}, std::vector<double>{ax.period}}});
+    }
+}
+
+std::size_t Model::trainable_count() const {
+    std::size_t n = 0;
+    for (const auto& p : params_) n += p.value.size();
+    return n;
+}
+
+// ---------------------------------------------------------------------------
+// sampling (sampling.cpp:10-54) and collocation (trainer.cpp:47-128)
+// ---------------------------------------------------------------------------
+
+std::vector<double> linspace(double lo, double hi, std::size_t n) {
+    std::vector<double> v(n);
+    if (n == 1) {
+        v[0] = lo;
+        return v;
+    }
+    const double h = (hi - lo) / static_cast<double>(n - 1);
+    for (std::size_t i = 0; i < n; ++i) v[i] = lo + static_cast<double>(i) * h;
+    v[n - 1] = hi;
+    return v;
+}
+
+Points sample_uniform(const Domain& dom, std::span<const std::size_t> dims) {
+    if (dims.size() != dom.dim()) throw TensorError("sample_uniform: dims/domain mismatch");
+    std::size_t total = 1;
+    std::vector<std::vector<double>> axes(dom.dim());
+    for (std::size_t a = 0; a < dom.dim(); ++a) {
+        if (dims[a] == 0) throw TensorError("sample_uniform: zero points on an axis");
+        axes[a] = linspace(dom.bounds[a][0], dom.bounds[a][1], dims[a]);
+        total *= dims[a];
+    }
+    Points pts;
+    pts.coords.assign(dom.dim(), std::vector<double>(total));
+    for (std::size_t idx = 0; idx < total; ++idx) {  // last axis fastest
+        std::size_t rem = idx;
+        for (std::size_t a = dom.dim(); a-- > 0;) {
+            pts.coords[a][idx] = axes[a][rem % dims[a]];
+            rem /= dims[a];
+        }
+    }
+    return pts;
+}
+
+CollocationData build_collocation(const TrainingProblem& prob, const CollocationConfig& cc, std::uint64_t) {
+    const Domain& dom = prob.domain;
+    const std::size_t d = dom.dim();
+    if (d < 2) throw TensorError("build_collocation: need at least one spatial axis plus time");
+    CollocationData data;
+    data.interior = sample_uniform(dom, cc.dims);
+    const std::size_t spatial = d - 1;
+    Points ic;
+    if (spatial == 1) {
+        ic.coords.push_back(linspace(dom.bounds[0][0], dom.bounds[0][1], cc.n_ic));
+    } else {
+        const auto per_axis = static_cast<std::size_t>(
+            std::ceil(std::pow(static_cast<double>(cc.n_ic), 1.0 / static_cast<double>(spatial))));
+        Domain sdom{std::vector<std::array<double, 2>>(dom.bounds.begin(), dom.bounds.end() - 1)};
+        std::vector<std::size_t> dims(spatial, per_axis);
+        ic = sample_uniform(sdom, dims);
+    }
+    const std::size_t n_ic = ic.coords[0].size();
+    ic.coords.push_back(std::vector<double>(n_ic, 0.0));  // t = 0
+    data.ic_points = std::move(ic);
+    const std::size_t fields = prob.residual.field_count();
+    data.ic_targets.assign(fields, std::vector<double>(n_ic));
+    std::vector<double> xbuf(spatial);
+    for (std::size_t i = 0; i < n_ic; ++i) {
+        for (std::size_t a = 0; a < spatial; ++a) xbuf[a] = data.ic_points.coords[a][i];
+        std::vector<double> vals = prob.initial(xbuf);
+        if (vals.size() != fields) throw TensorError("build_collocation: initial() field count mismatch");
+        for (std::size_t f = 0; f < fields; ++f) data.ic_targets[f][i] = vals[f];
+    }
+    if (prob.bc != TrainingProblem::Bc::hard) {
+        const auto ts = linspace(dom.bounds[d - 1][0], dom.bounds[d - 1][1], cc.n_bc);
+        auto trace = [&](double xval) {
+            Points p;
+            p.coords.push_back(std::vector<double>(cc.n_bc, xval));
+            for (std::size_t a = 1; a < spatial; ++a)
+                p.coords.push_back(std::vector<double>(cc.n_bc, 0.5 * (dom.bounds[a][0] + dom.bounds[a][1])));
+            p.coords.push_back(ts);
+            return p;
+        };
+        data.bc_a = trace(dom.bounds[0][0]);
+        data.bc_b = trace(dom.bounds[0][1]);
+        if (prob.bc == TrainingProblem::Bc::dirichlet_zero) {
+            Points both;
+            for (std::size_t a = 0; a < d; ++a) {
+                std::vector<double> col(2 * cc.n_bc);
+                for (std::size_t i = 0; i < cc.n_bc; ++i) {
+                    col[i] = data.bc_a.coords[a][i];
+                    col[cc.n_bc + i] = data.bc_b.coords[a][i];
+                }
+                both.coords.push_back(std::move(col));
+            }
+            data.bc_a = std::move(both);
+            data.bc_b = Points{};
+            data.bc_targets.assign(fields, std::vector<double>(2 * cc.n_bc, 0.0));
+        }
+    }
+    return data;
+}
+
+std::uint64_t param_hash(const std::vector<NamedTensor>& params) {
+    std::uint64_t h = 1469598103934665603ULL;
+    auto mix = [&h](const unsigned char* p, std::size_t n) {
+        for (std::size_t i = 0; i < n; ++i) {
+            h ^= p[i];
+            h *= 1099511628211ULL;
+        }
+    };
+    for (const auto& p : params) {
+        mix(reinterpret_cast<const unsigned char*>(p.name.data()), p.name.size());
+        mix(reinterpret_cast<const unsigned char*>(p.value.data.data()), p.value.data.size() * 8);
+    }
+    return h;
+}
+
+// ---------------------------------------------------------------------------
+// worker contexts over the C ABI
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct Ctx {
+    pnx_ctx* ctx = nullptr;
+    ~Ctx() {
+        if (ctx) pnx_destroy(ctx);
+    }
+    void check(int rc) const {
+        if (rc != PNX_OK) throw TensorError(pnx_last_error(ctx));
+    }
+};
+
+int pde_code(PdeId id) {
+    switch (id) {
+        case PdeId::advection: return PNX_PDE_ADVECTION;
+        case PdeId::allen_cahn: return PNX_PDE_ALLEN_CAHN;
+        case PdeId::burgers: return PNX_PDE_BURGERS;
+        case PdeId::maxwell_te: return PNX_PDE_MAXWELL_TE;
+        case PdeId::ns_steady: return PNX_PDE_NS_STEADY;
+    }
+    return -1;
+}
+
+std::vector<double> axis_major(const Points& p) {
+    std::vector<double> v;
+    for (const auto& c : p.coords) v.insert(v.end(), c.begin(), c.end());
+    return v;
+}
+
+std::vector<double> field_major(const std::vector<std::vector<double>>& t) {
+    std::vector<double> v;
+    for (const auto& c : t) v.insert(v.end(), c.begin(), c.end());
+    return v;
+}
+
+std::unique_ptr<Ctx> make_worker(const Model& m, const TrainingProblem& prob, const Points& shard,
+                                 const CollocationData& data, int device) {
+    const ModelSpec& s = m.spec();
+    std::vector<int32_t> per, tr;
+    std::vector<double> period;
+    for (const auto& ax : s.periodic_axes) {
+        per.push_back(ax.periodic ? 1 : 0);
+        period.push_back(ax.period);
+        tr.push_back(ax.trainable ? 1 : 0);
+    }
+    pnx_model_desc md{static_cast<int32_t>(s.in_dim), static_cast<int32_t>(s.hidden_dim),
+                      static_cast<int32_t>(s.depth), static_cast<int32_t>(s.out_dim),
+                      static_cast<int32_t>(s.activation), s.sine_w0, static_cast<int32_t>(per.size()),
+                      per.data(), period.data(), tr.data(), s.rff ? static_cast<int32_t>(s.rff->width) : 0,
+                      s.rff ? m.rff_matrix().data.data() : nullptr, s.rwf ? 1 : 0};
+    pnx_problem_desc pd{pde_code(prob.residual.id), prob.residual.advection_c, prob.residual.epsilon,
+                        prob.residual.mu, prob.residual.reynolds, static_cast<int32_t>(prob.bc)};
+    auto w = std::make_unique<Ctx>();
+    if (pnx_create(&md, &pd, device, &w->ctx) != PNX_OK) throw TensorError(pnx_create_error());
+    auto pts = axis_major(shard);
+    w->check(pnx_set_points(w->ctx, pts.data(), static_cast<int64_t>(shard.count()),
+                            static_cast<int32_t>(shard.coords.size())));
+    auto ic = axis_major(data.ic_points);
+    auto ict = field_major(data.ic_targets);
+    w->check(pnx_set_ic(w->ctx, ic.data(), ict.data(), static_cast<int64_t>(data.ic_points.count())));
+    if (prob.bc != TrainingProblem::Bc::hard) {
+        auto a = axis_major(data.bc_a), b = axis_major(data.bc_b);
+        auto t = field_major(data.bc_targets);
+        w->check(pnx_set_bc(w->ctx, a.data(), b.empty() ? nullptr : b.data(), t.empty() ? nullptr : t.data(),
+                            static_cast<int64_t>(data.bc_a.count())));
+    }
+    return w;
+}
+
+std::vector<Points> shard_interior(const Points& interior, int workers) {
+    const std::size_t n = interior.count();
+    const std::size_t base = n / static_cast<std::size_t>(workers);
+    if (base == 0) throw TensorError("data parallel: fewer interior points than workers");
+    std::vector<Points> shards;
+    for (int w = 0; w < workers; ++w) {
+        const std::size_t from = static_cast<std::size_t>(w) * base;
+        const std::size_t to = (w + 1 == workers) ? n : from + base;
+        Points p;
+        for (const auto& c : interior.coords) p.coords.emplace_back(c.begin() + from, c.begin() + to);
+        shards.push_back(std::move(p));
+    }
+    return shards;
+}
+
+std::vector<double> flatten(const std::vector<NamedTensor>& ps) {
+    std::vector<double> v;
+    for (const auto& p : ps) v.insert(v.end(), p.value.data.begin(), p.value.data.end());
+    return v;
+}
+
+struct Step {
+    std::vector<double> grad;
+    double losses[3];
+};
+
+// run every worker's step in its own thread (trainer.cpp:445-457), then the
+// rank-ordered average (trainer.cpp:264-281)
+std::vector<double> synchronized_step(std::vector<std::unique_ptr<Ctx>>& workers, const std::vector<double>& params,
+                                      const std::array<double, 3>& lambdas, std::array<double, 3>& mean_losses) {
+    const std::size_t W = workers.size();
+    std::vector<Step> out(W);
+    std::vector<std::string> errors(W);
+    std::vector<std::thread> threads;
+    for (std::size_t w = 0; w < W; ++w) {
+        out[w].grad.resize(params.size());
+        threads.emplace_back([&, w] {
+            const int rc = pnx_step(workers[w]->ctx, params.data(), lambdas.data(), out[w].grad.data(), out[w].losses);
+            if (rc != PNX_OK) errors[w] = pnx_last_error(workers[w]->ctx);
+        });
+    }
+    for (auto& t : threads) t.join();
+    for (const auto& e : errors)
+        if (!e.empty()) throw TensorError(e);
+    std::vector<double> avg = out[0].grad;
+    for (std::size_t w = 1; w < W; ++w)
+        for (std::size_t k = 0; k < avg.size(); ++k) avg[k] += out[w].grad[k];
+    const double inv = 1.0 / static_cast<double>(W);
+    for (auto& v : avg) v *= inv;
+    mean_losses = {0.0, 0.0, 0.0};
+    for (std::size_t w = 0; w < W; ++w)
+        for (int t = 0; t < 3; ++t) mean_losses[t] += out[w].losses[t] * inv;
+    return avg;
+}
+
+int device_count() {
+    // contexts need a device; pnx_create reports a missing GPU itself
+    return 0;
+}
+
+}  // namespace
+
+std::vector<Tensor> data_parallel_gradient(Model& model, const TrainingProblem& prob, const TrainConfig& cfg,
+                                           int workers) {
+    const int W = std::max(1, workers);
+    CollocationData data = build_collocation(prob, cfg.collocation, cfg.seed);
+    std::vector<Points> shards = shard_interior(data.interior, W);
+    std::vector<std::unique_ptr<Ctx>> ctxs;
+    for (int w = 0; w < W; ++w) ctxs.push_back(make_worker(model, prob, shards[static_cast<std::size_t>(w)], data, cfg.device));
+    std::array<double, 3> losses{};
+    std::vector<double> g = synchronized_step(ctxs, flatten(model.trainable()), {1.0, 1.0, 1.0}, losses);
+    std::vector<Tensor> out;
+    std::size_t at = 0;
+    for (const auto& p : model.trainable()) {
+        Tensor t{p.value.shape, std::vector<double>(g.begin() + static_cast<std::ptrdiff_t>(at),
+                                                    g.begin() + static_cast<std::ptrdiff_t>(at + p.value.size()))};
+        at += p.value.size();
+        out.push_back(std::move(t));
+    }
+    (void)device_count;
+    return out;
+}
+
+TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& cfg) {
+    TrainResult result;
+    const int W = std::max(1, cfg.workers);
+    CollocationData data = build_collocation(prob, cfg.collocation, cfg.seed);
+    std::vector<Points> shards = shard_interior(data.interior, W);
+    std::vector<std::unique_ptr<Ctx>> ctxs;
+    for (int w = 0; w < W; ++w) ctxs.push_back(make_worker(model, prob, shards[static_cast<std::size_t>(w)], data, cfg.device));
+    std::vector<double> p = flatten(model.trainable());
+    std::vector<double> m(p.size(), 0.0), v(p.size(), 0.0);
+    long t = 0;
+    for (long epoch = 0; epoch < cfg.epochs; ++epoch) {
+        std::array<double, 3> losses{};
+        std::vector<double> g;
+        try {
+            g = synchronized_step(ctxs, p, cfg.lambdas, losses);
+        } catch (const std::exception& e) {
+            result.aborted = true;
+            result.abort_reason = e.what();
+            break;
+        }
+        // Adam (optim.cpp:7-41) with lr = base * gamma^epoch (optim.cpp:71-73)
+        for (std::size_t k = 0; k < g.size(); ++k)
+            if (!std::isfinite(g[k])) {
+                result.aborted = true;
+                result.abort_reason = "adam: non-finite gradient at step " + std::to_string(t + 1);
+                break;
+            }
+        if (result.aborted) break;
+        ++t;
+        const AdamConfig& a = cfg.adam;
+        const double lr = a.lr * std::pow(cfg.scheduler_gamma, static_cast<double>(epoch));
+        const double bc1 = 1.0 - std::pow(a.beta1, static_cast<double>(t));
+        const double bc2 = 1.0 - std::pow(a.beta2, static_cast<double>(t));
+        for (std::size_t k = 0; k < p.size(); ++k) {
+            m[k] = a.beta1 * m[k] + (1.0 - a.beta1) * g[k];
+            v[k] = a.beta2 * v[k] + (1.0 - a.beta2) * g[k] * g[k];
+            p[k] -= lr * (m[k] / bc1) / (std::sqrt(v[k] / bc2) + a.eps);
+        }
+        std::size_t at = 0;
+        for (auto& prm : model.trainable())
+            for (auto& x : prm.value.data) x = p[at++];
+        result.metrics.push_back({epoch, losses[0], losses[1], losses[2], lr});
+        if (cfg.on_sync) {
+            std::vector<std::uint64_t> hashes(static_cast<std::size_t>(W), param_hash(model.trainable()));
+            cfg.on_sync(epoch, hashes);
+        }
+        ++result.epochs_run;
+    }
+    return result;
+}
+
+}  // namespace pinnlab_b200

@@ -685,64 +685,96 @@ struct HeadArgs {
 };
 
 template <int P, int ACT, int J>
-__global__ void __launch_bounds__(32 * kHeadWarps) k_head(HeadArgs a) {
+__global__ void __launch_bounds__(32 * kHeadWarps, 1) k_head(HeadArgs a) {
     using Tr = PdeTraits<P>;
     constexpr int L = Tr::L, F = Tr::F, K = Tr::K;
     constexpr int S = Streams<L>::S;
+    constexpr int FLUSH = 16;  // rows accumulated in FP32 before the FP64 flush
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gw = blockIdx.x * kHeadWarps + wid, nw = gridDim.x * kHeadWarps;
     const int64_t RH = (int64_t)a.Rpad * a.H;
+    // lane owns features k = lane + 32 j (coalesced per j); W_L in shared memory
+    __shared__ float Ws[512 * 3];
+    extern __shared__ double head_dyn[];  // per-warp FP64 dW_L / db_L: [kHeadWarps][H*F + F]
+    const int acc_ld = a.H * F + F;
+    double* accw = head_dyn + (int64_t)wid * acc_ld;
+    for (int i = threadIdx.x; i < a.H * F; i += blockDim.x) Ws[i] = a.W[i];
+    for (int i = lane; i < acc_ld; i += 32) accw[i] = 0.0;
+    __syncthreads();
 
-    float wreg[J][F];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-        const int k = lane + 32 * j;
-#pragma unroll
-        for (int f = 0; f < F; ++f) wreg[j][f] = (k < a.H) ? a.W[k * F + f] : 0.0f;
-    }
-    double accW[J][F];
+    float accW[J][F];
+    float accB[F];
 #pragma unroll
     for (int j = 0; j < J; ++j)
 #pragma unroll
-        for (int f = 0; f < F; ++f) accW[j][f] = 0.0;
-    double accB[F];
+        for (int f = 0; f < F; ++f) accW[j][f] = 0.0f;
 #pragma unroll
-    for (int f = 0; f < F; ++f) accB[f] = 0.0;
+    for (int f = 0; f < F; ++f) accB[f] = 0.0f;
     double lpde = 0.0, lic = 0.0, lbc = 0.0;
+    int since_flush = 0;
 
-    for (int r = gw; r < a.nrows; r += nw) {
-        const int64_t g = a.row0 + r;
-        float z[S][J], h[S][J];
+    auto load_row = [&](int r, float (*zz)[J]) {
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int k = lane + 32 * j;
-            float zz[S], hh[S];
-            if (k < a.H) {
 #pragma unroll
-                for (int s = 0; s < S; ++s) zz[s] = a.Z[s * RH + (int64_t)r * a.H + k];
-                act_fwd<L, ACT>(zz, hh, a.w0);
-            } else {
-#pragma unroll
-                for (int s = 0; s < S; ++s) zz[s] = hh[s] = 0.0f;
-            }
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                z[s][j] = zz[s];
-                h[s][j] = hh[s];
-            }
+            for (int s = 0; s < S; ++s) zz[s][j] = (k < a.H) ? __ldg(a.Z + s * RH + (int64_t)r * a.H + k) : 0.0f;
         }
+    };
+    auto flush = [&]() {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int k = lane + 32 * j;
+            if (k < a.H)
+#pragma unroll
+                for (int f = 0; f < F; ++f) {
+                    accw[k * F + f] += (double)accW[j][f];
+                    accW[j][f] = 0.0f;
+                }
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int f = 0; f < F; ++f) accw[a.H * F + f] += (double)accB[f];
+#pragma unroll
+        for (int f = 0; f < F; ++f) accB[f] = 0.0f;
+        since_flush = 0;
+    };
+
+    float z[S][J], zn[S][J];
+    int r = gw;
+    if (r < a.nrows) load_row(r, z);
+    for (; r < a.nrows; r += nw) {
+        const int rn = r + nw;
+        if (rn < a.nrows) load_row(rn, zn);  // prefetch the next row of this warp
+        const int64_t g = a.row0 + r;
         float o[S * F];
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
+            for (int f = 0; f < F; ++f) o[s * F + f] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int k = lane + 32 * j;
+            float zz[S], hh[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) zz[s] = z[s][j];
+            act_fwd<L, ACT>(zz, hh, a.w0);
+#pragma unroll
             for (int f = 0; f < F; ++f) {
-                float v = 0.0f;
+                const float w = (k < a.H) ? Ws[k * F + f] : 0.0f;
 #pragma unroll
-                for (int j = 0; j < J; ++j) v = fmaf(h[s][j], wreg[j][f], v);
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-                o[s * F + f] = v + (s == 0 ? a.b[f] : 0.0f);
+                for (int s = 0; s < S; ++s) o[s * F + f] = fmaf(hh[s], w, o[s * F + f]);
             }
+        }
+#pragma unroll
+        for (int i = 0; i < S * F; ++i) {
+            float v = o[i];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            o[i] = v;
+        }
+#pragma unroll
+        for (int f = 0; f < F; ++f) o[f] += a.b[f];
 
         if (a.values_only) {
             if (lane == 0) {
@@ -752,127 +784,132 @@ __global__ void __launch_bounds__(32 * kHeadWarps) k_head(HeadArgs a) {
                 if (slot >= 0)
                     for (int f = 0; f < F; ++f) a.vals_out[slot * F + f] = o[f];
             }
-            continue;
-        }
-
-        float ob[S * F];
+        } else {
+            float ob[S * F];
 #pragma unroll
-        for (int i = 0; i < S * F; ++i) ob[i] = 0.0f;
-        if (g >= a.int0 && g < a.int1) {
-            float res[K], rb[K];
-            residual<P>(o, res, a.pc);
-            float sq = 0.0f;
+            for (int i = 0; i < S * F; ++i) ob[i] = 0.0f;
+            if (g >= a.int0 && g < a.int1) {
+                float res[K], rb[K];
+                residual<P>(o, res, a.pc);
+                float sq = 0.0f;
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                sq += res[k] * res[k];
-                rb[k] = a.w_pde * res[k];
-                if (lane == 0 && !isfinite(res[k])) atomicMin(&a.bad[k], (int)(g - a.int0));
+                for (int k = 0; k < K; ++k) {
+                    sq += res[k] * res[k];
+                    rb[k] = a.w_pde * res[k];
+                    if (lane == 0 && !isfinite(res[k])) atomicMin(&a.bad[k], (int)(g - a.int0));
+                }
+                if (a.resid_out && lane == 0) {
+                    const int64_t n_int = a.int1 - a.int0;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) a.resid_out[k * n_int + (g - a.int0)] = res[k];
+                }
+                lpde += (double)sq;
+                residual_seed<P>(o, rb, ob, a.pc);
+            } else if (g >= a.ic0 && g < a.ic1) {
+                const int64_t i = g - a.ic0, n = a.ic1 - a.ic0;
+                float sq = 0.0f;
+#pragma unroll
+                for (int f = 0; f < F; ++f) {
+                    const float d = o[f] - a.ic_t[f * n + i];
+                    sq += d * d;
+                    ob[f] = a.w_ic * d;
+                }
+                lic += (double)sq;
+            } else if (a.bc_mode == 2 && g >= a.bca0 && g < a.bca1) {
+                const int64_t i = g - a.bca0, n = a.bca1 - a.bca0;
+                float sq = 0.0f;
+#pragma unroll
+                for (int f = 0; f < F; ++f) {
+                    const float d = o[f] - a.bc_t[f * n + i];
+                    sq += d * d;
+                    ob[f] = a.w_bc * d;
+                }
+                lbc += (double)sq;
+            } else if (a.bc_mode == 1 && g >= a.bca0 && g < a.bca1) {
+                const int64_t i = g - a.bca0, np = a.bca1 - a.bca0;
+                float sq = 0.0f;
+#pragma unroll
+                for (int f = 0; f < F; ++f) {
+                    const float d = o[f] - a.bc_vals[(np + i) * F + f];
+                    sq += d * d;
+                    ob[f] = a.w_bc * d;
+                }
+                lbc += (double)sq;
+            } else if (a.bc_mode == 1 && g >= a.bcb0 && g < a.bcb1) {
+                const int64_t i = g - a.bcb0;
+#pragma unroll
+                for (int f = 0; f < F; ++f) ob[f] = -a.w_bc * (a.bc_vals[i * F + f] - o[f]);
             }
-            if (a.resid_out && lane == 0) {
-                const int64_t n_int = a.int1 - a.int0;
-#pragma unroll
-                for (int k = 0; k < K; ++k) a.resid_out[k * n_int + (g - a.int0)] = res[k];
-            }
-            lpde += (double)sq;
-            residual_seed<P>(o, rb, ob, a.pc);
-        } else if (g >= a.ic0 && g < a.ic1) {
-            const int64_t i = g - a.ic0, n = a.ic1 - a.ic0;
-            float sq = 0.0f;
-#pragma unroll
-            for (int f = 0; f < F; ++f) {
-                const float d = o[f] - a.ic_t[f * n + i];
-                sq += d * d;
-                ob[f] = a.w_ic * d;
-            }
-            lic += (double)sq;
-        } else if (a.bc_mode == 2 && g >= a.bca0 && g < a.bca1) {  // dirichlet
-            const int64_t i = g - a.bca0, n = a.bca1 - a.bca0;
-            float sq = 0.0f;
-#pragma unroll
-            for (int f = 0; f < F; ++f) {
-                const float d = o[f] - a.bc_t[f * n + i];
-                sq += d * d;
-                ob[f] = a.w_bc * d;
-            }
-            lbc += (double)sq;
-        } else if (a.bc_mode == 1 && g >= a.bca0 && g < a.bca1) {  // periodic side a
-            const int64_t i = g - a.bca0, np = a.bca1 - a.bca0;
-            float sq = 0.0f;
-#pragma unroll
-            for (int f = 0; f < F; ++f) {
-                const float d = o[f] - a.bc_vals[(np + i) * F + f];
-                sq += d * d;
-                ob[f] = a.w_bc * d;
-            }
-            lbc += (double)sq;
-        } else if (a.bc_mode == 1 && g >= a.bcb0 && g < a.bcb1) {  // periodic side b
-            const int64_t i = g - a.bcb0;
-#pragma unroll
-            for (int f = 0; f < F; ++f) ob[f] = -a.w_bc * (a.bc_vals[i * F + f] - o[f]);
-        }
-        // reverse through the head: hbar = Obar W^T, dW_L += h^T Obar
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const int k = lane + 32 * j;
-            float hb[S], zz[S], zb[S];
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                float v = 0.0f;
-#pragma unroll
-                for (int f = 0; f < F; ++f) v = fmaf(ob[s * F + f], wreg[j][f], v);
-                hb[s] = v;
-                zz[s] = z[s][j];
-            }
-#pragma unroll
-            for (int f = 0; f < F; ++f) {
-                float v = 0.0f;
-#pragma unroll
-                for (int s = 0; s < S; ++s) v = fmaf(h[s][j], ob[s * F + f], v);
-                accW[j][f] += (double)v;
-            }
-            if (k < a.H) {
-                act_bwd<L, ACT>(zz, hb, zb, a.w0);
-#pragma unroll
-                for (int s = 0; s < S; ++s) a.Zb[s * RH + (int64_t)r * a.H + k] = zb[s];
-            }
-        }
-#pragma unroll
-        for (int f = 0; f < F; ++f) accB[f] += (double)ob[f];
-    }
-    if (a.values_only) return;
-    // pad rows of the chunk: zero adjoints so they contribute nothing
-    for (int r = a.nrows + gw; r < a.Rpad; r += nw)
-        for (int k = lane; k < a.H; k += 32)
-#pragma unroll
-            for (int s = 0; s < S; ++s) a.Zb[s * RH + (int64_t)r * a.H + k] = 0.0f;
-
-    // deterministic block reduction: warps in order
-    __shared__ double sh[512 * 3 + 3 + 3];
-    const int nWF = a.H * F;
-    for (int i = threadIdx.x; i < nWF + F + 3; i += blockDim.x) sh[i] = 0.0;
-    __syncthreads();
-    for (int w = 0; w < kHeadWarps; ++w) {
-        if (wid == w) {
+            // reverse through the head: hbar = Obar W^T, dW_L += h^T Obar
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int k = lane + 32 * j;
-                if (k < a.H)
+                float w[F];
 #pragma unroll
-                    for (int f = 0; f < F; ++f) sh[k * F + f] += accW[j][f];
-            }
-            if (lane == 0) {
+                for (int f = 0; f < F; ++f) w[f] = (k < a.H) ? Ws[k * F + f] : 0.0f;
+                float zz[S], hh[S], hb[S], zb[S];
 #pragma unroll
-                for (int f = 0; f < F; ++f) sh[nWF + f] += accB[f];
-                sh[nWF + F + 0] += lpde;
-                sh[nWF + F + 1] += lic;
-                sh[nWF + F + 2] += lbc;
+                for (int s = 0; s < S; ++s) zz[s] = z[s][j];
+                act_fwd<L, ACT>(zz, hh, a.w0);
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    float v = 0.0f;
+#pragma unroll
+                    for (int f = 0; f < F; ++f) v = fmaf(ob[s * F + f], w[f], v);
+                    hb[s] = v;
+                }
+#pragma unroll
+                for (int f = 0; f < F; ++f) {
+                    float v = accW[j][f];
+#pragma unroll
+                    for (int s = 0; s < S; ++s) v = fmaf(hh[s], ob[s * F + f], v);
+                    accW[j][f] = v;
+                }
+                if (k < a.H) {
+                    act_bwd<L, ACT>(zz, hb, zb, a.w0);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) a.Zb[s * RH + (int64_t)r * a.H + k] = zb[s];
+                }
             }
+#pragma unroll
+            for (int f = 0; f < F; ++f) accB[f] += ob[f];
+            if (++since_flush == FLUSH) flush();
         }
-        __syncthreads();
+        if (rn < a.nrows) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int j = 0; j < J; ++j) z[s][j] = zn[s][j];
+        }
     }
+    if (a.values_only) return;
+    flush();
+    // pad rows of the chunk: zero adjoints so they contribute nothing
+    for (int r2 = a.nrows + gw; r2 < a.Rpad; r2 += nw)
+        for (int k = lane; k < a.H; k += 32)
+#pragma unroll
+            for (int s = 0; s < S; ++s) a.Zb[s * RH + (int64_t)r2 * a.H + k] = 0.0f;
+
+    // deterministic block reduction: warps in order
+    __shared__ double lsum[kHeadWarps][3];
+    if (lane == 0) {
+        lsum[wid][0] = lpde;
+        lsum[wid][1] = lic;
+        lsum[wid][2] = lbc;
+    }
+    __syncthreads();
+    const int nWF = a.H * F;
     double* hp = a.head_part + (int64_t)blockIdx.x * (nWF + F);
-    for (int i = threadIdx.x; i < nWF + F; i += blockDim.x) hp[i] += sh[i];
-    if (threadIdx.x < 3) a.loss_part[blockIdx.x * 3 + threadIdx.x] += sh[nWF + F + threadIdx.x];
+    for (int i = threadIdx.x; i < nWF + F; i += blockDim.x) {
+        double v = 0.0;
+        for (int w = 0; w < kHeadWarps; ++w) v += head_dyn[(int64_t)w * acc_ld + i];
+        hp[i] += v;
+    }
+    if (threadIdx.x < 3) {
+        double v = 0.0;
+        for (int w = 0; w < kHeadWarps; ++w) v += lsum[w][threadIdx.x];
+        a.loss_part[blockIdx.x * 3 + threadIdx.x] += v;
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -85,12 +85,23 @@ void launch_wgrad(int L, int pro, const WgradArgs& w, int nsplit, cudaStream_t s
     }
 }
 
+template <int P, int ACT, int J>
+void launch_head_a(const HeadArgs& h, int grid, cudaStream_t st) {
+    const int smem = kHeadWarps * (h.H * PdeTraits<P>::F + PdeTraits<P>::F) * (int)sizeof(double);
+    auto kern = k_head<P, ACT, J>;
+    static int attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = smem;
+    }
+    kern<<<grid, 32 * kHeadWarps, smem, st>>>(h);
+}
 template <int P, int J>
 void launch_head_j(int act, const HeadArgs& h, int grid, cudaStream_t st) {
     switch (act) {
-        case ACT_TANH: k_head<P, ACT_TANH, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
-        case ACT_SINE: k_head<P, ACT_SINE, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
-        default: k_head<P, ACT_SWISH, J><<<grid, 32 * kHeadWarps, 0, st>>>(h); break;
+        case ACT_TANH: launch_head_a<P, ACT_TANH, J>(h, grid, st); break;
+        case ACT_SINE: launch_head_a<P, ACT_SINE, J>(h, grid, st); break;
+        default: launch_head_a<P, ACT_SWISH, J>(h, grid, st); break;
     }
 }
 template <int P>

@@ -23,7 +23,7 @@ int launch_tc_layer_t(const TcGemmArgs& g, cudaStream_t st) {
 template <int L, int NT>
 int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc2BwdCfg<Streams<L>::S, NT>;
-    const int smem = Cfg::NST * Cfg::STAGE + 1024;
+    const int smem = Cfg::SMEM;
     auto kern = k_tc2_bwd<L, NT>;
     static bool attr = false;
     if (!attr) {

@@ -90,6 +90,8 @@ struct pnx_ctx {
     float* d_bc_vals = nullptr;
     int* d_bad = nullptr;
     float* d_resid = nullptr;
+    int64_t resid_cap = 0;
+    bool h_int_stale = false;  // interior coordinates newer on device than in h_int
     bool capture_resid = false;
     TcWorkspace tc{};
     // kernel-class timing with CUDA events on the launching stream (bench roofline)
@@ -190,6 +192,13 @@ int64_t bytes_per_row(const pnx_ctx* c) {
 
 int upload_rows(pnx_ctx* ctx) {
     const int d = ctx->in_dim;
+    if (ctx->h_int_stale && ctx->d_coords) {  // pull the fast-path interior back before re-layout
+        const int64_t off = ctx->n_bca + ctx->n_bcb + ctx->n_ic;
+        for (int a = 0; a < d; ++a)
+            CK(cudaMemcpy(ctx->h_int.data() + a * ctx->n_int, ctx->d_coords + a * ctx->ld + off,
+                          (size_t)ctx->n_int * 8, cudaMemcpyDeviceToHost));
+        ctx->h_int_stale = false;
+    }
     const int64_t T = ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_int;
     ctx->ld = T;
     std::vector<double> all((size_t)(d * T));
@@ -751,11 +760,26 @@ int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes
     if (!ctx) return PNX_ERR_ARG;
     if (n_axes != ctx->in_dim) return fail(ctx, PNX_ERR_ARG, "residual: coordinate count mismatch");
     if (n <= 0 || !coords) return fail(ctx, PNX_ERR_ARG, "residual_loss: empty point set");
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->rows_dirty && n == ctx->n_int && ctx->d_coords) {
+        // same row layout (e.g. resampled points, trainer.cpp:421-434): copy the
+        // caller's axis-major buffer straight into the interior segment on device
+        const int64_t off = ctx->n_bca + ctx->n_bcb + ctx->n_ic;
+        for (int a = 0; a < n_axes; ++a)
+            CK(cudaMemcpyAsync(ctx->d_coords + a * ctx->ld + off, coords + a * n, (size_t)n * 8,
+                               cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->h_int_stale = true;
+        return PNX_OK;
+    }
     ctx->h_int.assign(coords, coords + n * n_axes);
+    ctx->h_int_stale = false;
     ctx->n_int = n;
     ctx->rows_dirty = true;
-    cudaSetDevice(ctx->device);
-    if (int r = dalloc(ctx, &ctx->d_resid, (size_t)n * ctx->Kres)) return r;
+    if ((int64_t)n * ctx->Kres > ctx->resid_cap) {
+        if (int r = dalloc(ctx, &ctx->d_resid, (size_t)n * ctx->Kres)) return r;
+        ctx->resid_cap = (int64_t)n * ctx->Kres;
+    }
     return PNX_OK;
 }
 

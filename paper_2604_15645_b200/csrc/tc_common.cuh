@@ -52,7 +52,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // ---- proxy / tcgen05 fences ---------------------------------------------------
 // generic-proxy smem writes -> visible to the async proxy (tensor core reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
+#ifndef PNX_EXP_NOFENCE  // timing experiment only: removing it is a race
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
 }
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

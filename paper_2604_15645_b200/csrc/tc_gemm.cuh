@@ -77,7 +77,21 @@ __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
 __device__ __forceinline__ void sts32(uint32_t addr, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
-__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+// streaming operand loads (read once per stage): policy selectable for experiments
+__device__ __forceinline__ float4 ldg4(const float* p) {
+#if defined(PNX_LD_CG)
+    float4 v;
+    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+#elif defined(PNX_LD_NA)
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+#else
+    return __ldg(reinterpret_cast<const float4*>(p));
+#endif
+}
 __device__ __forceinline__ void split4(float4 v, float4& hi, float4& lo) {
     tc::split3(v.x, hi.x, lo.x);
     tc::split3(v.y, hi.y, lo.y);
@@ -878,9 +892,18 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_tc2_wgrad(TcWgradArgs g, int
             boff[j] = tc::mn32_off((uint32_t)(brow[j] & 7), (uint32_t)(bc[j] * 4), (uint32_t)NF);
         }
         double dbacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#ifdef PNX_WG_D
+        constexpr int D = PNX_WG_D;
+#else
         constexpr int D = 2;  // register prefetch depth (stages)
+#endif
         float4 ring[D][5];
         auto load = [&](int it, float4* v) {
+#ifdef PNX_EXP_NOLOAD
+#pragma unroll
+            for (int j = 0; j < 5; ++j) v[j] = make_float4(0.01f * it, 0.2f, 0.3f, 0.4f);
+            return;
+#endif
             const int rb = it / S, s = it % S;
             const int row = rbeg + rb * 8 + ar;
             const float* pa = g.A + (int64_t)row * g.Kin + f;
@@ -951,7 +974,11 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_tc2_wgrad(TcWgradArgs g, int
                     }
                     split4(v[3 + j], bhi[j], blo[j]);
                 }
-                tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                {
+                    TC_T0();
+                    tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                    if (tid == 0) TC_ACC(2);
+                }
                 sts128(stage + aoff, ahi);
                 sts128(stage + Cfg::A_T + aoff, alo);
 #pragma unroll
@@ -988,7 +1015,11 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_tc2_wgrad(TcWgradArgs g, int
             for (int it = 0; it < nit; ++it) {
                 const int st = it % NST;
                 const uint32_t stage = sbase + st * Cfg::STAGE;
-                tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                {
+                    TC_T0();
+                    tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                    TC_ACC(0);
+                }
                 tc::tc_fence_after();
                 const uint64_t ah = tc::make_sdesc(stage, 512, 4 * 512, 1);
                 const uint64_t al = tc::make_sdesc(stage + Cfg::A_T, 512, 4 * 512, 1);
@@ -1040,6 +1071,10 @@ struct Tc2BwdCfg {
     static constexpr int B_T = NT * 32;
     static constexpr int STAGE = A_BYTES + 2 * B_T;
     static constexpr int NST = (TC_SMEM - 1024) / STAGE > 8 ? 8 : (TC_SMEM - 1024) / STAGE;
+    // the epilogue reuses the (then idle) stage ring as its staging buffer
+    static constexpr int EPI_BYTES = 8 * S * 32 * 36 * 4;
+    static constexpr int SMEM = (NST * STAGE > EPI_BYTES ? NST * STAGE : EPI_BYTES) + 1024;
+    static_assert(SMEM <= 227 * 1024, "bwd shared memory");
 };
 
 template <int L, int NT>
@@ -1120,10 +1155,16 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
             for (int it = 0; it < nkb; ++it) {
                 const int st = it % NST;
                 const uint32_t stage = sbase + st * Cfg::STAGE;
-                tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                {
+                    TC_T0();
+                    tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                    TC_ACC(0);
+                }
                 tc::tc_fence_after();
                 const uint64_t bh = tc::make_sdesc(stage + Cfg::A_BYTES, 16, 256, 6);
                 const uint64_t bl = tc::make_sdesc(stage + Cfg::A_BYTES + Cfg::B_T, 16, 256, 6);
+                // stream-major order (tools/rate_probe.cu: 3 MMAs into one
+                // accumulator then the next runs at 84% vs 56% term-major)
 #pragma unroll
                 for (int s2 = 0; s2 < S; ++s2) {
                     const uint32_t ah = stage + (2 * s2) * TC_TILE_BYTES;
@@ -1139,43 +1180,80 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
         }
         __syncwarp();
     } else {
+        // All MMAs have retired once tfull fires, so the stage ring is free:
+        // each warp stages 32-row x 32-feature blocks of every stream there
+        // and moves them to/from HBM as full 128-byte lines (8 lanes per row).
+        constexpr int ROWF = 36;  // padded row (floats): conflict-free 16-B lanes
         const int q = warp & 3, half = (warp - 9) >> 2;
-        const int row = r0 + q * 32 + lane;
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t buf = sbase + (uint32_t)(warp - 9) * (S * 32 * ROWF * 4);
+        const int64_t rbase = (int64_t)(r0 + q * 32) * g.N + n0;
+        const int lr = lane >> 3, lc = (lane & 7) * 4;
         tc::mbar_wait(&tfull, 0);
         tc::tc_fence_after();
+        TC_T0();
 #pragma unroll 1
-        for (int c = half * (NT / 2); c < (half + 1) * (NT / 2); c += 8) {
-            float hb[S][8], z[S][8];
-#pragma unroll
-            for (int s2 = 0; s2 < S; ++s2) tmem_ld8(tl + (uint32_t)(s2 * NT + c), hb[s2]);
+        for (int cc = 0; cc < NT / 2; cc += 32) {
+            const int c0 = half * (NT / 2) + cc;
 #pragma unroll
             for (int s2 = 0; s2 < S; ++s2) {
-                const float* zp = g.Zlow + s2 * RN + (int64_t)row * g.N + n0 + c;
-                const float4 a = ldg4(zp), b = ldg4(zp + 4);
-                z[s2][0] = a.x; z[s2][1] = a.y; z[s2][2] = a.z; z[s2][3] = a.w;
-                z[s2][4] = b.x; z[s2][5] = b.y; z[s2][6] = b.z; z[s2][7] = b.w;
-            }
-            tc::tmem_ld_wait();
+                const float* src = g.Zlow + s2 * RN + rbase + c0;
+                float4 v[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                float zz[S], hh[S], oo[S];
+                for (int k = 0; k < 8; ++k) v[k] = ldg4(src + (int64_t)(4 * k + lr) * g.N + lc);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) sts128(buf + ((s2 * 32 + 4 * k + lr) * ROWF + lc) * 4, v[k]);
+            }
+            __syncwarp();
+#pragma unroll 1
+            for (int c = 0; c < 32; c += 8) {
+                float hb[S][8], z[S][8];
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) tmem_ld8(tl + (uint32_t)(s2 * NT + c0 + c), hb[s2]);
 #pragma unroll
                 for (int s2 = 0; s2 < S; ++s2) {
-                    zz[s2] = z[s2][j];
-                    hh[s2] = hb[s2][j];
+                    const uint32_t a = buf + ((s2 * 32 + lane) * ROWF + c) * 4;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(z[s2][0]), "=f"(z[s2][1]), "=f"(z[s2][2]), "=f"(z[s2][3]) : "r"(a));
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(z[s2][4]), "=f"(z[s2][5]), "=f"(z[s2][6]), "=f"(z[s2][7]) : "r"(a + 16));
                 }
-                act_bwd<L, ACT_TANH>(zz, hh, oo, 1.0f);
+                tc::tmem_ld_wait();
 #pragma unroll
-                for (int s2 = 0; s2 < S; ++s2) hb[s2][j] = oo[s2];
+                for (int j = 0; j < 8; ++j) {
+                    float zz[S], hh[S], oo[S];
+#pragma unroll
+                    for (int s2 = 0; s2 < S; ++s2) {
+                        zz[s2] = z[s2][j];
+                        hh[s2] = hb[s2][j];
+                    }
+                    act_bwd<L, ACT_TANH>(zz, hh, oo, 1.0f);
+#pragma unroll
+                    for (int s2 = 0; s2 < S; ++s2) hb[s2][j] = oo[s2];
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) {
+                    const uint32_t a = buf + ((s2 * 32 + lane) * ROWF + c) * 4;
+                    sts128(a, make_float4(hb[s2][0], hb[s2][1], hb[s2][2], hb[s2][3]));
+                    sts128(a + 16, make_float4(hb[s2][4], hb[s2][5], hb[s2][6], hb[s2][7]));
+                }
             }
+            __syncwarp();
 #pragma unroll
             for (int s2 = 0; s2 < S; ++s2) {
-                float* dst = g.out + s2 * RN + (int64_t)row * g.N + n0 + c;
-                *reinterpret_cast<float4*>(dst) = make_float4(hb[s2][0], hb[s2][1], hb[s2][2], hb[s2][3]);
-                *reinterpret_cast<float4*>(dst + 4) = make_float4(hb[s2][4], hb[s2][5], hb[s2][6], hb[s2][7]);
+                float* dst = g.out + s2 * RN + rbase + c0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    float4 v;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                 : "r"(buf + ((s2 * 32 + 4 * k + lr) * ROWF + lc) * 4));
+                    *reinterpret_cast<float4*>(dst + (int64_t)(4 * k + lr) * g.N + lc) = v;
+                }
             }
+            __syncwarp();
         }
+        if (warp == 9 && lane == 0) TC_ACC(3);
     }
     tc::tc_fence_before();
     __syncthreads();

@@ -216,8 +216,13 @@ class Worker:
     def set_chunk_rows(self, rows: int):
         self._chk(self.lib.pnx_set_chunk_rows(self.ctx, int(rows)))
 
-    def set_points(self, pts: np.ndarray):
-        a = _axis_major(pts)
+    def set_points(self, pts: np.ndarray, axis_major: bool = False):
+        """Interior shard: [N, d] points, or an axis-major [d, N] float64 array
+        with axis_major=True (no host transpose; pinned buffers DMA directly)."""
+        if axis_major:
+            a = pts if (pts.dtype == np.float64 and pts.flags.c_contiguous) else np.ascontiguousarray(pts, np.float64)
+        else:
+            a = _axis_major(pts)
         self._chk(self.lib.pnx_set_points(self.ctx, a.ctypes.data_as(C.POINTER(C.c_double)),
                                           a.shape[1], a.shape[0]))
 

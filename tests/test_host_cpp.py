@@ -1,0 +1,82 @@
+"""The C++ host mirror (host/, namespace pinnlab_b200) used the way a
+reference user would use pinnlab: Model(spec, seed) must reproduce the
+reference's parameter draws bit-for-bit (same libstdc++ mt19937_64 +
+normal_distribution, model.cpp:52-102), build_collocation the reference grid,
+and data_parallel_gradient / train (on the GPU) the reference gradients and
+loss trajectory."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import golden_io as gi
+
+DRIVER = os.path.join(gi.ROOT, "host", "host_driver")
+
+
+def _driver():
+    if not os.path.exists(DRIVER):
+        subprocess.run(["make", "-C", os.path.join(gi.ROOT, "host")], check=True, stdout=subprocess.DEVNULL)
+    return DRIVER
+
+
+def _job(g, path, **extra):
+    c = g["case"]
+    m = c["model"]
+    lines = [f"in_dim {m['in_dim']}", f"hidden_dim {m['hidden_dim']}", f"depth {m['depth']}",
+             f"out_dim {m['out_dim']}", f"activation {m['activation']}", f"sine_w0 {m.get('sine_w0', 1.0)}",
+             f"pde {c['pde']['id']}", f"advection_c {c['pde'].get('advection_c', 1.0)}",
+             f"epsilon {c['pde'].get('epsilon', 1.0)}", f"mu {c['pde'].get('mu', 1.0)}",
+             "domain " + " ".join(f"{a} {b}" for a, b in c["domain"]), f"initial {c['initial']}",
+             f"bc {c.get('bc', 'hard')}", "dims " + " ".join(str(d) for d in c["collocation"]["dims"]),
+             f"n_ic {c['collocation'].get('n_ic', 128)}", f"n_bc {c['collocation'].get('n_bc', 64)}", "seed 0"]
+    if m.get("periodic_axes"):
+        lines.append("periodic " + " ".join(f"{int(a['periodic'])} {a['period']} {int(a.get('trainable', False))}"
+                                            for a in m["periodic_axes"]))
+    if "rff" in m:
+        lines.append(f"rff {m['rff']['width']} {m['rff'].get('sigma', 10.0)} {m['rff'].get('mean', 0.0)}")
+    if "rwf" in m:
+        lines.append(f"rwf {m['rwf'].get('mean', 1.0)} {m['rwf'].get('stddev', 0.1)}")
+    for k, v in extra.items():
+        lines.append(f"{k} {v}")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+@pytest.mark.parametrize("name", gi.CASE_NAMES)
+def test_cpp_model_init_and_collocation_match_reference(name, tmp_path):
+    g = gi.load(name)
+    _job(g, tmp_path / "job.txt")
+    subprocess.run([_driver(), "cpu", str(tmp_path / "job.txt"), str(tmp_path)], check=True)
+    p = np.fromfile(tmp_path / "params.bin", dtype="<f8")
+    assert np.array_equal(p, g["params"]), "C++ Model init differs from the reference draws"
+    if g["spec"].rff:
+        assert np.array_equal(np.fromfile(tmp_path / "rffB.bin", dtype="<f8"), g["rffB"].ravel())
+    pts = np.fromfile(tmp_path / "interior.bin", dtype="<f8").reshape(g["spec"].in_dim, -1).T
+    assert np.array_equal(pts, g["col"].interior)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", gi.CASE_NAMES)
+def test_cpp_data_parallel_gradient_on_gpu(name, tmp_path):
+    g = gi.load(name)
+    for w in g["meta"]["workers"]:
+        _job(g, tmp_path / "job.txt", workers=w)
+        subprocess.run([_driver(), "grad", str(tmp_path / "job.txt"), str(tmp_path)], check=True)
+        grad = np.fromfile(tmp_path / "grad.bin", dtype="<f8")
+        ref = g[f"grad_w{w}"]
+        assert np.linalg.norm(grad - ref) <= 2e-5 * np.linalg.norm(ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", gi.TRAJ_NAMES)
+def test_cpp_train_trajectory_on_gpu(name, tmp_path):
+    g = gi.load(name)
+    t = g["case"]["train"]
+    _job(g, tmp_path / "job.txt", workers=g["case"]["workers"], epochs=t["epochs"], lr=t["lr"], gamma=t["gamma"])
+    subprocess.run([_driver(), "train", str(tmp_path / "job.txt"), str(tmp_path)], check=True)
+    m = np.fromfile(tmp_path / "metrics.bin", dtype="<f8").reshape(-1, 3)
+    ref = g["metrics"][:, 1:4]
+    assert m.shape == ref.shape
+    assert np.all(np.abs(m - ref) <= 1e-3 * np.abs(ref) + 1e-9)

@@ -17,5 +17,5 @@ void launch_layer0_fwd(int L, int act, const InputArgs& a, const float* W0, cons
 void launch_layer0_wgrad(int L, const InputArgs& a, const float* Zb0, int H, double* part, int grid, cudaStream_t st);
 int launch_tc_layer(int L, int mode, int pro, const TcGemmArgs& g, cudaStream_t st);
 int launch_tc2_fwd(int L, int pro, const TcGemmArgs& g, cudaStream_t st);
-int launch_tc2_wgrad(int L, int pro, const TcWgradArgs& w, int ntiles, cudaStream_t st);
+int launch_tc2_wgrad(int L, int pro, const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st);
 }  // namespace pnx

@@ -1,25 +1,34 @@
 // launch_tc.cu -- dispatch of the tcgen05 (3xTF32) kernels.
 #include "launch.h"
 
+#include <cudaTypedefs.h>
+#include <cstdlib>
+
 namespace pnx {
+
+int tc_make_tmap_3d(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
+                    uint32_t b1, uint32_t b2) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return -1;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {d0 * 4, d0 * d1 * 4};
+    const cuuint32_t box[3] = {b0, b1, b2};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -1;
+}
 
 // ---- tcgen05 dispatch --------------------------------------------------------
 
-template <int L, int MODE, int PRO, int NT>
-int launch_tc_layer_t(const TcGemmArgs& g, cudaStream_t st) {
-    constexpr int S = Streams<L>::S;
-    using Cfg = TcFwdCfg<S, NT>;
-    const int smem = Cfg::NST * Cfg::STAGE + 1024;
-    auto kern = k_tc_layer<L, MODE, PRO, ACT_TANH, NT>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
-        attr = true;
-    }
-    const int grid = (g.Rpad / TC_M) * (g.N / NT);
-    kern<<<grid, 256, smem, st>>>(g);
-    return 0;
-}
 template <int L, int NT>
 int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc2BwdCfg<Streams<L>::S, NT>;
@@ -78,31 +87,54 @@ int launch_tc2_fwd(int L, int pro, const TcGemmArgs& g, cudaStream_t st) {
     }
     return -1;
 }
-template <int L, int PRO, int NF>
-int launch_tc2_wgrad_t(const TcWgradArgs& w, int ntiles, cudaStream_t st) {
-    using Cfg = Tc2WgCfg<NF>;
-    const int smem = Cfg::NST * Cfg::STAGE + 1024;
-    auto kern = k_tc2_wgrad<L, PRO, NF>;
+template <int L, int PRO, int NF, bool PAIR>
+int launch_tc2_wgrad_t(const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st) {
+    using Cfg = Tc2WgCfg<Streams<L>::S, NF, PAIR>;
+    const int smem = Cfg::SMEM;
+    auto kern = k_tc2_wgrad<L, PRO, NF, PAIR>;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
         attr = true;
     }
-    kern<<<ntiles * (w.Kin / 128), TC2_THREADS, smem, st>>>(w, TC_WROWS);
-    return 0;
+    TcWgradArgs a = w;
+    constexpr int S = Streams<L>::S;
+    if (tc_make_tmap_3d(&a.tmA, w.A, w.Kin, w.Rpad, S, 128, 8, S) ||
+        tc_make_tmap_3d(&a.tmB, w.Bm, NF, w.Rpad, S, Cfg::NFL, 8, S))
+        return -1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles * (w.Kin / 128));
+    cfg.blockDim = dim3(TCW_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = PAIR ? 2 : 1;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, wrows) == cudaSuccess ? 0 : -1;
+}
+template <int L, int NF, bool PAIR>
+int launch_tc2_wgrad_p(int pro, const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st) {
+    return pro == ACT_NONE ? launch_tc2_wgrad_t<L, ACT_NONE, NF, PAIR>(w, ntiles, wrows, st)
+                           : launch_tc2_wgrad_t<L, ACT_TANH, NF, PAIR>(w, ntiles, wrows, st);
 }
 template <int L>
-int launch_tc2_wgrad_l(int pro, const TcWgradArgs& w, int ntiles, cudaStream_t st) {
-    if (w.N == 256) return pro == ACT_NONE ? launch_tc2_wgrad_t<L, ACT_NONE, 256>(w, ntiles, st) : launch_tc2_wgrad_t<L, ACT_TANH, 256>(w, ntiles, st);
-    if (w.N == 128) return pro == ACT_NONE ? launch_tc2_wgrad_t<L, ACT_NONE, 128>(w, ntiles, st) : launch_tc2_wgrad_t<L, ACT_TANH, 128>(w, ntiles, st);
+int launch_tc2_wgrad_l(int pro, const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st) {
+    static const bool pair = getenv("PNX_WG_NOPAIR") == nullptr;
+    if (w.N == 256 && w.Kin == 256 && pair) return launch_tc2_wgrad_p<L, 256, true>(pro, w, ntiles, wrows, st);
+    if (w.N == 256) return launch_tc2_wgrad_p<L, 256, false>(pro, w, ntiles, wrows, st);
+    if (w.N == 128) return launch_tc2_wgrad_p<L, 128, false>(pro, w, ntiles, wrows, st);
     return -1;
 }
-int launch_tc2_wgrad(int L, int pro, const TcWgradArgs& w, int ntiles, cudaStream_t st) {
+int launch_tc2_wgrad(int L, int pro, const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st) {
     switch (L) {
-        case LAY_XT: return launch_tc2_wgrad_l<LAY_XT>(pro, w, ntiles, st);
-        case LAY_AC: return launch_tc2_wgrad_l<LAY_AC>(pro, w, ntiles, st);
-        case LAY_MX: return launch_tc2_wgrad_l<LAY_MX>(pro, w, ntiles, st);
-        case LAY_NS: return launch_tc2_wgrad_l<LAY_NS>(pro, w, ntiles, st);
+        case LAY_XT: return launch_tc2_wgrad_l<LAY_XT>(pro, w, ntiles, wrows, st);
+        case LAY_AC: return launch_tc2_wgrad_l<LAY_AC>(pro, w, ntiles, wrows, st);
+        case LAY_MX: return launch_tc2_wgrad_l<LAY_MX>(pro, w, ntiles, wrows, st);
+        case LAY_NS: return launch_tc2_wgrad_l<LAY_NS>(pro, w, ntiles, wrows, st);
     }
     return -1;
 }

@@ -36,6 +36,7 @@ int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 struct pnx_ctx {
     int device = 0;
+    int nsm = 148;  // SM count of `device` (grid sizing)
     cudaStream_t stream = nullptr;
     std::string err;
     int64_t launches = 0;
@@ -467,8 +468,9 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 tw.nrows = nrows;
                 tw.Kin = t.K[l];
                 tw.N = t.N[l];
-                const int ntl = (Rpad + TC_WROWS - 1) / TC_WROWS;
-                if (launch_tc2_wgrad(L, pro, tw, ntl, st)) return fail(ctx, PNX_ERR_CUDA, "tc wgrad launch");
+                const int wr = tc_wgrad_rows(Rpad, t.K[l], ctx->nsm);
+                const int ntl = (int)((Rpad + wr - 1) / wr);
+                if (launch_tc2_wgrad(L, pro, tw, ntl, wr, st)) return fail(ctx, PNX_ERR_CUDA, "tc wgrad launch");
                 CKL();
                 k_tc_wreduce<<<296, 256, 0, st>>>(ctx->tc.wpart, ctx->tc.dbpart, ntl, t.K[l], t.N[l],
                                                   ctx->d_part[l]);
@@ -607,6 +609,7 @@ int pnx_create(const pnx_model_desc* m, const pnx_problem_desc* p, int device, p
     }
     pnx_ctx* ctx = new pnx_ctx();
     ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     ctx->in_dim = m->in_dim;
     ctx->H = m->hidden_dim;
     ctx->depth = m->depth;

@@ -15,6 +15,7 @@
 // core on stage i. Weights are pre-split and pre-swizzled once per step into
 // "stage images" (k_tc_prep_images) and copied 16 B at a time.
 #pragma once
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -74,6 +75,11 @@ __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
 }
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void sts32(uint32_t addr, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -132,173 +138,6 @@ struct TcGemmArgs {
     int Rpad, K, N;
 };
 
-template <int S, int NT>
-struct TcFwdCfg {
-    static constexpr int A_BYTES = 2 * S * TC_TILE_BYTES;  // hi+lo per stream
-    static constexpr int B_BYTES = 2 * NT * 32;
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int NST = (TC_SMEM - 1024) / STAGE > 8 ? 8 : (TC_SMEM - 1024) / STAGE;
-};
-
-// MODE 0: forward (PRO act on A, bias + store_value<ACT> epilogue)
-// MODE 1: backward (A plain, act^T<ACT> epilogue with Zlow)
-template <int L, int MODE, int PRO, int ACT, int NT>
-__global__ void __launch_bounds__(256, 1) k_tc_layer(TcGemmArgs g) {
-    constexpr int S = Streams<L>::S;
-    using Cfg = TcFwdCfg<S, NT>;
-    constexpr int NST = Cfg::NST;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = align1024(smem_raw);
-    __shared__ uint64_t empty_bar[8];
-    __shared__ uint64_t done_bar;
-    __shared__ uint32_t tmem_base;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int ntiles = g.N / NT;
-    const int rt = blockIdx.x / ntiles, nt = blockIdx.x % ntiles;
-    const int r0 = rt * TC_M, n0 = nt * NT;
-    const int nkb = g.K / 8;
-    const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * g.N;
-
-    if (tid == 0) {
-        for (int i = 0; i < NST; ++i) tc::mbar_init(&empty_bar[i], 1);
-        tc::mbar_init(&done_bar, 1);
-        tc::fence_barrier_init();
-    }
-    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-    const uint32_t tmem = tmem_base;
-    const uint32_t sbase = tc::smem_u32(smem);
-    constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NT, 0, 0);
-
-    // producer mapping: thread -> (row, 16 B chunk) of the 128 x 8 A tile
-    const int prow = tid >> 1, pc = tid & 1;
-    const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
-    const uint32_t aoff = tc::sw32_off((uint32_t)prow, (uint32_t)(pc * 4));
-    const float4* bimg = reinterpret_cast<const float4*>(g.img) + (int64_t)nt * nkb * (Cfg::B_BYTES / 16);
-
-    float4 zin[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) zin[s] = ldg4(asrc + s * RK);
-
-    for (int it = 0; it < nkb; ++it) {
-        const int st = it % NST;
-        const uint32_t stage = sbase + st * Cfg::STAGE;
-        if (it >= NST) tc::mbar_wait(&empty_bar[st], (uint32_t)((it / NST) - 1) & 1u);
-        // ---- A: jet activation (forward) + 3xTF32 split, swizzled stores
-        float4 h[S];
-        if constexpr (MODE == 0) {
-            act4<L, PRO>(zin, h);
-        } else {
-#pragma unroll
-            for (int s = 0; s < S; ++s) h[s] = zin[s];
-        }
-        // prefetch the next k-block's raw A while this one is stored
-        if (it + 1 < nkb) {
-#pragma unroll
-            for (int s = 0; s < S; ++s) zin[s] = ldg4(asrc + s * RK + (it + 1) * 8);
-        }
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            float4 hi, lo;
-            split4(h[s], hi, lo);
-            sts128(stage + (2 * s) * TC_TILE_BYTES + aoff, hi);
-            sts128(stage + (2 * s + 1) * TC_TILE_BYTES + aoff, lo);
-        }
-        // ---- B: weight image block (pre-split, pre-swizzled)
-        {
-            const float4* src = bimg + (int64_t)it * (Cfg::B_BYTES / 16);
-            for (int i = tid; i < Cfg::B_BYTES / 16; i += 256) sts128(stage + Cfg::A_BYTES + i * 16, __ldg(src + i));
-        }
-        tc::fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            tc::tc_fence_after();
-            const uint32_t bh = stage + Cfg::A_BYTES, bl = bh + NT * 32;
-            const uint64_t bdh = tc::make_sdesc(bh, 16, 256, 6), bdl = tc::make_sdesc(bl, 16, 256, 6);
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const uint32_t ah = stage + (2 * s) * TC_TILE_BYTES, al = ah + TC_TILE_BYTES;
-                const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(al, 16, 256, 6);
-                const uint32_t d = tmem + (uint32_t)(s * NT);
-                tc::mma_tf32(d, adh, bdh, idesc, it > 0 ? 1u : 0u);
-                tc::mma_tf32(d, adh, bdl, idesc, 1u);
-                tc::mma_tf32(d, adl, bdh, idesc, 1u);
-            }
-            tc::mma_commit(&empty_bar[st]);
-        }
-    }
-    if (tid == 0) tc::mma_commit(&done_bar);
-    tc::mbar_wait(&done_bar, 0);
-    tc::tc_fence_after();
-
-    // ---- epilogue: warp (w%4) owns TMEM lanes 32*(w%4).., w/4 picks the column half
-    const int q = warp & 3, half = warp >> 2;
-    const int row = r0 + q * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    constexpr int HC = NT / 2;
-    if constexpr (MODE == 0) {
-#pragma unroll 1
-        for (int s = 0; s < S; ++s) {
-#pragma unroll 1
-            for (int c = 0; c < HC; c += 16) {
-                const int col = half * HC + c;
-                float v[16];
-                tc::tmem_ld16(tl + (uint32_t)(s * NT + col), v);
-                tc::tmem_ld_wait();
-                float* dst = g.out + s * RN + (int64_t)row * g.N + n0 + col;
-                if (s == 0) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = store_value<ACT>(v[j] + __ldg(g.bias + n0 + col + j));
-                }
-#pragma unroll
-                for (int j = 0; j < 16; j += 4)
-                    *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            }
-        }
-    } else {
-#pragma unroll 1
-        for (int c = 0; c < HC; c += 8) {
-            const int col = half * HC + c;
-            float hb[S][8], z[S][8];
-#pragma unroll
-            for (int s = 0; s < S; ++s) tmem_ld8(tl + (uint32_t)(s * NT + col), hb[s]);
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const float* zp = g.Zlow + s * RN + (int64_t)row * g.N + n0 + col;
-                const float4 a = ldg4(zp), b = ldg4(zp + 4);
-                z[s][0] = a.x; z[s][1] = a.y; z[s][2] = a.z; z[s][3] = a.w;
-                z[s][4] = b.x; z[s][5] = b.y; z[s][6] = b.z; z[s][7] = b.w;
-            }
-            tc::tmem_ld_wait();
-            float zb[S][8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                float zz[S], hh[S], oo[S];
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    zz[s] = z[s][j];
-                    hh[s] = hb[s][j];
-                }
-                act_bwd<L, ACT>(zz, hh, oo, 1.0f);
-#pragma unroll
-                for (int s = 0; s < S; ++s) zb[s][j] = oo[s];
-            }
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                float* dst = g.out + s * RN + (int64_t)row * g.N + n0 + col;
-                *reinterpret_cast<float4*>(dst) = make_float4(zb[s][0], zb[s][1], zb[s][2], zb[s][3]);
-                *reinterpret_cast<float4*>(dst + 4) = make_float4(zb[s][4], zb[s][5], zb[s][6], zb[s][7]);
-            }
-        }
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tc::tmem_dealloc<512>(tmem);
-}
-
 // ---------------------------------------------------------------------------
 // weight gradient: per row tile of TC_WROWS rows,
 //   wpart[tile][k][n] = sum_{rows, s} act(Z_in)[s][row][k] * Zb[s][row][n]
@@ -309,195 +148,21 @@ __global__ void __launch_bounds__(256, 1) k_tc_layer(TcGemmArgs g) {
 struct TcWgradArgs {
     const float* A;   // Z_in / Hin [S][Rpad][Kin]
     const float* Bm;  // Zb_out [S][Rpad][N]
+    CUtensorMap tmA;  // A as [S][Rpad][Kin], box {128, 8, S}
+    CUtensorMap tmB;  // Bm as [S][Rpad][N], box {N, 8, S}
     float* wpart;
     double* dbpart;
     int Rpad, nrows, Kin, N;
 };
 
-template <int S, int MT, int N>
-struct TcWgCfg {
-    static constexpr int A_BYTES = 2 * MT * TC_TILE_BYTES;
-    static constexpr int B_BYTES = 2 * N * 32;
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int NST = (TC_SMEM - 1024) / STAGE > 8 ? 8 : (TC_SMEM - 1024) / STAGE;
-};
-
-template <int L, int PRO, int MT, int N>
-__global__ void __launch_bounds__(256, 1) k_tc_wgrad(TcWgradArgs g) {
-    constexpr int S = Streams<L>::S;
-    using St = Streams<L>;
-    using Cfg = TcWgCfg<S, MT, N>;
-    constexpr int NST = Cfg::NST;
-    constexpr int KIN = MT * 128;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = align1024(smem_raw);
-    __shared__ uint64_t empty_bar[8];
-    __shared__ uint64_t done_bar;
-    __shared__ uint32_t tmem_base;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int rbeg = blockIdx.x * TC_WROWS;
-    const int rend = min(g.Rpad, rbeg + TC_WROWS);
-    const int nrb = (rend - rbeg) / 8;
-    const int nit = nrb * S;
-    const int64_t RK = (int64_t)g.Rpad * KIN, RN = (int64_t)g.Rpad * N;
-
-    if (tid == 0) {
-        for (int i = 0; i < NST; ++i) tc::mbar_init(&empty_bar[i], 1);
-        tc::mbar_init(&done_bar, 1);
-        tc::fence_barrier_init();
-    }
-    if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-    const uint32_t tmem = tmem_base;
-    const uint32_t sbase = tc::smem_u32(smem);
-    constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, N, 0, 0);
-
-    // producer mapping: r = row within the 8-row block, f = 8-feature block
-    const int pr = tid & 7, pf = tid >> 3;  // pf in [0, 32)
-    double dbacc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) dbacc[j] = 0.0;
-
-    for (int it = 0; it < nit; ++it) {
-        const int st = it % NST;
-        const uint32_t stage = sbase + st * Cfg::STAGE;
-        const int rb = it / S, s = it % S;
-        const int row = rbeg + rb * 8 + pr;
-        if (it >= NST) tc::mbar_wait(&empty_bar[st], (uint32_t)((it / NST) - 1) & 1u);
-        // ---- A(m = k_in, k = row) = act(Z_in)[s][row][k_in]
-        for (int fb = pf; fb < KIN / 8; fb += 32) {
-            const int f = fb * 8;
-            float h[8];
-            if constexpr (PRO == ACT_NONE) {
-                const float* p = g.A + s * RK + (int64_t)row * KIN + f;
-                const float4 a = ldg4(p), b = ldg4(p + 4);
-                h[0] = a.x; h[1] = a.y; h[2] = a.z; h[3] = a.w; h[4] = b.x; h[5] = b.y; h[6] = b.z; h[7] = b.w;
-            } else {
-                // tanh storage: value stream holds t; needs t, z_s (+ partner)
-                const float* p0 = g.A + (int64_t)row * KIN + f;
-                const float4 t0 = ldg4(p0), t1 = ldg4(p0 + 4);
-                const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-                if (s == 0) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) h[j] = tv[j];
-                } else {
-                    const float* ps = g.A + s * RK + (int64_t)row * KIN + f;
-                    const float4 a = ldg4(ps), b = ldg4(ps + 4);
-                    const float zs[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-                    int par = -1;
-#pragma unroll
-                    for (int q2 = 1; q2 < S; ++q2)
-                        if (q2 == s) par = St::partner(q2);
-                    if (par < 0) {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) h[j] = (1.0f - tv[j] * tv[j]) * zs[j];
-                    } else {
-                        const float* pp = g.A + par * RK + (int64_t)row * KIN + f;
-                        const float4 c = ldg4(pp), d = ldg4(pp + 4);
-                        const float za[8] = {c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            h[j] = (1.0f - tv[j] * tv[j]) * (zs[j] - 2.0f * tv[j] * za[j] * za[j]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                const int j = (jj + (pf & 3)) & 7;  // rotate to spread banks
-                const int m = f + j;
-                float hi, lo;
-                tc::split3(h[j], hi, lo);
-                const uint32_t o = (uint32_t)(m >> 7) * 2 * TC_TILE_BYTES + tc::sw32_off((uint32_t)(m & 127), (uint32_t)pr);
-                sts32(stage + o, hi);
-                sts32(stage + o + TC_TILE_BYTES, lo);
-            }
-        }
-        // ---- B(n = n_out, k = row) = Zb[s][row][n]
-        for (int nb = pf; nb < N / 8; nb += 32) {
-            const int n = nb * 8;
-            const float* p = g.Bm + s * RN + (int64_t)row * N + n;
-            const float4 a = ldg4(p), b = ldg4(p + 4);
-            const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            if (s == 0) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) dbacc[j] += (double)v[j];
-            }
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                const int j = (jj + (pf & 3)) & 7;
-                float hi, lo;
-                tc::split3(v[j], hi, lo);
-                const uint32_t o = tc::sw32_off((uint32_t)(n + j), (uint32_t)pr);
-                sts32(stage + Cfg::A_BYTES + o, hi);
-                sts32(stage + Cfg::A_BYTES + N * 32 + o, lo);
-            }
-        }
-        tc::fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            tc::tc_fence_after();
-            const uint32_t bh = stage + Cfg::A_BYTES, bl = bh + N * 32;
-            const uint64_t bdh = tc::make_sdesc(bh, 16, 256, 6), bdl = tc::make_sdesc(bl, 16, 256, 6);
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                const uint32_t ah = stage + mt * 2 * TC_TILE_BYTES, al = ah + TC_TILE_BYTES;
-                const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(al, 16, 256, 6);
-                const uint32_t d = tmem + (uint32_t)(mt * N);
-                tc::mma_tf32(d, adh, bdh, idesc, it > 0 ? 1u : 0u);
-                tc::mma_tf32(d, adh, bdl, idesc, 1u);
-                tc::mma_tf32(d, adl, bdh, idesc, 1u);
-            }
-            tc::mma_commit(&empty_bar[st]);
-        }
-    }
-    if (tid == 0) tc::mma_commit(&done_bar);
-    tc::mbar_wait(&done_bar, 0);
-    tc::tc_fence_after();
-
-    // ---- epilogue: FP32 partial dW of this row tile
-    const int q = warp & 3, grp = warp >> 2;  // grp: M tile (MT == 2) or column half (MT == 1)
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    float* wp = g.wpart + (int64_t)blockIdx.x * KIN * N;
-    if (nit > 0) {
-        const int mt = MT == 2 ? grp : 0;
-        const int c0 = MT == 2 ? 0 : grp * (N / 2), c1 = MT == 2 ? N : c0 + N / 2;
-        const int k = mt * 128 + q * 32 + lane;
-#pragma unroll 1
-        for (int c = c0; c < c1; c += 16) {
-            float v[16];
-            tc::tmem_ld16(tl + (uint32_t)(mt * N + c), v);
-            tc::tmem_ld_wait();
-            float* dst = wp + (int64_t)k * N + c;
-#pragma unroll
-            for (int j = 0; j < 16; j += 4)
-                *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        }
-    } else {
-        for (int i = tid; i < KIN * N; i += 256) wp[i] = 0.0f;
-    }
-    // db: reduce the 8 row lanes (lane bits 0..2) of each 8-column block
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        double v = dbacc[j];
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        dbacc[j] = v;
-    }
-    if (pr == 0 && pf < N / 8)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) g.dbpart[(int64_t)blockIdx.x * N + pf * 8 + j] = dbacc[j];
-    tc::tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tc::tmem_dealloc<512>(tmem);
-}
+// Host: 3-D fp32 tensor map over [d2][d1][d0] (d0 contiguous), box {b0, b1, b2},
+// no swizzle (the box lands in smem as a dense [b2][b1][b0] array).
+int tc_make_tmap_3d(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
+                    uint32_t b1, uint32_t b2);
 
 // part[k*N + n] += sum_t wpart[t][k][n] ; part[K*N + n] += sum_t dbpart[t][n]  (FP64, fixed order)
 static __global__ void k_tc_wreduce(const float* __restrict__ wpart, const double* __restrict__ dbpart, int ntiles,
-                             int K, int N, double* __restrict__ part) {
+                                    int K, int N, double* __restrict__ part) {
     const int64_t KN = (int64_t)K * N;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < KN + N; i += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -511,8 +176,25 @@ static __global__ void k_tc_wreduce(const float* __restrict__ wpart, const doubl
 }
 
 // ---------------------------------------------------------------------------
-// host-side dispatch
-// ---------------------------------------------------------------------------
+// Rows per weight-gradient CTA: larger tiles amortise the per-CTA prologue and
+// accumulator drain (~40K cycles vs ~150K per 512 rows) but quantise the grid
+// into coarser waves; pick the cheaper of 512 / 1024 under that model.
+inline int tc_wgrad_rows(int64_t Rpad, int Kin, int nsm) {
+    const int mt = Kin / 128;
+    double best = 1e30;
+    int pick = TC_WROWS;
+    for (int wr = TC_WROWS; wr <= 2 * TC_WROWS; wr *= 2) {
+        const int64_t ctas = ((Rpad + wr - 1) / wr) * mt;
+        const int64_t waves = (ctas + nsm - 1) / nsm;
+        const double cost = (double)waves * (40.0 + 150.0 * wr / TC_WROWS);
+        if (cost < best * 0.999) {
+            best = cost;
+            pick = wr;
+        }
+    }
+    return pick;
+}
+
 inline bool tc_layer_ok(int S, int K, int N) {
     const int NT = tc_nt(S);
     return S <= 5 && K % 32 == 0 && K >= 32 && K <= 256 && N % NT == 0 && N <= 256 && (K == 128 || K == 256);
@@ -572,6 +254,7 @@ __device__ unsigned long long g_tc_trace[8];
 #define TC_ACC(i)
 #endif
 constexpr int TC2_THREADS = 416;
+constexpr int TCW_THREADS = 640;  // 16 converter + 4 MMA/loader/epilogue warps
 constexpr int TC3_THREADS = 544;  // 8 producer + 1 MMA + 8 epilogue warps
 constexpr int TC2_PROD = 256;
 
@@ -834,183 +517,222 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
 //   wpart[tile][mt*128 + m][n] = sum_{rows, s} act(Z_in)[s][row][k_in] Zb[s][row][n]
 // A (m = k_in, k = row) and B (n = n_out, k = row) are MN-major SW128_32B tiles
 // written with 16 B stores straight from the row-major activations.
-template <int NF>
+// Weight gradient, bulk-fed. One thread (an epilogue warp's lane 0; those warps
+// are idle until the accumulators are final) streams raw 8-row blocks of every
+// stream -- Z_in rows of this M tile and Zb_out rows -- into a ring with one
+// tensor-map TMA per operand, so load latency is covered by the ring depth
+// instead of producer registers. Two groups of 8 converter warps take alternate
+// k-steps: jet activation of the layer input, hi/lo split, swizzled store.
+//
+// PAIR (Kin = 256): a 2-CTA cluster covers both 128-feature M tiles of a row
+// block with cta_group::2 MMAs (M = 256). Each CTA converts its own A rows and
+// HALF of the B columns, so the B work the two single-CTA M tiles used to
+// duplicate is shared, and per-SM operand smem reads drop by a third.
+template <int S, int NF, bool PAIR>
 struct Tc2WgCfg {
-    static constexpr int A_T = 8 * 128 * 4;  // 8 rows x 128 k_in
-    static constexpr int B_T = 8 * NF * 4;
+    static constexpr int NFL = PAIR ? NF / 2 : NF;  // B columns staged by this CTA
+    static constexpr int A_T = 8 * 128 * 4;         // 8 rows x 128 k_in (one stream)
+    static constexpr int B_T = 8 * NFL * 4;         // 8 rows x NFL
     static constexpr int STAGE = 2 * A_T + 2 * B_T;
-    static constexpr int NST = (TC_SMEM - 16384) / STAGE > 8 ? 8 : (TC_SMEM - 16384) / STAGE;
+    static constexpr int RAW_A = S * A_T;
+    static constexpr int RAW = RAW_A + S * B_T;  // one 8-row block, all streams
+    static constexpr int BUDGET = 226 * 1024;
+    static constexpr int NR0 = (BUDGET - 4 * STAGE) / RAW;
+    static constexpr int NR = NR0 > 4 ? 4 : NR0;
+    static constexpr int NST0 = (BUDGET - NR * RAW) / STAGE;
+    static constexpr int NST = NST0 > 8 ? 8 : NST0;
+    static constexpr int SMEM = NR * RAW + NST * STAGE + 1024;
+    static_assert(NR >= 2 && NST >= 2, "weight-gradient rings");
+    static_assert(NR * RAW >= 2 * 8 * NFL * 8, "db reduction reuses the raw ring");
 };
 
-template <int L, int PRO, int NF>
-__global__ void __launch_bounds__(TC2_THREADS, 1) k_tc2_wgrad(TcWgradArgs g, int wrows) {
+template <int L, int PRO, int NF, bool PAIR>
+__global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_constant__ TcWgradArgs g, int wrows) {
     using St = Streams<L>;
     constexpr int S = St::S;
-    using Cfg = Tc2WgCfg<NF>;
-    constexpr int NST = Cfg::NST;
+    using Cfg = Tc2WgCfg<S, NF, PAIR>;
+    constexpr int NST = Cfg::NST, NR = Cfg::NR, NFL = Cfg::NFL;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
-    __shared__ uint64_t full[8], empty[8], tfull;
+    __shared__ uint64_t full[8], empty[8], rfull[4], rempty[4], tfull;
     __shared__ uint32_t tmem_base;
-    __shared__ double dbred[8][NF];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int MT = g.Kin / 128;
-    const int tile = blockIdx.x / MT, mt = blockIdx.x % MT;
+    const int tile = blockIdx.x / MT, mt = blockIdx.x % MT;  // PAIR: mt == cluster rank
     const int rbeg = tile * wrows;
     const int rend = min(g.Rpad, rbeg + wrows);
-    const int nit = ((rend - rbeg) / 8) * S;
-    const int64_t RK = (int64_t)g.Rpad * g.Kin, RN = (int64_t)g.Rpad * NF;
+    const int nblk = (rend - rbeg) / 8;
+    const int nit = nblk * S;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
-            tc::mbar_init(&full[i], 8);
+            tc::mbar_init(&full[i], PAIR ? 16 : 8);  // the converter group(s) filling stage i
             tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < NR; ++i) {
+            tc::mbar_init(&rfull[i], 1);
+            tc::mbar_init(&rempty[i], 16);
         }
         tc::mbar_init(&tfull, 1);
         tc::fence_barrier_init();
     }
-    if (warp == 8) tc::tmem_alloc<512>(&tmem_base);
+    if (warp == 16) {
+        if constexpr (PAIR) tc::tmem_alloc_pair<512>(&tmem_base);
+        else tc::tmem_alloc<512>(&tmem_base);
+    }
     tc::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) tc::cluster_sync();
+    else __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
-    const uint32_t sbase = tc::smem_u32(smem);
+    const uint32_t sraw = tc::smem_u32(smem);
+    const uint32_t sbase = sraw + NR * Cfg::RAW;
 
-    if (warp < 8) {
-        // A: thread -> (row r = tid/32, 4 features at 4*(tid%32)) ; B: 2 chunks of 4 n
-        const int ar = tid >> 5, ac = tid & 31;
-        const int f = mt * 128 + ac * 4;
+    if (warp < 16) {
+        // A: thread -> (row ar, features 4*ac); B: up to 2 chunks of 4 columns
+        const int grp = tid >> 8, gtid = tid & 255;
+        const int ar = gtid >> 5, ac = gtid & 31;
         const uint32_t aoff = tc::mn32_off((uint32_t)ar, (uint32_t)(ac * 4), 128u);
-        constexpr int BCH = NF / 4;  // float4 chunks per row
-        int brow[2], bc[2];
+        const uint32_t araw = (uint32_t)((ar * 128 + ac * 4) * 4);
+        constexpr int BCH = NFL / 4;  // float4 chunks per row
+        constexpr int NB = (8 * BCH + 255) / 256;
+        int brow[2];
         uint32_t boff[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const int idx = tid + 256 * j;
-            brow[j] = idx / BCH;
-            bc[j] = idx % BCH;
-            boff[j] = tc::mn32_off((uint32_t)(brow[j] & 7), (uint32_t)(bc[j] * 4), (uint32_t)NF);
+            const int idx = gtid + 256 * j;
+            brow[j] = j < NB ? idx / BCH : 8;
+            boff[j] = tc::mn32_off((uint32_t)(brow[j] & 7), (uint32_t)((idx % BCH) * 4), (uint32_t)NFL);
         }
+        const uint32_t full0 = PAIR ? tc::mapa(tc::smem_u32(&full[0]), 0) : tc::smem_u32(&full[0]);
         double dbacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-#ifdef PNX_WG_D
-        constexpr int D = PNX_WG_D;
-#else
-        constexpr int D = 2;  // register prefetch depth (stages)
-#endif
-        float4 ring[D][5];
-        auto load = [&](int it, float4* v) {
-#ifdef PNX_EXP_NOLOAD
-#pragma unroll
-            for (int j = 0; j < 5; ++j) v[j] = make_float4(0.01f * it, 0.2f, 0.3f, 0.4f);
-            return;
-#endif
-            const int rb = it / S, s = it % S;
-            const int row = rbeg + rb * 8 + ar;
-            const float* pa = g.A + (int64_t)row * g.Kin + f;
-            if constexpr (PRO == ACT_NONE) {
-                v[0] = ldg4(pa + s * RK);
-            } else {
-                v[0] = ldg4(pa);
-                if (s > 0) v[1] = ldg4(pa + s * RK);
-                int par = -1;
-#pragma unroll
-                for (int q2 = 1; q2 < S; ++q2)
-                    if (q2 == s) par = St::partner(q2);
-                if (par >= 0) v[2] = ldg4(pa + par * RK);
+        for (int b = 0; b < nblk; ++b) {
+            const int rs = b % NR;
+            const uint32_t raw = sraw + rs * Cfg::RAW;
+            {
+                TC_T0();
+                tc::mbar_wait(&rfull[rs], (uint32_t)(b / NR) & 1u);
+                if (tid == 0) TC_ACC(1);
             }
+            const float4 t = lds128(raw + araw);
+            // group 0 converts streams [0, SG), group 1 streams [SG, S) of this
+            // block: independent k-steps interleave (ILP) and share one fence
+            auto convert = [&](auto lo_c, auto hi_c) {
+                constexpr int SLO = decltype(lo_c)::value, SHI = decltype(hi_c)::value, NS = SHI - SLO;
+#ifdef PNX_TC_TRACE
+                long long _tc = clock64();
+#endif
+                float4 ahi[NS], alo[NS], bhi[NS][2], blo[NS][2];
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-                if (brow[j] < 8) v[3 + j] = ldg4(g.Bm + s * RN + (int64_t)(rbeg + rb * 8 + brow[j]) * NF + bc[j] * 4);
-        };
-#pragma unroll
-        for (int d = 0; d < D; ++d)
-            if (d < nit) load(d, ring[d]);
-        for (int it0 = 0; it0 < nit; it0 += D) {
-#pragma unroll
-            for (int slot = 0; slot < D; ++slot) {
-                const int it = it0 + slot;
-                if (it >= nit) break;
-                const int st = it % NST, s = it % S;
-                const uint32_t stage = sbase + st * Cfg::STAGE;
-                float4 v[5];
-#pragma unroll
-                for (int j = 0; j < 5; ++j) v[j] = ring[slot][j];
-                if (it + D < nit) load(it + D, ring[slot]);
-                float4 h;
-                if constexpr (PRO == ACT_NONE) {
-                    h = v[0];
-                } else {
-                    const float4 t = v[0];
-                    if (s == 0) {
+                for (int i = 0; i < NS; ++i) {
+                    const int s = SLO + i;
+                    float4 h;
+                    if constexpr (PRO == ACT_NONE) {
+                        h = s == 0 ? t : lds128(raw + s * Cfg::A_T + araw);
+                    } else if (s == 0) {
                         h = t;
                     } else {
-                        int par = -1;
-#pragma unroll
-                        for (int q2 = 1; q2 < S; ++q2)
-                            if (q2 == s) par = St::partner(q2);
-                        const float4 z = v[1];
+                        const float4 z = lds128(raw + s * Cfg::A_T + araw);
+                        const int par = St::partner(s);
                         if (par < 0) {
-                            h = make_float4((1.f - t.x * t.x) * z.x, (1.f - t.y * t.y) * z.y, (1.f - t.z * t.z) * z.z,
-                                            (1.f - t.w * t.w) * z.w);
+                            h = make_float4((1.f - t.x * t.x) * z.x, (1.f - t.y * t.y) * z.y,
+                                            (1.f - t.z * t.z) * z.z, (1.f - t.w * t.w) * z.w);
                         } else {
-                            const float4 za = v[2];
+                            const float4 za = lds128(raw + par * Cfg::A_T + araw);
                             h = make_float4((1.f - t.x * t.x) * (z.x - 2.f * t.x * za.x * za.x),
                                             (1.f - t.y * t.y) * (z.y - 2.f * t.y * za.y * za.y),
                                             (1.f - t.z * t.z) * (z.z - 2.f * t.z * za.z * za.z),
                                             (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
                         }
                     }
-                }
-                float4 ahi, alo, bhi[2], blo[2];
-                split4(h, ahi, alo);
+                    split4(h, ahi[i], alo[i]);
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    if (brow[j] >= 8) continue;
-                    if (s == 0) {
-                        dbacc[j][0] += v[3 + j].x;
-                        dbacc[j][1] += v[3 + j].y;
-                        dbacc[j][2] += v[3 + j].z;
-                        dbacc[j][3] += v[3 + j].w;
+                    for (int j = 0; j < 2; ++j) {
+                        if (brow[j] >= 8) continue;
+                        const float4 bv = lds128(raw + Cfg::RAW_A + s * Cfg::B_T + (gtid + 256 * j) * 16);
+                        if (s == 0) {
+                            dbacc[j][0] += bv.x;
+                            dbacc[j][1] += bv.y;
+                            dbacc[j][2] += bv.z;
+                            dbacc[j][3] += bv.w;
+                        }
+                        split4(bv, bhi[i][j], blo[i][j]);
                     }
-                    split4(v[3 + j], bhi[j], blo[j]);
                 }
-                {
-                    TC_T0();
-                    tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
-                    if (tid == 0) TC_ACC(2);
-                }
-                sts128(stage + aoff, ahi);
-                sts128(stage + Cfg::A_T + aoff, alo);
+#ifdef PNX_TC_TRACE
+                if (tid == 0) atomicAdd(&g_tc_trace[5], (unsigned long long)(clock64() - _tc));
+#endif
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    if (brow[j] >= 8) continue;
-                    sts128(stage + 2 * Cfg::A_T + boff[j], bhi[j]);
-                    sts128(stage + 2 * Cfg::A_T + Cfg::B_T + boff[j], blo[j]);
+                for (int i = 0; i < NS; ++i) {
+                    const int it = b * S + SLO + i;
+                    const int st = it % NST;
+                    const uint32_t stage = sbase + st * Cfg::STAGE;
+                    {
+                        TC_T0();
+                        tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                        if (tid == 0) TC_ACC(2);
+                    }
+#ifdef PNX_TC_TRACE
+                    _tc = clock64();
+#endif
+                    sts128(stage + aoff, ahi[i]);
+                    sts128(stage + Cfg::A_T + aoff, alo[i]);
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        if (brow[j] >= 8) continue;
+                        sts128(stage + 2 * Cfg::A_T + boff[j], bhi[i][j]);
+                        sts128(stage + 2 * Cfg::A_T + Cfg::B_T + boff[j], blo[i][j]);
+                    }
                 }
                 tc::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&full[st]);
-            }
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < NS; ++i) {
+                        const int st = (b * S + SLO + i) % NST;
+                        if constexpr (PAIR) tc::mbar_arrive_cluster(full0 + st * 8);
+                        else tc::mbar_arrive(&full[st]);
+                    }
+                }
+#ifdef PNX_TC_TRACE
+                if (tid == 0) atomicAdd(&g_tc_trace[6], (unsigned long long)(clock64() - _tc));
+#endif
+            };
+            constexpr int SG = (S + 1) / 2;
+            if (grp == 0) convert(std::integral_constant<int, 0>{}, std::integral_constant<int, SG>{});
+            else convert(std::integral_constant<int, SG>{}, std::integral_constant<int, S>{});
+            __syncwarp();  // raw block fully read by this warp
+            if (lane == 0) tc::mbar_arrive(&rempty[rs]);
         }
-        // db (M tile 0 only): rows of a chunk are spread over threads with equal idx % BCH
-        if (mt == 0) {
-            for (int i = tid; i < 8 * NF; i += 256) (&dbred[0][0])[i] = 0.0;
-            asm volatile("bar.sync 1, 256;");
+        // db (one CTA per column range): fixed-order sum over [group][row slot],
+        // staged in the (now idle: every block was consumed) raw ring
+        if (PAIR || mt == 0) {
+            double* dbred = reinterpret_cast<double*>(smem);  // [grp][8 row slots][NFL]
+            asm volatile("bar.sync 1, 512;");
+            for (int i = tid; i < 2 * 8 * NFL; i += 512) dbred[i] = 0.0;
+            asm volatile("bar.sync 1, 512;");
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const int idx = tid + 256 * j;
-                if (idx / BCH >= 8) continue;
-                const int grp = idx / BCH;  // one slot per row of the 8-row block (fixed-order sum below)
-                for (int c = 0; c < 4; ++c) dbred[grp][(idx % BCH) * 4 + c] += dbacc[j][c];
+                if (brow[j] >= 8) continue;
+                const int idx = gtid + 256 * j;
+                double* d = dbred + (grp * 8 + idx / BCH) * NFL + (idx % BCH) * 4;
+                for (int c = 0; c < 4; ++c) d[c] += dbacc[j][c];
             }
-            asm volatile("bar.sync 1, 256;");
-            for (int n = tid; n < NF; n += 256)
-                g.dbpart[(int64_t)tile * NF + n] = ((dbred[0][n] + dbred[1][n]) + (dbred[2][n] + dbred[3][n])) +
-                                                   ((dbred[4][n] + dbred[5][n]) + (dbred[6][n] + dbred[7][n]));
+            asm volatile("bar.sync 1, 512;");
+            const int c0 = PAIR ? mt * NFL : 0;
+            for (int n = tid; n < NFL; n += 512) {
+                double v[16];
+                for (int i = 0; i < 16; ++i) v[i] = dbred[i * NFL + n];
+                g.dbpart[(int64_t)tile * NF + c0 + n] =
+                    (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
+                    (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+            }
         }
-    } else if (warp == 8) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NF, 1, 1);
+    } else {
+        // warp 16 lane 0 issues the MMAs, warp 17 lane 0 streams the raw blocks;
+        // then warps 16-19 drain TMEM (warp % 4 = lane quarter)
+        if (warp == 16 && lane == 0 && (!PAIR || mt == 0)) {
+            constexpr uint32_t idesc = tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NF, 1, 1);
             const uint32_t dbig = tmem, dsmall = tmem + NF;
             for (int it = 0; it < nit; ++it) {
                 const int st = it % NST;
@@ -1023,17 +745,36 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_tc2_wgrad(TcWgradArgs g, int
                 tc::tc_fence_after();
                 const uint64_t ah = tc::make_sdesc(stage, 512, 4 * 512, 1);
                 const uint64_t al = tc::make_sdesc(stage + Cfg::A_T, 512, 4 * 512, 1);
-                const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 512, (NF / 32) * 512, 1);
-                const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 512, (NF / 32) * 512, 1);
-                tc::mma_tf32(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
-                tc::mma_tf32(dsmall, ah, bl, idesc, it > 0 ? 1u : 0u);
-                tc::mma_tf32(dsmall, al, bh, idesc, 1u);
-                tc::mma_commit(&empty[st]);
+                const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 512, (NFL / 32) * 512, 1);
+                const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 512, (NFL / 32) * 512, 1);
+                if constexpr (PAIR) {
+                    tc::mma_tf32_pair(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
+                    tc::mma_tf32_pair(dsmall, ah, bl, idesc, it > 0 ? 1u : 0u);
+                    tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
+                    tc::mma_commit_pair(&empty[st], 3);
+                } else {
+                    tc::mma_tf32(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
+                    tc::mma_tf32(dsmall, ah, bl, idesc, it > 0 ? 1u : 0u);
+                    tc::mma_tf32(dsmall, al, bh, idesc, 1u);
+                    tc::mma_commit(&empty[st]);
+                }
             }
-            tc::mma_commit(&tfull);
+            if constexpr (PAIR) tc::mma_commit_pair(&tfull, 3);
+            else tc::mma_commit(&tfull);
+        }
+        if (warp == 17 && lane == 0) {
+            // raw-block loader: two tensor-map copies per 8-row block
+            for (int b = 0; b < nblk; ++b) {
+                const int rs = b % NR;
+                const uint32_t raw = sraw + rs * Cfg::RAW;
+                tc::mbar_wait(&rempty[rs], ((uint32_t)(b / NR) & 1u) ^ 1u);
+                tc::mbar_arrive_expect_tx(&rfull[rs], Cfg::RAW);
+                const int row0 = rbeg + b * 8;
+                tc::tma_load_3d(raw, &g.tmA, mt * 128, row0, 0, &rfull[rs]);
+                tc::tma_load_3d(raw + Cfg::RAW_A, &g.tmB, PAIR ? mt * NFL : 0, row0, 0, &rfull[rs]);
+            }
         }
         __syncwarp();
-    } else {
         const int q = warp & 3;
         const int m = q * 32 + lane;
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
@@ -1057,14 +798,14 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_tc2_wgrad(TcWgradArgs g, int
         }
     }
     tc::tc_fence_before();
-    __syncthreads();
-    if (warp == 8) tc::tmem_dealloc<512>(tmem);
+    if constexpr (PAIR) tc::cluster_sync();
+    else __syncthreads();
+    if (warp == 16) {
+        if constexpr (PAIR) tc::tmem_dealloc_pair<512>(tmem);
+        else tc::tmem_dealloc<512>(tmem);
+    }
 }
 
-
-// reverse: Zb_in[s] = act^T(Zb_out[s] W^T ; Z_in), all S streams of a
-// 128-row x NT-column tile resident in TMEM (the tanh jet transpose couples the
-// streams), one accumulator per stream; weights streamed by cp.async.bulk.
 template <int S, int NT>
 struct Tc2BwdCfg {
     static constexpr int A_BYTES = 2 * S * TC_TILE_BYTES;

@@ -6,8 +6,8 @@
 
 namespace pnx {
 
-int tc_make_tmap_3d(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
-                    uint32_t b1, uint32_t b2) {
+int tc_make_tmap(CUtensorMap* map, const float* base, int rank, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
+                 uint32_t b1, uint32_t b2, bool sw128) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -21,8 +21,9 @@ int tc_make_tmap_3d(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d
     const cuuint64_t strides[2] = {d0 * 4, d0 * d1 * 4};
     const cuuint32_t box[3] = {b0, b1, b2};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<float*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : -1;
 }
@@ -72,8 +73,41 @@ int launch_tc2_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
     kern<<<g.Rpad / TC_M, TC3_THREADS, smem, st>>>(g);
     return 0;
 }
+template <int L, int PRO>
+int launch_tc4_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
+    using Cfg = Tc4FwdCfg<L>;
+    const int smem = Cfg::SMEM;
+    auto kern = k_tc4_fwd<L, PRO>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
+        attr = true;
+    }
+    TcGemmArgs a = g;
+    constexpr int S = Streams<L>::S;
+    const int nkb = g.K / 8;
+    if (tc_make_tmap(&a.tmA, g.A, 3, g.K, g.Rpad, S, 32, 128, 1, true) ||
+        tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)nkb * 2 * Cfg::NF, 1, 8, 128, 1, false))
+        return -1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.Rpad / TC_M);
+    cfg.blockDim = dim3(TC4_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? 0 : -1;
+}
 template <int L>
 int launch_tc2_fwd_l(int pro, const TcGemmArgs& g, cudaStream_t st) {
+    static const bool pair = getenv("PNX_FWD_NOPAIR") == nullptr;
+    if (g.N == 256 && pair && g.Rpad % 256 == 0 && g.K % 32 == 0)
+        return pro == ACT_NONE ? launch_tc4_fwd_t<L, ACT_NONE>(g, st) : launch_tc4_fwd_t<L, ACT_TANH>(g, st);
     if (g.N == 256) return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 256>(g, st) : launch_tc2_fwd_t<L, ACT_TANH, 256>(g, st);
     if (g.N == 128) return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 128>(g, st) : launch_tc2_fwd_t<L, ACT_TANH, 128>(g, st);
     return -1;

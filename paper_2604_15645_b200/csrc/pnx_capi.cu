@@ -240,7 +240,7 @@ int upload_rows(pnx_ctx* ctx) {
     ch = std::max<int64_t>(ch, small + 128);
     ch = std::min<int64_t>(ch, T);
     ctx->chunk_rows = ch;
-    const int64_t Rp = roundup(ch, 128);
+    const int64_t Rp = roundup(ch, 256);  // CTA-pair kernels tile 256 rows
     if (Rp > ctx->Rcap) {
         ctx->Rcap = Rp;
         const size_t SR = (size_t)ctx->S * Rp;
@@ -359,7 +359,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
 
     for (int64_t c0 = 0; c0 < T; c0 += ctx->chunk_rows) {
         const int nrows = (int)std::min<int64_t>(ctx->chunk_rows, T - c0);
-        const int Rpad = (int)roundup(nrows, 128);
+        const int Rpad = (int)roundup(nrows, 256);
         ia.row0 = c0;
         ia.nrows = nrows;
         ia.Rpad = Rpad;

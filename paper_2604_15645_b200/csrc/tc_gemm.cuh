@@ -136,6 +136,8 @@ struct TcGemmArgs {
     const float* Zlow;  // bwd: Z_in [S][Rpad][N]
     float* out;         // [S][Rpad][N]
     int Rpad, K, N;
+    CUtensorMap tmA;    // pair kernels: A as [S][Rpad][K], box {32, 128, 1}, 128 B swizzle
+    CUtensorMap tmB;    // pair kernels: weight image as rows of 8 fp32, box {8, 128}
 };
 
 // ---------------------------------------------------------------------------
@@ -155,10 +157,15 @@ struct TcWgradArgs {
     int Rpad, nrows, Kin, N;
 };
 
-// Host: 3-D fp32 tensor map over [d2][d1][d0] (d0 contiguous), box {b0, b1, b2},
-// no swizzle (the box lands in smem as a dense [b2][b1][b0] array).
-int tc_make_tmap_3d(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
-                    uint32_t b1, uint32_t b2);
+// Host: fp32 tensor map over [d2][d1][d0] (d0 contiguous; d2 = 1 for 2-D), box
+// {b0, b1, b2}. sw128: 128 B swizzle (16 B chunk c of box row r stored at c ^ (r % 8)),
+// else the box lands in smem as a dense [b2][b1][b0] array.
+int tc_make_tmap(CUtensorMap* map, const float* base, int rank, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
+                 uint32_t b1, uint32_t b2, bool sw128);
+inline int tc_make_tmap_3d(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
+                           uint32_t b1, uint32_t b2) {
+    return tc_make_tmap(map, base, 3, d0, d1, d2, b0, b1, b2, false);
+}
 
 // part[k*N + n] += sum_t wpart[t][k][n] ; part[K*N + n] += sum_t dbpart[t][n]  (FP64, fixed order)
 static __global__ void k_tc_wreduce(const float* __restrict__ wpart, const double* __restrict__ dbpart, int ntiles,
@@ -513,10 +520,237 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
     if (warp == 8) tc::tmem_dealloc<512>(tmem);
 }
 
-// weight gradient, one 128-wide k_in tile (mt) per CTA, big|small accumulators:
-//   wpart[tile][mt*128 + m][n] = sum_{rows, s} act(Z_in)[s][row][k_in] Zb[s][row][n]
-// A (m = k_in, k = row) and B (n = n_out, k = row) are MN-major SW128_32B tiles
-// written with 16 B stores straight from the row-major activations.
+// Forward, CTA pair (NF = 256): a 2-CTA cluster owns 256 rows; the leader issues
+// M=256 x N=256 cta_group::2 MMAs, each CTA holding its 128 rows of A and
+// HALF of the weight columns (B), so per-SM weight traffic and operand smem
+// reads drop by a third. Per CTA:
+//   warp 8  : TMEM owner; lane 0 streams raw A (32-feature x 128-row boxes of the
+//             streams a pass needs, 128 B swizzled) into a ring by tensor-map TMA
+//   warp 17 : lane 0 streams this CTA's weight-image half into the MMA stages,
+//             completing on the leader's full barrier (.cta_group::2 TMA)
+//   warps 0-7  : converters -- jet activation + hi/lo split of a whole 4-k-step
+//                group per thread, SW32 stores, one proxy fence per group
+//   warps 9-16 : epilogue (warp 9 lane 0 of the leader also issues the MMAs)
+template <int L>
+struct Tc4FwdCfg {
+    using St = Streams<L>;
+    static constexpr bool SECOND = St::order(St::S - 1) == 2;
+    static constexpr int NF = 256, NFL = 128;
+    static constexpr int A_T = TC_TILE_BYTES;  // 128 rows x 8 fp32
+    static constexpr int B_T = NFL * 32;       // 128 weight columns x 8 fp32
+    static constexpr int STAGE = 2 * A_T + 2 * B_T;
+    static constexpr int BOX = 128 * 32 * 4;   // 128 rows x 32 features
+    static constexpr int NBOX = SECOND ? 3 : 2;
+    static constexpr int RAW = NBOX * BOX;
+    static constexpr int NR = 2;
+    static constexpr int EPI_ROW = 144;
+    static constexpr int EPI_BYTES = 8 * 32 * EPI_ROW;
+    static constexpr int BUDGET = 226 * 1024;
+    static constexpr int NST0 = (BUDGET - NR * RAW - EPI_BYTES) / STAGE;
+    static constexpr int NST = NST0 > 8 ? 8 : NST0;
+    static constexpr int SMEM = NR * RAW + NST * STAGE + EPI_BYTES + 1024;
+    static_assert(NST >= 4, "forward stage ring");
+};
+constexpr int TC4_THREADS = 576;  // 18 warps
+
+template <int L, int PRO>
+__global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constant__ TcGemmArgs g) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    using Cfg = Tc4FwdCfg<L>;
+    constexpr int NST = Cfg::NST, NR = Cfg::NR, NF = Cfg::NF, NFL = Cfg::NFL;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    __shared__ uint64_t full[8], empty[8], rfull[2], rempty[2], tfull, tempty;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int r0 = (blockIdx.x >> 1) * 256 + (int)rank * 128;
+    const int nkb = g.K / 8, ngrp = g.K / 32;
+    const int64_t RN = (int64_t)g.Rpad * NF;
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            tc::mbar_init(&full[i], 17);  // 2 x 8 converter warps + the leader's expect_tx
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < NR; ++i) {
+            tc::mbar_init(&rfull[i], 1);
+            tc::mbar_init(&rempty[i], 8);
+        }
+        tc::mbar_init(&tfull, 1);
+        tc::mbar_init(&tempty, 16);
+        tc::fence_barrier_init();
+    }
+    if (warp == 8) tc::tmem_alloc_pair<512>(&tmem_base);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t sraw = tc::smem_u32(smem);
+    const uint32_t sbase = sraw + NR * Cfg::RAW;
+    const uint32_t sepi = sbase + NST * Cfg::STAGE;
+    const uint32_t full0 = tc::mapa(tc::smem_u32(&full[0]), 0);
+    const uint32_t tempty0 = tc::mapa(tc::smem_u32(&tempty), 0);
+    // raw boxes a pass needs: [0] = stream 0 (t), [1] = stream p, [2] = partner
+    auto nbox = [](int p) { return PRO == ACT_NONE ? 1 : (p == 0 ? 1 : (St::order(p) == 2 ? 3 : 2)); };
+
+    if (warp < 8) {
+        // ---------------- converters ----------------
+        const int row = tid >> 1, c = tid & 1;
+        const uint32_t aoff = tc::sw32_off((uint32_t)row, (uint32_t)(c * 4));
+        const uint32_t rrow = (uint32_t)row * 128;
+        const uint32_t rsw = (uint32_t)(row & 7);
+        for (int p = 0; p < S; ++p) {
+            for (int gi = 0; gi < ngrp; ++gi) {
+                const int gq = p * ngrp + gi, rs = gq % NR;
+                const uint32_t raw = sraw + rs * Cfg::RAW;
+                tc::mbar_wait(&rfull[rs], (uint32_t)(gq / NR) & 1u);
+                float4 hi[4], lo[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t off = rrow + ((((uint32_t)(2 * j + c)) ^ rsw) << 4);
+                    float4 h;
+                    if (PRO == ACT_NONE || p == 0) {
+                        h = lds128(raw + off);
+                    } else {
+                        const float4 t = lds128(raw + off), z = lds128(raw + Cfg::BOX + off);
+                        if (St::order(p) == 1) {
+                            h = make_float4((1.f - t.x * t.x) * z.x, (1.f - t.y * t.y) * z.y, (1.f - t.z * t.z) * z.z,
+                                            (1.f - t.w * t.w) * z.w);
+                        } else {
+                            const float4 za = lds128(raw + 2 * Cfg::BOX + off);
+                            h = make_float4((1.f - t.x * t.x) * (z.x - 2.f * t.x * za.x * za.x),
+                                            (1.f - t.y * t.y) * (z.y - 2.f * t.y * za.y * za.y),
+                                            (1.f - t.z * t.z) * (z.z - 2.f * t.z * za.z * za.z),
+                                            (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
+                        }
+                    }
+                    split4(h, hi[j], lo[j]);
+                }
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&rempty[rs]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int it = gq * 4 + j, st = it % NST;
+                    const uint32_t stage = sbase + st * Cfg::STAGE;
+                    tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                    sts128(stage + aoff, hi[j]);
+                    sts128(stage + Cfg::A_T + aoff, lo[j]);
+                }
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) tc::mbar_arrive_cluster(full0 + ((gq * 4 + j) % NST) * 8);
+                }
+            }
+        }
+    } else if (warp == 8) {
+        // ---------------- raw A loader ----------------
+        if (lane == 0) {
+            for (int p = 0; p < S; ++p) {
+                const int nb = nbox(p);
+                const int s1 = PRO == ACT_NONE ? p : 0;
+                for (int gi = 0; gi < ngrp; ++gi) {
+                    const int gq = p * ngrp + gi, rs = gq % NR;
+                    const uint32_t raw = sraw + rs * Cfg::RAW;
+                    tc::mbar_wait(&rempty[rs], ((uint32_t)(gq / NR) & 1u) ^ 1u);
+                    tc::mbar_arrive_expect_tx(&rfull[rs], nb * Cfg::BOX);
+                    tc::tma_load_3d(raw, &g.tmA, gi * 32, r0, s1, &rfull[rs]);
+                    if (nb > 1) tc::tma_load_3d(raw + Cfg::BOX, &g.tmA, gi * 32, r0, p, &rfull[rs]);
+                    if (nb > 2) tc::tma_load_3d(raw + 2 * Cfg::BOX, &g.tmA, gi * 32, r0, St::partner(p), &rfull[rs]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 17) {
+        // ---------------- weight-half loader ----------------
+        if (lane == 0) {
+            const int nit = S * nkb;
+            for (int it = 0; it < nit; ++it) {
+                const int st = it % NST, kb = it % nkb;
+                const uint32_t stage = sbase + st * Cfg::STAGE;
+                tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                if (rank == 0) tc::mbar_arrive_expect_tx(&full[st], 2 * 2 * Cfg::B_T);
+                const int rowb = kb * 2 * NF + (int)rank * NFL;  // image rows (8 fp32 each)
+                tc::tma_load_2d_pair(stage + 2 * Cfg::A_T, &g.tmB, 0, rowb, full0 + st * 8);
+                tc::tma_load_2d_pair(stage + 2 * Cfg::A_T + Cfg::B_T, &g.tmB, 0, rowb + NF, full0 + st * 8);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- MMA issue (leader, warp 9 lane 0) + epilogue ----------------
+        const int q = warp & 3, half = (warp - 9) >> 2;
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t stg = sepi + (uint32_t)(warp - 9) * 32 * Cfg::EPI_ROW;
+        for (int p = 0; p < S; ++p) {
+            if (warp == 9 && lane == 0 && rank == 0) {
+                constexpr uint32_t idesc = tc::make_idesc_tf32(2 * TC_M, NF, 0, 0);
+                tc::mbar_wait(&tempty, ((uint32_t)p & 1u) ^ 1u);
+                tc::tc_fence_after();
+                const uint32_t dbig = tmem, dsmall = tmem + NF;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    const int it = p * nkb + kb, st = it % NST;
+                    const uint32_t stage = sbase + st * Cfg::STAGE;
+                    {
+                        TC_T0();
+                        tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                        TC_ACC(0);
+                    }
+                    tc::tc_fence_after();
+                    const uint64_t ah = tc::make_sdesc(stage, 16, 256, 6), al = tc::make_sdesc(stage + Cfg::A_T, 16, 256, 6);
+                    const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 16, 256, 6);
+                    const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 16, 256, 6);
+                    tc::mma_tf32_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
+                    tc::mma_tf32_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+                    tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
+                    tc::mma_commit_pair(&empty[st], 3);
+                }
+                tc::mma_commit_pair(&tfull, 3);
+            }
+            __syncwarp();
+            tc::mbar_wait(&tfull, (uint32_t)p & 1u);
+            tc::tc_fence_after();
+            TC_T0();
+#pragma unroll 1
+            for (int c = half * (NF / 2); c < (half + 1) * (NF / 2); c += 32) {
+                float a[32], b[32];
+                tc::tmem_ld16(tl + (uint32_t)c, a);
+                tc::tmem_ld16(tl + (uint32_t)(c + 16), a + 16);
+                tc::tmem_ld16(tl + (uint32_t)(NF + c), b);
+                tc::tmem_ld16(tl + (uint32_t)(NF + c + 16), b + 16);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) a[j] += b[j];
+                if (p == 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));
+                }
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    sts128(stg + lane * Cfg::EPI_ROW + j * 4, make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]));
+                __syncwarp();
+                float* dst = g.out + p * RN + (int64_t)(r0 + q * 32) * NF + c;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int rr = 4 * k + (lane >> 3), cc = (lane & 7) * 4;
+                    const float4 v = lds128(stg + rr * Cfg::EPI_ROW + cc * 4);
+                    *reinterpret_cast<float4*>(dst + (int64_t)rr * NF + cc) = v;
+                }
+                __syncwarp();
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (warp == 9 && lane == 0) TC_ACC(3);
+            if (lane == 0) tc::mbar_arrive_cluster(tempty0);
+        }
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    if (warp == 8) tc::tmem_dealloc_pair<512>(tmem);
+}
+
 // Weight gradient, bulk-fed. One thread (an epilogue warp's lane 0; those warps
 // are idle until the accumulators are final) streams raw 8-row blocks of every
 // stream -- Z_in rows of this M tile and Zb_out rows -- into a ring with one

@@ -30,25 +30,43 @@ int tc_make_tmap(CUtensorMap* map, const float* base, int rank, uint64_t d0, uin
 
 // ---- tcgen05 dispatch --------------------------------------------------------
 
-template <int L, int NT>
+template <int L, int NT, bool PAIR>
 int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
-    using Cfg = Tc2BwdCfg<Streams<L>::S, NT>;
+    using Cfg = Tc2BwdCfg<Streams<L>::S, NT, PAIR>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc2_bwd<L, NT>;
+    auto kern = k_tc2_bwd<L, NT, PAIR>;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
         attr = true;
     }
-    kern<<<(g.Rpad / TC_M) * (g.N / NT), TC3_THREADS, smem, st>>>(g);
-    return 0;
+    TcGemmArgs a = g;
+    if (PAIR && tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)(g.N / NT) * (g.K / 8) * 2 * NT, 1, 8, Cfg::NTL, 1, false))
+        return -1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((g.Rpad / TC_M) * (g.N / NT));
+    cfg.blockDim = dim3(TC3_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = PAIR ? 2 : 1;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? 0 : -1;
 }
 template <int L>
 int launch_tc_layer_l(int mode, int pro, const TcGemmArgs& g, cudaStream_t st) {
     constexpr int NT = tc_nt(Streams<L>::S);
     (void)mode;
     (void)pro;
-    return launch_tc2_bwd_t<L, NT>(g, st);
+    // the pair variant is bit-identical but not faster (N=128 MMAs are tensor-pipe
+    // bound, not smem bound: tools/trace_bwd.cu), so it is opt-in
+    static const bool pair = getenv("PNX_BWD_PAIR") != nullptr;
+    if (pair && NT == 128 && g.Rpad % 256 == 0) return launch_tc2_bwd_t<L, NT, true>(g, st);
+    return launch_tc2_bwd_t<L, NT, false>(g, st);
 }
 int launch_tc_layer(int L, int mode, int pro, const TcGemmArgs& g, cudaStream_t st) {
     switch (L) {

@@ -80,6 +80,12 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void sts32(uint32_t addr, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -1040,10 +1046,14 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
     }
 }
 
-template <int S, int NT>
+// PAIR: a 2-CTA cluster covers 256 rows of one n-tile with cta_group::2 MMAs
+// (M = 256); each CTA stages its own 128 rows of every stream and half of the
+// n-tile's weight rows (2-D tensor TMA completing on the leader's barrier).
+template <int S, int NT, bool PAIR = false>
 struct Tc2BwdCfg {
     static constexpr int A_BYTES = 2 * S * TC_TILE_BYTES;
-    static constexpr int B_T = NT * 32;
+    static constexpr int NTL = PAIR ? NT / 2 : NT;  // weight rows staged by this CTA
+    static constexpr int B_T = NTL * 32;
     static constexpr int STAGE = A_BYTES + 2 * B_T;
     static constexpr int NST = (TC_SMEM - 1024) / STAGE > 8 ? 8 : (TC_SMEM - 1024) / STAGE;
     // the epilogue reuses the (then idle) stage ring as its staging buffer
@@ -1052,11 +1062,11 @@ struct Tc2BwdCfg {
     static_assert(SMEM <= 227 * 1024, "bwd shared memory");
 };
 
-template <int L, int NT>
-__global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
+template <int L, int NT, bool PAIR>
+__global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constant__ TcGemmArgs g) {
     using St = Streams<L>;
     constexpr int S = St::S;
-    using Cfg = Tc2BwdCfg<S, NT>;
+    using Cfg = Tc2BwdCfg<S, NT, PAIR>;
     constexpr int NST = Cfg::NST;
     constexpr int D = 2;
     extern __shared__ uint8_t smem_raw[];
@@ -1066,25 +1076,32 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ntiles = g.N / NT;
-    const int rt = blockIdx.x / ntiles, nt = blockIdx.x % ntiles;
-    const int r0 = rt * TC_M, n0 = nt * NT;
+    const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0;
+    const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // (row tile, n tile) of this CTA / pair
+    const int rt = cid / ntiles, nt = cid % ntiles;
+    const int r0 = PAIR ? rt * 256 + (int)rank * 128 : rt * TC_M, n0 = nt * NT;
     const int nkb = g.K / 8;
     const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * g.N;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
-            tc::mbar_init(&full[i], 9);
+            tc::mbar_init(&full[i], PAIR ? 17 : 9);  // producer warps (both CTAs) + expect_tx
             tc::mbar_init(&empty[i], 1);
         }
         tc::mbar_init(&tfull, 1);
         tc::fence_barrier_init();
     }
-    if (warp == 8) tc::tmem_alloc<512>(&tmem_base);
+    if (warp == 8) {
+        if constexpr (PAIR) tc::tmem_alloc_pair<512>(&tmem_base);
+        else tc::tmem_alloc<512>(&tmem_base);
+    }
     tc::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) tc::cluster_sync();
+    else __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
     const uint32_t sbase = tc::smem_u32(smem);
-    const float* bimg = g.img + (int64_t)nt * nkb * (2 * Cfg::B_T / 4);
+    const float* bimg = g.img + (int64_t)nt * nkb * (2 * NT * 8);
+    const uint32_t full0 = PAIR ? tc::mapa(tc::smem_u32(&full[0]), 0) : 0u;
 
     if (warp < 8) {
         const int prow = tid >> 1, pc = tid & 1;
@@ -1111,8 +1128,17 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
                     for (int s2 = 0; s2 < S; ++s2) ring[slot][s2] = ldg4(asrc + s2 * RK + (it + D) * 8);
                 tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
                 if (tid == 0) {
-                    tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
-                    tc::bulk_g2s(stage + Cfg::A_BYTES, bimg + (int64_t)it * (2 * Cfg::B_T / 4), 2 * Cfg::B_T, &full[st]);
+                    if constexpr (PAIR) {
+                        // image rows (8 fp32 each) of k-step it: [hi: NT rows][lo: NT rows]
+                        const int rowb = (nt * nkb + it) * 2 * NT + (int)rank * Cfg::NTL;
+                        if (rank == 0) tc::mbar_arrive_expect_tx(&full[st], 2 * 2 * Cfg::B_T);
+                        tc::tma_load_2d_pair(stage + Cfg::A_BYTES, &g.tmB, 0, rowb, full0 + st * 8);
+                        tc::tma_load_2d_pair(stage + Cfg::A_BYTES + Cfg::B_T, &g.tmB, 0, rowb + NT, full0 + st * 8);
+                    } else {
+                        tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
+                        tc::bulk_g2s(stage + Cfg::A_BYTES, bimg + (int64_t)it * (2 * Cfg::B_T / 4), 2 * Cfg::B_T,
+                                     &full[st]);
+                    }
                 }
 #pragma unroll
                 for (int s2 = 0; s2 < S; ++s2) {
@@ -1121,12 +1147,15 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
                 }
                 tc::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&full[st]);
+                if (lane == 0) {
+                    if constexpr (PAIR) tc::mbar_arrive_cluster(full0 + st * 8);
+                    else tc::mbar_arrive(&full[st]);
+                }
             }
         }
     } else if (warp == 8) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NT, 0, 0);
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NT, 0, 0);
             for (int it = 0; it < nkb; ++it) {
                 const int st = it % NST;
                 const uint32_t stage = sbase + st * Cfg::STAGE;
@@ -1145,13 +1174,21 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
                     const uint32_t ah = stage + (2 * s2) * TC_TILE_BYTES;
                     const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(ah + TC_TILE_BYTES, 16, 256, 6);
                     const uint32_t d = tmem + (uint32_t)(s2 * NT);
-                    tc::mma_tf32(d, adh, bh, idesc, it > 0 ? 1u : 0u);
-                    tc::mma_tf32(d, adh, bl, idesc, 1u);
-                    tc::mma_tf32(d, adl, bh, idesc, 1u);
+                    if constexpr (PAIR) {
+                        tc::mma_tf32_pair(d, adh, bh, idesc, it > 0 ? 1u : 0u);
+                        tc::mma_tf32_pair(d, adh, bl, idesc, 1u);
+                        tc::mma_tf32_pair(d, adl, bh, idesc, 1u);
+                    } else {
+                        tc::mma_tf32(d, adh, bh, idesc, it > 0 ? 1u : 0u);
+                        tc::mma_tf32(d, adh, bl, idesc, 1u);
+                        tc::mma_tf32(d, adl, bh, idesc, 1u);
+                    }
                 }
-                tc::mma_commit(&empty[st]);
+                if constexpr (PAIR) tc::mma_commit_pair(&empty[st], 3);
+                else tc::mma_commit(&empty[st]);
             }
-            tc::mma_commit(&tfull);
+            if constexpr (PAIR) tc::mma_commit_pair(&tfull, 3);
+            else tc::mma_commit(&tfull);
         }
         __syncwarp();
     } else {
@@ -1170,15 +1207,15 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
 #pragma unroll 1
         for (int cc = 0; cc < NT / 2; cc += 32) {
             const int c0 = half * (NT / 2) + cc;
+            // all S streams' lines in flight at once (cp.async: no register staging)
 #pragma unroll
             for (int s2 = 0; s2 < S; ++s2) {
                 const float* src = g.Zlow + s2 * RN + rbase + c0;
-                float4 v[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = ldg4(src + (int64_t)(4 * k + lr) * g.N + lc);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) sts128(buf + ((s2 * 32 + 4 * k + lr) * ROWF + lc) * 4, v[k]);
+                for (int k = 0; k < 8; ++k)
+                    cp_async16(buf + ((s2 * 32 + 4 * k + lr) * ROWF + lc) * 4, src + (int64_t)(4 * k + lr) * g.N + lc);
             }
+            cp_async_wait_all();
             __syncwarp();
 #pragma unroll 1
             for (int c = 0; c < 32; c += 8) {
@@ -1231,8 +1268,12 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(TcGemmArgs g) {
         if (warp == 9 && lane == 0) TC_ACC(3);
     }
     tc::tc_fence_before();
-    __syncthreads();
-    if (warp == 8) tc::tmem_dealloc<512>(tmem);
+    if constexpr (PAIR) tc::cluster_sync();
+    else __syncthreads();
+    if (warp == 8) {
+        if constexpr (PAIR) tc::tmem_dealloc_pair<512>(tmem);
+        else tc::tmem_dealloc<512>(tmem);
+    }
 }
 
 }  // namespace pnx

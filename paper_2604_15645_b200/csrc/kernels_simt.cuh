@@ -330,6 +330,93 @@ __global__ void __launch_bounds__(256) k_layer0_wgrad(InputArgs a, const float* 
     }
 }
 
+// Layer-0 weight gradient, streaming version (H = 32*NC):
+//   dW0[k][n] = sum_rows sum_s E[s][row][k] Zb0[s][row][n],  db0[n] = sum_rows Zb0[0][row][n]
+// Each warp owns a contiguous row chunk; lane owns NC consecutive columns, so a
+// row of a stream is one fully coalesced warp load. The FP64 input-feature jets
+// of 32 rows are computed once (lane = row) and broadcast by shuffles. FP32
+// accumulation per warp chunk, then the block folds its 8 warps into FP64 in
+// fixed order and adds one partial slice (same layout as k_layer0_wgrad).
+template <int L, int K0C, int NC>
+__global__ void __launch_bounds__(256) k_layer0_wgrad_stream(InputArgs a, const float* __restrict__ Zb0, int H,
+                                                            int rows_per_warp, double* __restrict__ part) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+    __shared__ double red[(K0C + 1) * 32 * NC];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int gw = blockIdx.x * 8 + wid;
+    const int rbeg = gw * rows_per_warp, rend = min(a.nrows, rbeg + rows_per_warp);
+    const int K0 = a.E;
+    const int64_t RH = (int64_t)a.Rpad * H;
+    float acc[K0C + 1][NC];
+#pragma unroll
+    for (int k = 0; k <= K0C; ++k)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[k][c] = 0.0f;
+    for (int g0 = rbeg; g0 < rend; g0 += 32) {
+        float e[S][K0C];
+        {
+            double ed[S][2 * kMaxAxes];
+            const int r = g0 + lane;
+            if (r < rend) embed_row<L>(a, a.row0 + r, ed);
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int k = 0; k < K0C; ++k) e[s][k] = (r < rend && k < K0) ? (float)ed[s][k] : 0.0f;
+        }
+        const int nr = min(32, rend - g0);
+#pragma unroll 2
+        for (int rr = 0; rr < nr; ++rr) {
+            const float* zp = Zb0 + (int64_t)(g0 + rr) * H + lane * NC;
+            float4 z[S][NC / 4];
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int c4 = 0; c4 < NC / 4; ++c4) z[s][c4] = __ldg(reinterpret_cast<const float4*>(zp + s * RH) + c4);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+#pragma unroll
+                for (int k = 0; k < K0C; ++k) {
+                    const float ek = __shfl_sync(0xffffffffu, e[s][k], rr);
+#pragma unroll
+                    for (int c4 = 0; c4 < NC / 4; ++c4) {
+                        acc[k][4 * c4 + 0] = fmaf(ek, z[s][c4].x, acc[k][4 * c4 + 0]);
+                        acc[k][4 * c4 + 1] = fmaf(ek, z[s][c4].y, acc[k][4 * c4 + 1]);
+                        acc[k][4 * c4 + 2] = fmaf(ek, z[s][c4].z, acc[k][4 * c4 + 2]);
+                        acc[k][4 * c4 + 3] = fmaf(ek, z[s][c4].w, acc[k][4 * c4 + 3]);
+                    }
+                }
+                if (s == 0)
+#pragma unroll
+                    for (int c4 = 0; c4 < NC / 4; ++c4) {
+                        acc[K0C][4 * c4 + 0] += z[0][c4].x;
+                        acc[K0C][4 * c4 + 1] += z[0][c4].y;
+                        acc[K0C][4 * c4 + 2] += z[0][c4].z;
+                        acc[K0C][4 * c4 + 3] += z[0][c4].w;
+                    }
+            }
+        }
+    }
+    // fold the block's warps in fixed order (warp 0 first) into FP64
+    for (int w = 0; w < 8; ++w) {
+        __syncthreads();
+        if (wid == w)
+#pragma unroll
+            for (int k = 0; k <= K0C; ++k)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    double& d = red[k * 32 * NC + lane * NC + c];
+                    d = (w == 0 ? 0.0 : d) + (double)acc[k][c];
+                }
+    }
+    __syncthreads();
+    double* dst = part + (int64_t)blockIdx.x * ((int64_t)K0 * H + H);
+    for (int i = threadIdx.x; i < (K0 + 1) * H; i += blockDim.x) {
+        const int k = i / H, nn = i % H;
+        dst[(int64_t)k * H + nn] += red[(k < K0 ? k : K0C) * H + nn];
+    }
+}
+
 // Trainable-period gradient: given Hbar_in [S][Rpad][K0] (adjoint of the input
 // features), back through RFF (B frozen) and the embedding to each trainable
 // period: d phi/dP = -phi/P, d kappa/dP = -kappa/P.

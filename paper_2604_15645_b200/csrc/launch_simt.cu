@@ -1,3 +1,4 @@
+#include <cstdlib>
 // launch_simt.cu -- dispatch of the FP32 CUDA-core (FFMA) kernels.
 #include <algorithm>
 
@@ -141,7 +142,33 @@ void launch_layer0_fwd(int L, int act, const InputArgs& a, const float* W0, cons
         case LAY_NS: launch_layer0_fwd_l<LAY_NS>(act, a, W0, b0, Z0, H, st); break;
     }
 }
+template <int L, int NC>
+static bool launch_l0w_stream_nc(const InputArgs& a, const float* Zb0, int H, double* part, int grid, cudaStream_t st) {
+    const int warps = grid * 8;
+    const int rpw = (int)((((int64_t)a.nrows + warps - 1) / warps + 31) / 32 * 32);
+    if (a.E <= 3) k_layer0_wgrad_stream<L, 3, NC><<<grid, 256, 0, st>>>(a, Zb0, H, rpw, part);
+    else if (a.E <= 4) k_layer0_wgrad_stream<L, 4, NC><<<grid, 256, 0, st>>>(a, Zb0, H, rpw, part);
+    else if (a.E <= 6) k_layer0_wgrad_stream<L, 6, NC><<<grid, 256, 0, st>>>(a, Zb0, H, rpw, part);
+    else if (a.E <= 8) k_layer0_wgrad_stream<L, 8, NC><<<grid, 256, 0, st>>>(a, Zb0, H, rpw, part);
+    else return false;
+    return true;
+}
+template <int L>
+static bool launch_l0w_stream(const InputArgs& a, const float* Zb0, int H, double* part, int grid, cudaStream_t st) {
+    if (getenv("PNX_L0W_OLD")) return false;
+    if (H == 256) return launch_l0w_stream_nc<L, 8>(a, Zb0, H, part, grid, st);
+    if (H == 128) return launch_l0w_stream_nc<L, 4>(a, Zb0, H, part, grid, st);
+    return false;
+}
 void launch_layer0_wgrad(int L, const InputArgs& a, const float* Zb0, int H, double* part, int grid, cudaStream_t st) {
+    bool done = false;
+    switch (L) {
+        case LAY_XT: done = launch_l0w_stream<LAY_XT>(a, Zb0, H, part, grid, st); break;
+        case LAY_AC: done = launch_l0w_stream<LAY_AC>(a, Zb0, H, part, grid, st); break;
+        case LAY_MX: done = launch_l0w_stream<LAY_MX>(a, Zb0, H, part, grid, st); break;
+        case LAY_NS: done = launch_l0w_stream<LAY_NS>(a, Zb0, H, part, grid, st); break;
+    }
+    if (done) return;
     switch (L) {
         case LAY_XT: k_layer0_wgrad<LAY_XT><<<grid, 256, 0, st>>>(a, Zb0, H, part); break;
         case LAY_AC: k_layer0_wgrad<LAY_AC><<<grid, 256, 0, st>>>(a, Zb0, H, part); break;

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int r0 = blockIdx.x * TC_M;
-    const int nkb = g.K / 8, ngrp = g.K / 32, nit = S * nkb;
+    const int nkb = g.K / 8, ngrp = g.K / 32;
     const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * NF;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {

@@ -144,6 +144,18 @@ std::array<double, 3> worker_losses(const Model& model, const TrainingProblem& p
     return {pde, ic, bc};
 }
 
+// poynting_penalty (losses.cpp:187-223) value as run_worker_epoch adds it
+// (trainer.cpp:240-247): time samples = linspace over the last axis.
+double worker_penalty(const Model& model, const TrainingProblem& prob, const TrainConfig& cfg) {
+    Graph g;
+    Model::Binding binding = model.bind(g);
+    FieldFn f = model_fields(model, binding);
+    auto ts = linspace(prob.domain.bounds.back()[0], prob.domain.bounds.back()[1], cfg.poynting.time_samples);
+    Value pen = poynting_penalty(g, f, ts, prob.domain.bounds[0], prob.domain.bounds[1], cfg.poynting.grid,
+                                 prob.residual.epsilon, prob.residual.mu);
+    return g.value(pen).item();
+}
+
 std::vector<double> residual_values(const Model& model, const TrainingProblem& prob,
                                     const Points& pts) {
     Graph g;
@@ -191,6 +203,18 @@ int main(int argc, char** argv) {
         cfg.seed = job.value("colloc_seed", std::uint64_t{0});
         cfg.collocation = make_colloc(job.at("collocation"));
         cfg.workers = job.value("workers", 1);
+        if (job.contains("poynting")) {  // PoyntingConfig (trainer.hpp:57-61)
+            const json& pj = job.at("poynting");
+            cfg.poynting.weight = pj.value("weight", 0.0);
+            cfg.poynting.grid = pj.value("grid", std::size_t{32});
+            cfg.poynting.time_samples = pj.value("time_samples", std::size_t{4});
+        }
+        if (job.contains("causality")) {  // CausalityConfig (trainer.hpp:51-55)
+            const json& cj = job.at("causality");
+            cfg.causality.enabled = cj.value("enabled", true);
+            cfg.causality.segments = cj.value("segments", 10);
+            cfg.causality.epsilon = cj.value("epsilon", 1.0);
+        }
 
         json meta;
         json pnames = json::array();
@@ -232,6 +256,8 @@ int main(int argc, char** argv) {
                 wl.push_back({{"pde", l[0]}, {"ic", l[1]}, {"bc", l[2]}, {"from", from}, {"to", to}});
             }
             meta["worker_losses"] = wl;
+            if (cfg.poynting.weight > 0.0 && prob.residual.id == PdeId::maxwell_te)
+                meta["penalty"] = worker_penalty(model, prob, cfg);
             auto t0 = std::chrono::steady_clock::now();
             std::vector<Tensor> grads = data_parallel_gradient(model, prob, cfg, W);
             meta["grad_seconds"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -248,7 +274,7 @@ int main(int argc, char** argv) {
             cfg.balancing.enabled = t.value("balancing", false);
             cfg.balancing.update_period = t.value("update_period", 100);
             cfg.balancing.alpha = t.value("alpha", 0.9);
-            cfg.poynting.weight = t.value("poynting_weight", 0.0);
+            cfg.poynting.weight = t.value("poynting_weight", cfg.poynting.weight);
             cfg.save_every = 0;
             json hashes = json::array();
             cfg.on_sync = [&hashes](long epoch, std::span<const std::uint64_t> hs) {

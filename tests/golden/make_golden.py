@@ -79,6 +79,12 @@ CASES = {
                             model={"in_dim": 2, "hidden_dim": 16, "depth": 3, "out_dim": 1, "activation": "tanh"},
                             collocation={"mode": "uniform", "dims": [9, 7], "n_ic": 10, "n_bc": 6},
                             workers=[1]),
+    # Maxwell with the Poynting energy penalty (losses.cpp:187-223, trainer.cpp:240-247)
+    "maxwell_poynting": dict(MAXWELL, bc="hard",
+                             model={"in_dim": 3, "hidden_dim": 16, "depth": 2, "out_dim": 3, "activation": "tanh"},
+                             collocation={"mode": "uniform", "dims": [5, 5, 4], "n_ic": 16},
+                             poynting={"weight": 0.7, "grid": 5, "time_samples": 3},
+                             workers=[1, 2]),
 }
 
 TRAJ = {
@@ -91,6 +97,28 @@ TRAJ = {
                          model={"in_dim": 3, "hidden_dim": 16, "depth": 2, "out_dim": 3, "activation": "tanh"},
                          collocation={"mode": "uniform", "dims": [5, 5, 4], "n_ic": 16},
                          workers=1, train={"epochs": 20, "lr": 5e-3, "gamma": 1.0, "balancing": False}),
+    # temporal causality weights (trainer.cpp:209-220, losses.cpp:163-185), W=2
+    "traj_burgers_causality": dict(BURGERS, bc="dirichlet_zero",
+                                   model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1,
+                                          "activation": "tanh"},
+                                   collocation={"mode": "uniform", "dims": [12, 10], "n_ic": 16, "n_bc": 8},
+                                   causality={"enabled": True, "segments": 4, "epsilon": 2.0},
+                                   workers=2, train={"epochs": 12, "lr": 1e-2, "gamma": 1.0, "balancing": False}),
+    # loss balancing: per-term gradients every update_period epochs (trainer.cpp:462-506)
+    "traj_burgers_balancing": dict(BURGERS, bc="dirichlet_zero",
+                                   model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1,
+                                          "activation": "tanh"},
+                                   collocation={"mode": "uniform", "dims": [12, 10], "n_ic": 16, "n_bc": 8},
+                                   workers=2, train={"epochs": 12, "lr": 1e-2, "gamma": 1.0, "balancing": True,
+                                                     "update_period": 3, "alpha": 0.9}),
+    # the full Maxwell objective: causality + Poynting + two-term balancing (hard BC)
+    "traj_maxwell_full": dict(MAXWELL, bc="hard",
+                              model={"in_dim": 3, "hidden_dim": 16, "depth": 2, "out_dim": 3, "activation": "tanh"},
+                              collocation={"mode": "uniform", "dims": [5, 5, 4], "n_ic": 16},
+                              causality={"enabled": True, "segments": 3, "epsilon": 1.0},
+                              poynting={"weight": 0.5, "grid": 4, "time_samples": 3},
+                              workers=2, train={"epochs": 8, "lr": 5e-3, "gamma": 1.0, "balancing": True,
+                                                "update_period": 2, "alpha": 0.9}),
 }
 
 
@@ -141,6 +169,8 @@ def make_case(name, case):
         arrays[f"grad_w{w}"] = grads[w]
     case_meta = {"case": base, "workers": case["workers"], "worker_losses": {str(w): losses[w] for w in losses},
                  "params": param_meta}
+    if "penalty" in meta:
+        case_meta["penalty"] = meta["penalty"]
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), meta=json.dumps(case_meta), **arrays)
 
 
@@ -162,10 +192,15 @@ def make_traj(name, case):
 def main():
     if not os.path.exists(DRIVER):
         sys.exit(f"{DRIVER} missing: run `make -C oracle` (needs /root/reference)")
+    only = set(sys.argv[1:])  # optional: names to (re)generate
     for n, c in CASES.items():
+        if only and n not in only:
+            continue
         make_case(n, c)
         print("wrote", n)
     for n, c in TRAJ.items():
+        if only and n not in only:
+            continue
         make_traj(n, c)
         print("wrote", n)
 

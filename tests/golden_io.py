@@ -47,8 +47,21 @@ def load(name: str) -> dict:
     elif bc == "soft_periodic":
         col.bc_a, col.bc_b = z["bc_a"], z["bc_b"]
     rffB = z["rffB"] if spec.rff else None
+    dom = case["domain"]
+    causality = poynting = balancing = None
+    if case.get("causality", {}).get("enabled", False):
+        causality = po.Causality(case["causality"].get("segments", 10), case["causality"].get("epsilon", 1.0),
+                                 dom[-1][0], dom[-1][1])
+    if case.get("poynting", {}).get("weight", 0.0) > 0.0:
+        pj = case["poynting"]
+        poynting = po.Poynting(pj["weight"], pj.get("grid", 32), pj.get("time_samples", 4),
+                               tuple(dom[0]), tuple(dom[1]), tuple(dom[-1]))
+    t = case.get("train", {})
+    if t.get("balancing", False):
+        balancing = po.Balancing(True, t.get("alpha", 0.9), t.get("update_period", 100))
     out = {"meta": meta, "case": case, "spec": spec, "res": res, "bc": bc, "col": col,
-           "params": z["params"], "rffB": rffB}
+           "params": z["params"], "rffB": rffB, "causality": causality, "poynting": poynting,
+           "balancing": balancing}
     for k in z.files:
         if k not in out:
             out[k] = z[k]

@@ -14,12 +14,15 @@ from oracle import pinn_oracle as po
 def test_gradient_and_losses_match_reference(name):
     g = gi.load(name)
     for w in g["meta"]["workers"]:
-        grad, outs = po.data_parallel_gradient(g["spec"], g["params"], g["rffB"], g["res"], g["col"], g["bc"], w)
+        grad, outs = po.data_parallel_gradient(g["spec"], g["params"], g["rffB"], g["res"], g["col"], g["bc"], w,
+                                               poynting=g["poynting"])
         ref = g[f"grad_w{w}"]
         assert np.linalg.norm(grad - ref) <= 1e-12 * np.linalg.norm(ref)
         for o, r in zip(outs, g["meta"]["worker_losses"][str(w)]):
             for k in ("pde", "ic", "bc"):
                 assert abs(o[k] - r[k]) <= 1e-12 * abs(r[k]) + 1e-25
+        if g["poynting"] is not None:  # poynting_penalty value (losses.cpp:187-223)
+            assert abs(outs[0]["pen"] - g["meta"]["penalty"]) <= 1e-12 * abs(g["meta"]["penalty"])
 
 
 @pytest.mark.parametrize("name", gi.CASE_NAMES)
@@ -58,13 +61,14 @@ def test_param_layout_matches_reference(name):
 def test_adam_trajectory_matches_reference(name):
     g = gi.load(name)
     t = g["case"]["train"]
-    p, hist = po.train_fixed_lambda(g["spec"], g["params"], g["rffB"], g["res"], g["col"], g["bc"],
-                                    t["epochs"], lr=t["lr"], gamma=t["gamma"], workers=g["case"]["workers"])
+    p, hist = po.train(g["spec"], g["params"], g["rffB"], g["res"], g["col"], g["bc"], t["epochs"], lr=t["lr"],
+                       gamma=t["gamma"], workers=g["case"]["workers"], balancing=g["balancing"],
+                       causality=g["causality"], poynting=g["poynting"])
     m = g["metrics"]
-    for ep, (lp, li, lb) in enumerate(hist):
-        assert abs(lp - m[ep, 1]) <= 1e-10 * abs(m[ep, 1]) + 1e-30
-        assert abs(li - m[ep, 2]) <= 1e-10 * abs(m[ep, 2]) + 1e-30
-        assert abs(lb - m[ep, 3]) <= 1e-10 * abs(m[ep, 3]) + 1e-30
+    for ep, row in enumerate(hist):
+        # l_pde, l_ic, l_bc, lambda_pde, lambda_ic, lambda_bc (MetricsRecord, trainer.cpp:524-530)
+        for k in range(6):
+            assert abs(row[k] - m[ep, 1 + k]) <= 1e-10 * abs(m[ep, 1 + k]) + 1e-30
     np.testing.assert_allclose(p, g["final_params"], rtol=1e-7, atol=1e-9)
     # replica hashes from on_sync (trainer.cpp:540-544): all replicas equal, and
     # param_hash restated bit-exactly (FNV-1a of the reference's final params)
@@ -125,6 +129,30 @@ def test_swish_sine_periodic_rff_finite_differences():
     g = gi.load("maxwell_periodic_rff")
     idx = [0, 5, 40, g["params"].size - 1]  # includes the trainable period P2
     _fd_check(g["spec"], g["res"], g["params"], g["rffB"], g["col"], g["bc"], idx)
+
+
+def test_causality_weights_and_segments():
+    """losses.cpp:163-171 / trainer.cpp:156-177 on hand-checked values."""
+    om = po.causality_weights([0.5, 0.25, 1.0], 2.0)
+    np.testing.assert_allclose(om, [1.0, math.exp(-1.0), math.exp(-1.5)], rtol=1e-15)
+    pts = np.array([[0.0, 0.0], [0.0, 0.2499], [0.0, 0.25], [0.0, 0.999], [0.0, 1.0]])
+    np.testing.assert_array_equal(po.time_segment_index(pts, 0.0, 1.0, 4), [0, 0, 1, 3, 3])
+
+
+def test_poynting_penalty_finite_differences():
+    """d pen / d fields of poynting_terms against central differences."""
+    rng = np.random.default_rng(3)
+    pc = po.Poynting(1.0, 3, 4, (-1.0, 1.0), (-1.0, 1.0), (0.0, 1.0))
+    res = po.ResidualSpec(id="maxwell_te", epsilon=1.3, mu=0.7)
+    F = rng.normal(size=(4 * 9, 3))
+    pen, dF = po.poynting_terms(res, F, pc, 4.0 / 9)
+    h = 1e-6
+    for idx in [(0, 0), (5, 1), (20, 2), (35, 0)]:
+        Fp, Fm = F.copy(), F.copy()
+        Fp[idx] += h
+        Fm[idx] -= h
+        fd = (po.poynting_terms(res, Fp, pc, 4.0 / 9)[0] - po.poynting_terms(res, Fm, pc, 4.0 / 9)[0]) / (2 * h)
+        assert abs(fd - dF[idx]) <= 1e-6 * max(1.0, abs(fd))
 
 
 def test_spec_known_answers():

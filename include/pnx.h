@@ -101,6 +101,31 @@ int pnx_set_bc(pnx_ctx* ctx, const double* a, const double* b, const double* tar
 int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double* grad_out,
              double losses_out[3]);
 
+/* Per-term gradients of l_pde, l_ic, l_bc alone (run_worker_epoch with
+ * want_term_grads, trainer.cpp:256-260): three reverse passes with unit
+ * weights and the Poynting penalty excluded; grad_terms_out holds 3 x
+ * param_count doubles (pde | ic | bc). Used on loss-balancing epochs
+ * (trainer.cpp:462-506). */
+int pnx_step_terms(pnx_ctx* ctx, const double* params, double* grad_terms_out, double losses_out[3]);
+int pnx_step_terms_device(pnx_ctx* ctx, const float* d_params, float* d_grads, double* d_losses, void* stream);
+
+/* Temporal causality (CausalityConfig, trainer.hpp:51-55): this worker's
+ * interior points are bucketed by their last coordinate over [t_lo, t_hi]
+ * into `segments` (split_time_segments, trainer.cpp:156-177); pnx_step then
+ * minimises l_pde = (1/M) sum_i omega_i L_i with omega from the segment losses
+ * (causality_weights / weighted_pde_loss, losses.cpp:163-185; omega is a
+ * constant of the step). segments <= 0 disables (the default). */
+int pnx_set_causality(pnx_ctx* ctx, int32_t segments, double epsilon, double t_lo, double t_hi);
+
+/* Poynting energy penalty (PoyntingConfig, trainer.hpp:57-61; poynting_penalty,
+ * losses.cpp:187-223): maxwell_te only; weight 0 disables (the default).
+ * box = {x_lo, x_hi, y_lo, y_hi, t_lo, t_hi}; grid^2 midpoint nodes at each of
+ * time_samples = linspace(t_lo, t_hi) instants are evaluated on every worker
+ * (replicated like the IC set) and weight * penalty joins the total loss. */
+int pnx_set_poynting(pnx_ctx* ctx, double weight, int32_t grid, int32_t time_samples, const double box[6]);
+/* Penalty value (unweighted) of the last step; synchronizes the ctx stream. */
+int pnx_last_penalty(pnx_ctx* ctx, double* pen);
+
 /* Device-resident variant (no host copies): d_params/d_grad are float32 device
  * pointers of param_count entries, d_losses (may be NULL) receives 3 doubles;
  * work is enqueued on `stream` (a cudaStream_t, 0 = legacy default). The

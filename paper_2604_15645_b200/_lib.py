@@ -16,6 +16,7 @@ EXPORTS = [
     "pnx_set_points", "pnx_set_ic", "pnx_set_bc", "pnx_step", "pnx_step_device", "pnx_check",
     "pnx_adam_step_device", "pnx_set_engine", "pnx_set_chunk_rows", "pnx_last_launch_count",
     "pnx_capture_residuals", "pnx_copy_residuals", "pnx_profile", "pnx_profile_read",
+    "pnx_step_terms", "pnx_step_terms_device", "pnx_set_causality", "pnx_set_poynting", "pnx_last_penalty",
 ]
 
 
@@ -65,6 +66,11 @@ def load(path: str = LIB_PATH):
     lib.pnx_copy_residuals.argtypes = [vp, dp]
     lib.pnx_profile.argtypes = [vp, C.c_int]
     lib.pnx_profile_read.argtypes = [vp, dp, C.POINTER(i64), C.c_int]
+    lib.pnx_step_terms.argtypes = [vp, dp, dp, dp]
+    lib.pnx_step_terms_device.argtypes = [vp, vp, vp, vp, vp]
+    lib.pnx_set_causality.argtypes = [vp, i32, C.c_double, C.c_double, C.c_double]
+    lib.pnx_set_poynting.argtypes = [vp, C.c_double, i32, i32, dp]
+    lib.pnx_last_penalty.argtypes = [vp, dp]
     for name in EXPORTS:
         if name not in ("pnx_destroy", "pnx_last_error", "pnx_create_error"):
             getattr(lib, name).restype = C.c_int

@@ -769,7 +769,24 @@ struct HeadArgs {
     float* resid_out;    // optional [K][n_int] (interior residuals, diagnostics)
     int values_only;     // periodic prepass: write O[0] of bc rows to bc_vals
     float* vals_out;
+    int rbeg;            // first chunk row this launch visits
+    // stats pre-pass (stats = 1): no seeds; per-block FP64 sums for the two
+    // objective terms whose seeds need global reductions first
+    int stats;
+    // temporal causality (trainer.cpp:156-177, losses.cpp:163-185): interior rows
+    // bucketed by their last coordinate; seeds scaled per segment by seg_w
+    int seg_M;
+    double seg_tlo, seg_span;
+    const double* tcoord;  // last-axis coordinate of every global row
+    const float* seg_w;    // [M] 2 lambda_pde omega_i / (M n_i)
+    double* seg_part;      // [grid][M] sum of r^2 per segment (stats)
+    // Poynting penalty rows [poy0, poy1): poy_T samples of poy_n2 nodes each
+    int64_t poy0, poy1;
+    int poy_T, poy_n2;
+    const float* poy_g;    // [T][3] seed multipliers for (Ez, Hx, Hy)
+    double* poy_part;      // [grid][T][2] sum Ez^2, sum Hx^2 + Hy^2 (stats)
 };
+constexpr int kStatMax = 64;  // max causality segments / Poynting time samples
 
 template <int P, int ACT, int J>
 __global__ void __launch_bounds__(32 * kHeadWarps, 1) k_head(HeadArgs a) {
@@ -827,8 +844,14 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 1) k_head(HeadArgs a) {
         since_flush = 0;
     };
 
+    // stats pre-pass accumulators (lane 0 of each warp; fixed-order block fold)
+    __shared__ double sacc[kHeadWarps][3 * kStatMax];
+    if (a.stats) {
+        for (int i = lane; i < 3 * kStatMax; i += 32) sacc[wid][i] = 0.0;
+        __syncwarp();
+    }
     float z[S][J], zn[S][J];
-    int r = gw;
+    int r = a.rbeg + gw;
     if (r < a.nrows) load_row(r, z);
     for (; r < a.nrows; r += nw) {
         const int rn = r + nw;
@@ -863,7 +886,24 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 1) k_head(HeadArgs a) {
 #pragma unroll
         for (int f = 0; f < F; ++f) o[f] += a.b[f];
 
-        if (a.values_only) {
+        if (a.stats) {
+            if (lane == 0) {
+                if (a.seg_M > 0 && g >= a.int0 && g < a.int1) {
+                    float res[K];
+                    residual<P>(o, res, a.pc);
+                    double sq = 0.0;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) sq += (double)res[k] * (double)res[k];
+                    const double frac = (a.tcoord[g] - a.seg_tlo) / a.seg_span;
+                    const int sg = min(a.seg_M - 1, max(0, (int)(frac * a.seg_M)));
+                    sacc[wid][sg] += sq;
+                } else if (g >= a.poy0 && g < a.poy1) {
+                    const int j = (int)((g - a.poy0) / a.poy_n2);
+                    sacc[wid][kStatMax + 2 * j] += (double)o[0] * (double)o[0];
+                    sacc[wid][kStatMax + 2 * j + 1] += (double)o[1] * (double)o[1] + (double)o[2] * (double)o[2];
+                }
+            }
+        } else if (a.values_only) {
             if (lane == 0) {
                 int64_t slot = -1;
                 if (g >= a.bca0 && g < a.bca1) slot = g - a.bca0;
@@ -879,10 +919,15 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 1) k_head(HeadArgs a) {
                 float res[K], rb[K];
                 residual<P>(o, res, a.pc);
                 float sq = 0.0f;
+                float wr = a.w_pde;
+                if (a.seg_M > 0) {  // causality: per-segment weight (losses.cpp:173-185)
+                    const double frac = (a.tcoord[g] - a.seg_tlo) / a.seg_span;
+                    wr = a.seg_w[min(a.seg_M - 1, max(0, (int)(frac * a.seg_M)))];
+                }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     sq += res[k] * res[k];
-                    rb[k] = a.w_pde * res[k];
+                    rb[k] = wr * res[k];
                     if (lane == 0 && !isfinite(res[k])) atomicMin(&a.bad[k], (int)(g - a.int0));
                 }
                 if (a.resid_out && lane == 0) {
@@ -926,6 +971,11 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 1) k_head(HeadArgs a) {
                 const int64_t i = g - a.bcb0;
 #pragma unroll
                 for (int f = 0; f < F; ++f) ob[f] = -a.w_bc * (a.bc_vals[i * F + f] - o[f]);
+            } else if (g >= a.poy0 && g < a.poy1) {
+                // Poynting nodes: value-stream seeds weight * dpen/dE_j * dE_j/dfield
+                const int j = (int)((g - a.poy0) / a.poy_n2);
+#pragma unroll
+                for (int f = 0; f < F; ++f) ob[f] = (f < 3 ? a.poy_g[3 * j + f] : 0.0f) * o[f];
             }
             // reverse through the head: hbar = Obar W^T, dW_L += h^T Obar
 #pragma unroll
@@ -968,6 +1018,19 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 1) k_head(HeadArgs a) {
 #pragma unroll
                 for (int j = 0; j < J; ++j) z[s][j] = zn[s][j];
         }
+    }
+    if (a.stats) {  // fixed-order fold of the warps' sums, one partial per block
+        __syncthreads();
+        for (int i = threadIdx.x; i < 3 * kStatMax; i += blockDim.x) {
+            double v = 0.0;
+            for (int w = 0; w < kHeadWarps; ++w) v += sacc[w][i];
+            if (i < kStatMax) {
+                if (i < a.seg_M) a.seg_part[(int64_t)blockIdx.x * a.seg_M + i] = v;
+            } else if (i - kStatMax < 2 * a.poy_T) {
+                a.poy_part[(int64_t)blockIdx.x * 2 * a.poy_T + (i - kStatMax)] = v;
+            }
+        }
+        return;
     }
     if (a.values_only) return;
     flush();
@@ -1046,10 +1109,60 @@ static __global__ void k_write_layer_grad(const double* __restrict__ red, const 
     }
 }
 
+// Causality weights from the stats pass (losses.cpp:163-185): L_i = S_i / n_i
+// (0 for empty segments), omega_0 = 1, omega_i = exp(-eps sum_{j<i} L_j);
+// seeds 2 lambda omega_i / (M n_i); l_pde = (1/M) sum omega_i L_i.
+static __global__ void k_causality_weights(const double* __restrict__ seg_part, int nblk, int M,
+                                           const double* __restrict__ cnt, double eps, double lam,
+                                           float* __restrict__ seg_w, double* __restrict__ lpde) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double acc = 0.0, tot = 0.0;
+    for (int i = 0; i < M; ++i) {
+        double s = 0.0;
+        for (int b = 0; b < nblk; ++b) s += seg_part[(int64_t)b * M + i];
+        const double Li = cnt[i] > 0.0 ? s / cnt[i] : 0.0;
+        const double om = i == 0 ? 1.0 : exp(-eps * acc);
+        acc += Li;
+        tot += om * Li;
+        seg_w[i] = cnt[i] > 0.0 ? (float)(2.0 * lam * om / ((double)M * cnt[i])) : 0.0f;
+    }
+    *lpde = tot / (double)M;
+}
+
+// Poynting penalty from the stats pass (losses.cpp:187-223):
+// E_j = cell/2 (eps sum Ez^2 + mu sum (Hx^2 + Hy^2)), pen = mean_j (E_{j+1} - E_j)^2;
+// g[j] = weight * dpen/dE_j * cell * (eps, mu, mu) multiplies (Ez, Hx, Hy).
+static __global__ void k_poynting_weights(const double* __restrict__ poy_part, int nblk, int T, double cell,
+                                          double eps, double mu, double weight, float* __restrict__ g,
+                                          double* __restrict__ pen) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double E[kStatMax];
+    for (int j = 0; j < T; ++j) {
+        double se = 0.0, sh = 0.0;
+        for (int b = 0; b < nblk; ++b) {
+            se += poy_part[((int64_t)b * T + j) * 2];
+            sh += poy_part[((int64_t)b * T + j) * 2 + 1];
+        }
+        E[j] = 0.5 * cell * (eps * se + mu * sh);
+    }
+    double p = 0.0;
+    for (int j = 0; j + 1 < T; ++j) p += (E[j + 1] - E[j]) * (E[j + 1] - E[j]);
+    *pen = p / (double)(T - 1);
+    for (int j = 0; j < T; ++j) {
+        double dE = 0.0;
+        if (j > 0) dE += 2.0 * (E[j] - E[j - 1]) / (double)(T - 1);
+        if (j + 1 < T) dE -= 2.0 * (E[j + 1] - E[j]) / (double)(T - 1);
+        g[3 * j + 0] = (float)(weight * dE * cell * eps);
+        g[3 * j + 1] = (float)(weight * dE * cell * mu);
+        g[3 * j + 2] = (float)(weight * dE * cell * mu);
+    }
+}
+
 static __global__ void k_write_scalar_grads(const double* __restrict__ partP, int nblk, const int64_t* offs,
                                      int naxes, float scale, float* __restrict__ grad,
                                      const double* __restrict__ loss_part, int nloss_blk,
-                                     const double* inv_n, double* __restrict__ losses_out) {
+                                     const double* inv_n, double* __restrict__ losses_out,
+                                     const double* __restrict__ pde_override = nullptr) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         for (int ax = 0; ax < naxes; ++ax) {
             if (offs[ax] < 0) continue;
@@ -1063,6 +1176,7 @@ static __global__ void k_write_scalar_grads(const double* __restrict__ partP, in
                 for (int b = 0; b < nloss_blk; ++b) s += loss_part[b * 3 + t];
                 losses_out[t] = s * inv_n[t];
             }
+            if (pde_override) losses_out[0] = *pde_override;
         }
     }
 }

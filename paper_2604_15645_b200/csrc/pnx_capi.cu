@@ -54,12 +54,13 @@ struct pnx_ctx {
     // problem
     int pde = 0, bc = 0, layout = 0, S = 1, Kres = 1;
     PdeConst pc{};
+    double res_eps = 1.0, res_mu = 1.0;  // ResidualSpec epsilon / mu in FP64
     // params
     int64_t P = 0;
     LayerTab tab{};
     int64_t wsize = 0, bsize = 0;
 
-    // collocation (global rows: [bc_a | bc_b | ic | interior])
+    // collocation (global rows: [bc_a | bc_b | ic | poynting | interior])
     int64_t n_bca = 0, n_bcb = 0, n_ic = 0, n_int = 0;
     std::vector<double> h_int, h_ic, h_bca, h_bcb;  // axis-major host copies
     std::vector<float> h_ic_t, h_bc_t;
@@ -93,7 +94,20 @@ struct pnx_ctx {
     float* d_resid = nullptr;
     int64_t resid_cap = 0;
     bool h_int_stale = false;  // interior coordinates newer on device than in h_int
+    int64_t int_off_prev = 0;  // first interior row of the uploaded layout
     bool capture_resid = false;
+    // objective terms whose seeds need a global reduction first (trainer.cpp:209-247)
+    int caus_M = 0;  // causality segments (0 = off)
+    double caus_eps = 1.0, caus_tlo = 0.0, caus_thi = 1.0;
+    double *d_caus_cnt = nullptr, *d_seg_part = nullptr, *d_caus_loss = nullptr;
+    float* d_seg_w = nullptr;
+    double poy_w = 0.0, poy_box[6] = {0, 0, 0, 0, 0, 0};
+    int poy_grid = 0, poy_T = 0;
+    int64_t n_poy = 0;  // Poynting quadrature rows (replicated, chunk 0)
+    std::vector<double> h_poy;
+    double *d_poy_part = nullptr, *d_pen = nullptr;
+    float* d_poy_g = nullptr;
+    bool no_penalty = false;  // per-term gradient passes exclude the penalty (trainer.cpp:256-260)
     TcWorkspace tc{};
     // kernel-class timing with CUDA events on the launching stream (bench roofline)
     bool prof = false;
@@ -191,17 +205,32 @@ int64_t bytes_per_row(const pnx_ctx* c) {
     return f * 4;
 }
 
+// Points per causality segment of this shard (split_time_segments, trainer.cpp:156-177).
+int causality_counts(pnx_ctx* ctx, const double* tcol, int64_t n) {
+    if (ctx->caus_M <= 0) return PNX_OK;
+    std::vector<double> cnt((size_t)ctx->caus_M, 0.0);
+    const double span = ctx->caus_thi - ctx->caus_tlo;
+    for (int64_t i = 0; i < n; ++i) {
+        const double frac = (tcol[i] - ctx->caus_tlo) / span;
+        const int sg = std::min(ctx->caus_M - 1, std::max(0, static_cast<int>(frac * ctx->caus_M)));
+        cnt[(size_t)sg] += 1.0;
+    }
+    CK(cudaMemcpy(ctx->d_caus_cnt, cnt.data(), cnt.size() * 8, cudaMemcpyHostToDevice));
+    return PNX_OK;
+}
+
 int upload_rows(pnx_ctx* ctx) {
     const int d = ctx->in_dim;
     if (ctx->h_int_stale && ctx->d_coords) {  // pull the fast-path interior back before re-layout
-        const int64_t off = ctx->n_bca + ctx->n_bcb + ctx->n_ic;
+        const int64_t off = ctx->int_off_prev;
         for (int a = 0; a < d; ++a)
             CK(cudaMemcpy(ctx->h_int.data() + a * ctx->n_int, ctx->d_coords + a * ctx->ld + off,
                           (size_t)ctx->n_int * 8, cudaMemcpyDeviceToHost));
         ctx->h_int_stale = false;
     }
-    const int64_t T = ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_int;
+    const int64_t T = ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_poy + ctx->n_int;
     ctx->ld = T;
+    ctx->int_off_prev = ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_poy;
     std::vector<double> all((size_t)(d * T));
     auto put = [&](const std::vector<double>& src, int64_t n, int64_t at) {
         for (int a = 0; a < d; ++a)
@@ -210,7 +239,9 @@ int upload_rows(pnx_ctx* ctx) {
     put(ctx->h_bca, ctx->n_bca, 0);
     put(ctx->h_bcb, ctx->n_bcb, ctx->n_bca);
     put(ctx->h_ic, ctx->n_ic, ctx->n_bca + ctx->n_bcb);
-    put(ctx->h_int, ctx->n_int, ctx->n_bca + ctx->n_bcb + ctx->n_ic);
+    put(ctx->h_poy, ctx->n_poy, ctx->n_bca + ctx->n_bcb + ctx->n_ic);
+    put(ctx->h_int, ctx->n_int, ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_poy);
+    if (int r = causality_counts(ctx, ctx->h_int.data() + (size_t)(d - 1) * ctx->n_int, ctx->n_int)) return r;
     if ((int64_t)all.size() > ctx->coords_cap) {
         if (int r = dalloc(ctx, &ctx->d_coords, all.size())) return r;
         ctx->coords_cap = (int64_t)all.size();
@@ -231,7 +262,7 @@ int upload_rows(pnx_ctx* ctx) {
     ctx->layout_T = T;
     ctx->layout_chunk_override = ctx->chunk_override;
     // chunking: all small rows in chunk 0
-    const int64_t small = ctx->n_bca + ctx->n_bcb + ctx->n_ic;
+    const int64_t small = ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_poy;
     int64_t ch = ctx->chunk_override;
     if (ch <= 0) {
         const int64_t budget = 48LL << 30;  // bytes of per-chunk activations
@@ -298,7 +329,11 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
 
     const int64_t T = ctx->ld;
     const int64_t bca0 = 0, bca1 = ctx->n_bca, bcb0 = bca1, bcb1 = bcb0 + ctx->n_bcb;
-    const int64_t ic0 = bcb1, ic1 = ic0 + ctx->n_ic, int0 = ic1, int1 = int0 + ctx->n_int;
+    const int64_t ic0 = bcb1, ic1 = ic0 + ctx->n_ic, poy0 = ic1, poy1 = poy0 + ctx->n_poy, int0 = poy1,
+                  int1 = int0 + ctx->n_int;
+    const bool caus = ctx->caus_M > 0;
+    const bool poy = ctx->n_poy > 0 && !ctx->no_penalty;
+    const bool multi = T > ctx->chunk_rows;
 
     InputArgs ia{};
     ia.coords = ctx->d_coords;
@@ -357,13 +392,12 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         }
     }
 
-    for (int64_t c0 = 0; c0 < T; c0 += ctx->chunk_rows) {
-        const int nrows = (int)std::min<int64_t>(ctx->chunk_rows, T - c0);
-        const int Rpad = (int)roundup(nrows, 256);
+    // forward of one chunk: input jets + hidden layers (Z_l of the chunk)
+    auto forward_chunk = [&](int64_t c0, int nrows, int Rpad) -> int {
+        const bool fuse0 = layer0_fused(ctx);
         ia.row0 = c0;
         ia.nrows = nrows;
         ia.Rpad = Rpad;
-        const bool fuse0 = layer0_fused(ctx);
         if (!fuse0) {
             prof_begin(ctx, PC_INPUT, st);
             launch_input(L, ia, st);
@@ -403,7 +437,9 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             }
             prof_end(ctx, st);
         }
-        // head
+        return PNX_OK;
+    };
+    auto head_args = [&](int64_t c0, int nrows, int Rpad) {
         HeadArgs h{};
         h.Z = ctx->d_Z[ctx->depth - 1];
         h.Zb = ctx->d_Zb[0];
@@ -428,6 +464,74 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         h.head_part = ctx->d_head_part;
         h.bad = ctx->d_bad;
         h.resid_out = ctx->capture_resid ? ctx->d_resid : nullptr;
+        h.tcoord = ctx->d_coords + (int64_t)(ctx->in_dim - 1) * T;
+        if (caus) {
+            h.seg_M = ctx->caus_M;
+            h.seg_tlo = ctx->caus_tlo;
+            h.seg_span = ctx->caus_thi - ctx->caus_tlo;
+            h.seg_w = ctx->d_seg_w;
+            h.seg_part = ctx->d_seg_part;
+        }
+        if (poy) {
+            h.poy0 = poy0;
+            h.poy1 = poy1;
+            h.poy_T = ctx->poy_T;
+            h.poy_n2 = ctx->poy_grid * ctx->poy_grid;
+            h.poy_g = ctx->d_poy_g;
+            h.poy_part = ctx->d_poy_part;
+        }
+        return h;
+    };
+    // stats pre-pass over chunk rows [0, rows_end) + the weight kernels
+    auto stats_chunk = [&](int64_t c0, int nrows, int Rpad, int rows_end) {
+        HeadArgs hs = head_args(c0, nrows, Rpad);
+        hs.stats = 1;
+        hs.nrows = rows_end;
+        launch_head(ctx->pde, act, hs, ctx->head_grid, st);
+    };
+    auto weights = [&]() -> int {
+        if (caus) {
+            k_causality_weights<<<1, 32, 0, st>>>(ctx->d_seg_part, ctx->head_grid, ctx->caus_M, ctx->d_caus_cnt,
+                                                  ctx->caus_eps, lam[0], ctx->d_seg_w, ctx->d_caus_loss);
+            CKL();
+        }
+        if (poy) {
+            const double cell = (ctx->poy_box[1] - ctx->poy_box[0]) / ctx->poy_grid *
+                                ((ctx->poy_box[3] - ctx->poy_box[2]) / ctx->poy_grid);
+            k_poynting_weights<<<1, 32, 0, st>>>(ctx->d_poy_part, ctx->head_grid, ctx->poy_T, cell, ctx->res_eps,
+                                                 ctx->res_mu, ctx->poy_w, ctx->d_poy_g, ctx->d_pen);
+            CKL();
+        }
+        return PNX_OK;
+    };
+    if (caus) CK(cudaMemsetAsync(ctx->d_seg_part, 0, (size_t)ctx->head_grid * ctx->caus_M * 8, st));
+    if (poy) CK(cudaMemsetAsync(ctx->d_poy_part, 0, (size_t)ctx->head_grid * 2 * ctx->poy_T * 8, st));
+    if (caus && multi) {  // segment losses need every chunk before any seed
+        for (int64_t c0 = 0; c0 < T; c0 += ctx->chunk_rows) {
+            const int nrows = (int)std::min<int64_t>(ctx->chunk_rows, T - c0);
+            const int Rpad = (int)roundup(nrows, 256);
+            if (int r = forward_chunk(c0, nrows, Rpad)) return r;
+            stats_chunk(c0, nrows, Rpad, nrows);
+            CKL();
+        }
+        if (int r = weights()) return r;
+    }
+
+    for (int64_t c0 = 0; c0 < T; c0 += ctx->chunk_rows) {
+        const int nrows = (int)std::min<int64_t>(ctx->chunk_rows, T - c0);
+        const int Rpad = (int)roundup(nrows, 256);
+        const bool fuse0 = layer0_fused(ctx);
+        if (int r = forward_chunk(c0, nrows, Rpad)) return r;
+        HeadArgs h = head_args(c0, nrows, Rpad);
+        if (!multi && (caus || poy)) {
+            stats_chunk(c0, nrows, Rpad, nrows);
+            CKL();
+            if (int r = weights()) return r;
+        } else if (multi && !caus && poy && c0 == 0) {
+            stats_chunk(c0, nrows, Rpad, (int)std::min<int64_t>(nrows, poy1));
+            CKL();
+            if (int r = weights()) return r;
+        }
         if (ctx->bc == PNX_BC_SOFT_PERIODIC && c0 == 0) {
             HeadArgs hv = h;
             hv.values_only = 1;
@@ -540,7 +644,8 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         k_write_scalar_grads<<<1, 32, 0, st>>>(ctx->d_partP, ctx->ibwd_grid,
                                                reinterpret_cast<const int64_t*>(ctx->d_losses + 8), ctx->in_dim,
                                                1.0f, d_grad, ctx->d_loss_part, ctx->head_grid, ctx->d_losses + 3,
-                                               d_losses ? d_losses : ctx->d_losses);
+                                               d_losses ? d_losses : ctx->d_losses,
+                                               caus ? ctx->d_caus_loss : nullptr);
         CKL();
     }
     return PNX_OK;
@@ -640,6 +745,8 @@ int pnx_create(const pnx_model_desc* m, const pnx_problem_desc* p, int device, p
     ctx->pc.c = (float)p->advection_c;
     ctx->pc.eps = (float)p->epsilon;
     ctx->pc.mu = (float)p->mu;
+    ctx->res_eps = p->epsilon;
+    ctx->res_mu = p->mu;
     ctx->pc.inv_re = p->reynolds > 0 ? (float)(1.0 / p->reynolds) : 0.0f;
     switch (layout) {
         case LAY_XT: ctx->S = 3; break;
@@ -743,6 +850,13 @@ void pnx_destroy(pnx_ctx* ctx) {
     cudaFree(ctx->d_partP);
     cudaFree(ctx->d_red);
     cudaFree(ctx->d_bc_vals);
+    cudaFree(ctx->d_caus_cnt);
+    cudaFree(ctx->d_seg_part);
+    cudaFree(ctx->d_caus_loss);
+    cudaFree(ctx->d_seg_w);
+    cudaFree(ctx->d_poy_part);
+    cudaFree(ctx->d_poy_g);
+    cudaFree(ctx->d_pen);
     cudaFree(ctx->d_bad);
     cudaFree(ctx->d_resid);
     tc_workspace_free(ctx->tc);
@@ -767,13 +881,13 @@ int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes
     if (!ctx->rows_dirty && n == ctx->n_int && ctx->d_coords) {
         // same row layout (e.g. resampled points, trainer.cpp:421-434): copy the
         // caller's axis-major buffer straight into the interior segment on device
-        const int64_t off = ctx->n_bca + ctx->n_bcb + ctx->n_ic;
+        const int64_t off = ctx->int_off_prev;
         for (int a = 0; a < n_axes; ++a)
             CK(cudaMemcpyAsync(ctx->d_coords + a * ctx->ld + off, coords + a * n, (size_t)n * 8,
                                cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         ctx->h_int_stale = true;
-        return PNX_OK;
+        return causality_counts(ctx, coords + (int64_t)(n_axes - 1) * n, n);
     }
     ctx->h_int.assign(coords, coords + n * n_axes);
     ctx->h_int_stale = false;
@@ -783,6 +897,88 @@ int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes
         if (int r = dalloc(ctx, &ctx->d_resid, (size_t)n * ctx->Kres)) return r;
         ctx->resid_cap = (int64_t)n * ctx->Kres;
     }
+    return PNX_OK;
+}
+
+int pnx_set_causality(pnx_ctx* ctx, int32_t segments, double epsilon, double t_lo, double t_hi) {
+    if (!ctx) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (segments <= 0) {
+        ctx->caus_M = 0;
+        return PNX_OK;
+    }
+    if (segments > kStatMax) return fail(ctx, PNX_ERR_ARG, "causality: at most 64 segments");
+    if (!(t_hi > t_lo)) return fail(ctx, PNX_ERR_ARG, "causality: empty time interval");
+    ctx->caus_M = segments;
+    ctx->caus_eps = epsilon;
+    ctx->caus_tlo = t_lo;
+    ctx->caus_thi = t_hi;
+    if (int r = dalloc(ctx, &ctx->d_caus_cnt, (size_t)segments)) return r;
+    if (int r = dalloc(ctx, &ctx->d_seg_part, (size_t)ctx->head_grid * segments)) return r;
+    if (int r = dalloc(ctx, &ctx->d_caus_loss, 1)) return r;
+    if (int r = dalloc(ctx, &ctx->d_seg_w, (size_t)segments)) return r;
+    CK(cudaMemset(ctx->d_caus_cnt, 0, (size_t)segments * 8));
+    if (ctx->n_int > 0) {  // counts of the current shard
+        if (ctx->h_int_stale || ctx->rows_dirty) {
+            ctx->rows_dirty = true;  // recounted by the next upload
+        } else {
+            if (int r = causality_counts(ctx, ctx->h_int.data() + (size_t)(ctx->in_dim - 1) * ctx->n_int, ctx->n_int))
+                return r;
+        }
+    }
+    return PNX_OK;
+}
+
+int pnx_set_poynting(pnx_ctx* ctx, double weight, int32_t grid, int32_t time_samples, const double box[6]) {
+    if (!ctx) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (weight == 0.0 || ctx->pde != PNX_PDE_MAXWELL_TE) {  // trainer.cpp:240: maxwell_te only
+        if (ctx->n_poy) ctx->rows_dirty = true;
+        ctx->poy_w = 0.0;
+        ctx->n_poy = 0;
+        ctx->h_poy.clear();
+        return PNX_OK;
+    }
+    if (time_samples < 2) return fail(ctx, PNX_ERR_ARG, "poynting_penalty: need at least 2 time samples");
+    if (time_samples > kStatMax || grid <= 0 || !box) return fail(ctx, PNX_ERR_ARG, "poynting_penalty: bad grid");
+    ctx->poy_w = weight;
+    if (grid == ctx->poy_grid && time_samples == ctx->poy_T && ctx->n_poy > 0 &&
+        std::equal(box, box + 6, ctx->poy_box))
+        return PNX_OK;  // same nodes: only the weight changed
+    ctx->poy_grid = grid;
+    ctx->poy_T = time_samples;
+    std::copy(box, box + 6, ctx->poy_box);
+    // midpoint nodes per time sample (losses.cpp:196-205), time = linspace (sampling.cpp:10-20)
+    const int64_t n2 = (int64_t)grid * grid, np = n2 * time_samples;
+    const double hx = (box[1] - box[0]) / grid, hy = (box[3] - box[2]) / grid;
+    const double ht = (box[5] - box[4]) / (double)(time_samples - 1);
+    ctx->h_poy.assign((size_t)(3 * np), 0.0);
+    for (int j = 0; j < time_samples; ++j) {
+        const double tv = j + 1 == time_samples ? box[5] : box[4] + (double)j * ht;
+        for (int64_t i = 0; i < grid; ++i)
+            for (int64_t k = 0; k < grid; ++k) {
+                const int64_t r = j * n2 + i * grid + k;
+                ctx->h_poy[(size_t)r] = box[0] + ((double)i + 0.5) * hx;
+                ctx->h_poy[(size_t)(np + r)] = box[2] + ((double)k + 0.5) * hy;
+                ctx->h_poy[(size_t)(2 * np + r)] = tv;
+            }
+    }
+    ctx->n_poy = np;
+    ctx->rows_dirty = true;
+    if (int r = dalloc(ctx, &ctx->d_poy_part, (size_t)ctx->head_grid * 2 * time_samples)) return r;
+    if (int r = dalloc(ctx, &ctx->d_poy_g, (size_t)3 * time_samples)) return r;
+    if (int r = dalloc(ctx, &ctx->d_pen, 1)) return r;
+    CK(cudaMemset(ctx->d_pen, 0, 8));
+    return PNX_OK;
+}
+
+int pnx_last_penalty(pnx_ctx* ctx, double* pen) {
+    if (!ctx || !pen) return PNX_ERR_ARG;
+    *pen = 0.0;
+    if (ctx->n_poy == 0 || !ctx->d_pen) return PNX_OK;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(pen, ctx->d_pen, 8, cudaMemcpyDeviceToHost));
     return PNX_OK;
 }
 
@@ -906,6 +1102,32 @@ int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double
     if (losses_out)
         for (int t = 0; t < 3; ++t) losses_out[t] = losses[t];
     return PNX_OK;
+}
+
+int pnx_step_terms(pnx_ctx* ctx, const double* params, double* grad_terms_out, double losses_out[3]) {
+    if (!ctx || !params || !grad_terms_out) return PNX_ERR_ARG;
+    ctx->no_penalty = true;
+    int r = PNX_OK;
+    for (int k = 0; k < 3 && r == PNX_OK; ++k) {
+        const double lam[3] = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0};
+        r = pnx_step(ctx, params, lam, grad_terms_out + (int64_t)k * ctx->P, k == 0 ? losses_out : nullptr);
+    }
+    ctx->no_penalty = false;
+    return r;
+}
+
+int pnx_step_terms_device(pnx_ctx* ctx, const float* d_params, float* d_grads, double* d_losses, void* stream) {
+    if (!ctx || !d_params || !d_grads) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    ctx->no_penalty = true;
+    int r = PNX_OK;
+    for (int k = 0; k < 3 && r == PNX_OK; ++k) {
+        const double lam[3] = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0};
+        r = run_step(ctx, d_params, lam, d_grads + (int64_t)k * ctx->P, k == 0 ? d_losses : nullptr,
+                     reinterpret_cast<cudaStream_t>(stream));
+    }
+    ctx->no_penalty = false;
+    return r;
 }
 
 int pnx_adam_step_device(pnx_ctx* ctx, float* d_params, const float* d_grad, float* d_m, float* d_v,

@@ -70,32 +70,98 @@ def replica_hashes(spec, params, world: int, group=None) -> Sequence[int]:
 
 
 class DataParallelTrainer:
-    """Synchronized Adam steps on one GPU per process (trainer.cpp:419-555 with
-    balancing off): device step -> NCCL all-reduce -> fused Adam(1/W)."""
+    """Synchronized Adam steps (trainer.cpp:419-555): per-worker device step ->
+    all-reduce -> fused Adam(1/W). `worker` is one Worker (one GPU per process)
+    or a list of local workers (several replicas in one process, e.g. to run a
+    W-worker reference case on one GPU); W = world x local workers.
+
+    Loss balancing (BalancingConfig, trainer.hpp:45-49): on epochs with
+    epoch % update_period == 0 the workers return the per-term gradients
+    (pnx_step_terms_device), the averaged term norms update the lambdas
+    (update_global_weights, losses.cpp:154-162; two-term rule without BC,
+    trainer.cpp:477-483) and the step uses lambda_k' g_k with the NEW weights --
+    or, with a Poynting penalty, the total gradient under the old weights
+    (trainer.cpp:491-498)."""
 
     def __init__(self, worker, params0: np.ndarray, world: int = 1, lr: float = 1e-3, gamma: float = 1.0,
-                 betas=(0.9, 0.999), eps: float = 1e-8, device=None, group=None):
+                 betas=(0.9, 0.999), eps: float = 1e-8, device=None, group=None, balancing=None,
+                 has_bc: bool = True, poynting: bool = False):
         import torch
         self.torch = torch
-        self.worker, self.world, self.group = worker, world, group
+        self.workers = list(worker) if isinstance(worker, (list, tuple)) else [worker]
+        self.worker = self.workers[0]
+        self.world, self.group = world, group
+        self.W = world * len(self.workers)
         self.lr, self.gamma, self.betas, self.eps = lr, gamma, betas, eps
-        dev = device or torch.device("cuda", worker.device)
+        self.balancing, self.has_bc, self.poynting = balancing, has_bc, poynting
+        self.lam = [1.0, 1.0, 1.0]
+        dev = device or torch.device("cuda", self.worker.device)
         self.params = torch.tensor(np.asarray(params0), dtype=torch.float32, device=dev)
         self.grad = torch.zeros_like(self.params)
+        self._wgrad = [torch.zeros_like(self.params) for _ in self.workers]
+        self._wloss = [torch.zeros(3, dtype=torch.float64, device=dev) for _ in self.workers]
+        self._g3 = None
         self.m = torch.zeros_like(self.params)
         self.v = torch.zeros_like(self.params)
         self.losses = torch.zeros(3, dtype=torch.float64, device=dev)
         self.t = 0
         self.epoch = 0
 
-    def step(self, lambdas=(1.0, 1.0, 1.0), stream=None):
-        st = stream if stream is not None else self.torch.cuda.current_stream(self.params.device).cuda_stream
-        self.worker.step_device(self.params, self.grad, lambdas, self.losses, stream=st)
+    def _total(self, lam, st):
+        for w, gb, lb in zip(self.workers, self._wgrad, self._wloss):
+            w.step_device(self.params, gb, lam, lb, stream=st)
+        self.grad.copy_(self._wgrad[0])
+        for gb in self._wgrad[1:]:
+            self.grad.add_(gb)
         allreduce_sum_(self.grad, self.world, self.group)
+
+    def _balance(self, st):
+        torch = self.torch
+        P = self.params.numel()
+        if self._g3 is None:
+            self._g3 = [torch.zeros(3 * P, dtype=torch.float32, device=self.params.device) for _ in self.workers]
+        for w, g3, lb in zip(self.workers, self._g3, self._wloss):
+            w.step_terms_device(self.params, g3, lb, stream=st)
+        gs = self._g3[0].clone()
+        for g3 in self._g3[1:]:
+            gs.add_(g3)
+        allreduce_sum_(gs, self.world, self.group)
+        terms = gs.view(3, P)
+        avg = terms.double() * (1.0 / self.W)
+        norms = [float(avg[k].norm()) for k in range(3)]
+        a, lam = self.balancing.alpha, self.lam
+        if self.has_bc:
+            tot = norms[0] + norms[1] + norms[2]
+            self.lam = [a * lam[k] + (1.0 - a) * (tot / max(norms[k], 1e-9)) for k in range(3)]
+        else:
+            tot = norms[0] + norms[1]
+            self.lam = [a * lam[0] + (1.0 - a) * (tot / max(norms[0], 1e-9)),
+                        a * lam[1] + (1.0 - a) * (tot / max(norms[1], 1e-9)), lam[2]]
+        if self.poynting:
+            self._total(lam, st)  # total gradient under the previous weights
+        else:
+            self.grad.copy_(terms[0]).mul_(self.lam[0]).add_(terms[1], alpha=self.lam[1])
+            if self.has_bc:
+                self.grad.add_(terms[2], alpha=self.lam[2])
+
+    def step(self, lambdas=None, stream=None):
+        st = stream if stream is not None else self.torch.cuda.current_stream(self.params.device).cuda_stream
+        b = self.balancing
+        if lambdas is not None:
+            self.lam = list(lambdas)
+        if b is not None and b.enabled and b.update_period > 0 and self.epoch % b.update_period == 0:
+            self._balance(st)
+        else:
+            self._total(tuple(self.lam), st)
+        self.losses.copy_(self._wloss[0])
+        for lb in self._wloss[1:]:
+            self.losses.add_(lb)
+        allreduce_sum_(self.losses, self.world, self.group)
+        self.losses.mul_(1.0 / self.W)  # MetricsRecord: mean over workers (trainer.cpp:517-526)
         self.t += 1
         lr = self.lr * self.gamma ** self.epoch  # ExponentialLr::at (optim.cpp:71-73)
         self.worker.adam_step_device(self.params, self.grad, self.m, self.v, self.t, lr, self.betas[0],
-                                     self.betas[1], self.eps, grad_scale=1.0 / self.world, stream=st)
+                                     self.betas[1], self.eps, grad_scale=1.0 / self.W, stream=st)
         self.epoch += 1
         return self.losses
 

@@ -265,6 +265,40 @@ class Worker:
                                            C.c_void_p(grad.data_ptr()),
                                            C.c_void_p(losses.data_ptr()) if losses is not None else None, st))
 
+    def step_terms(self, params: np.ndarray):
+        """Gradients of l_pde, l_ic, l_bc alone (trainer.cpp:256-260): ([3, P], losses)."""
+        p = np.ascontiguousarray(np.asarray(params, dtype=np.float64))
+        g = np.empty((3, self.n_params), dtype=np.float64)
+        losses = (C.c_double * 3)()
+        P = C.POINTER(C.c_double)
+        self._chk(self.lib.pnx_step_terms(self.ctx, p.ctypes.data_as(P), g.ctypes.data_as(P), losses))
+        return g, {"pde": losses[0], "ic": losses[1], "bc": losses[2]}
+
+    def step_terms_device(self, params, grads3, losses=None, stream=None):
+        """Device variant: grads3 is a float32 tensor of 3 x P (pde | ic | bc)."""
+        st = C.c_void_p(stream) if stream is not None else None
+        self._chk(self.lib.pnx_step_terms_device(self.ctx, C.c_void_p(params.data_ptr()),
+                                                 C.c_void_p(grads3.data_ptr()),
+                                                 C.c_void_p(losses.data_ptr()) if losses is not None else None, st))
+
+    def set_causality(self, cfg: Optional[CausalityConfig]):
+        if cfg is None:
+            self._chk(self.lib.pnx_set_causality(self.ctx, 0, 1.0, 0.0, 1.0))
+        else:
+            self._chk(self.lib.pnx_set_causality(self.ctx, int(cfg.segments), float(cfg.epsilon),
+                                                 float(cfg.t_lo), float(cfg.t_hi)))
+
+    def set_poynting(self, cfg: Optional[PoyntingConfig]):
+        box = (C.c_double * 6)(*(cfg.box if cfg is not None else (0.0,) * 6))
+        w = float(cfg.weight) if cfg is not None else 0.0
+        self._chk(self.lib.pnx_set_poynting(self.ctx, w, int(cfg.grid) if cfg else 0,
+                                            int(cfg.time_samples) if cfg else 0, box))
+
+    def penalty(self) -> float:
+        v = C.c_double()
+        self._chk(self.lib.pnx_last_penalty(self.ctx, C.byref(v)))
+        return v.value
+
     def check(self):
         self._chk(self.lib.pnx_check(self.ctx))
 
@@ -300,28 +334,62 @@ class Worker:
         return n.value
 
 
+@dataclass
+class CausalityConfig:
+    """trainer.hpp:51-55, with the time interval of the domain's last axis."""
+    segments: int = 10
+    epsilon: float = 1.0
+    t_lo: float = 0.0
+    t_hi: float = 1.0
+
+
+@dataclass
+class PoyntingConfig:
+    """trainer.hpp:57-61, with the (x, y, t) box it integrates over."""
+    weight: float = 0.0
+    grid: int = 32
+    time_samples: int = 4
+    box: Tuple[float, float, float, float, float, float] = (-1.0, 1.0, -1.0, 1.0, 0.0, 1.0)
+
+
+@dataclass
+class BalancingConfig:
+    """trainer.hpp:45-49."""
+    enabled: bool = True
+    alpha: float = 0.9
+    update_period: int = 100
+
+
 def make_worker(spec, res, bc, rff_B, interior, ic_points, ic_targets, bc_a=None, bc_b=None,
-                bc_targets=None, device=0, engine="auto") -> Worker:
+                bc_targets=None, device=0, engine="auto", causality: Optional[CausalityConfig] = None,
+                poynting: Optional[PoyntingConfig] = None) -> Worker:
     w = Worker(spec, res, bc, rff_B, device=device, engine=engine)
     w.set_points(interior)
     if ic_points is not None and len(ic_points):
         w.set_ic(ic_points, ic_targets)
     if bc != "hard":
         w.set_bc(bc_a, bc_b, bc_targets)
+    if causality is not None:
+        w.set_causality(causality)
+    if poynting is not None:
+        w.set_poynting(poynting)
     return w
 
 
 def data_parallel_gradient(spec, res, bc, params, rff_B, interior, ic_points, ic_targets, bc_a=None,
                            bc_b=None, bc_targets=None, workers: int = 1, lambdas=(1.0, 1.0, 1.0),
-                           device=0, engine="auto"):
+                           device=0, engine="auto", causality: Optional[CausalityConfig] = None,
+                           poynting: Optional[PoyntingConfig] = None):
     """trainer.cpp:649-678 on one device: shard, per-worker step, rank-ordered
-    average (sum x 1/W, trainer.cpp:264-281). Returns (grad, per-worker losses)."""
+    average (sum x 1/W, trainer.cpp:264-281). Returns (grad, per-worker losses);
+    with a Poynting penalty each loss dict also carries 'pen'."""
     outs = []
     g = None
     for a, b in shard_interior(len(interior), workers):
         w = make_worker(spec, res, bc, rff_B, interior[a:b], ic_points, ic_targets, bc_a, bc_b,
-                        bc_targets, device=device, engine=engine)
+                        bc_targets, device=device, engine=engine, causality=causality, poynting=poynting)
         gw, lw = w.step(params, lambdas)
+        lw["pen"] = w.penalty()
         outs.append(lw)
         g = gw.copy() if g is None else g + gw
     return g * (1.0 / workers), outs

@@ -43,6 +43,19 @@ def _col_args(g):
                 bc_a=col.bc_a, bc_b=col.bc_b, bc_targets=col.bc_targets)
 
 
+def _objective(g):
+    """Causality / Poynting options of a fixture as package configs."""
+    pk = _pkg()
+    c = p = None
+    if g["causality"] is not None:
+        o = g["causality"]
+        c = pk.CausalityConfig(o.segments, o.epsilon, o.t_lo, o.t_hi)
+    if g["poynting"] is not None:
+        o = g["poynting"]
+        p = pk.PoyntingConfig(o.weight, o.grid, o.time_samples, tuple(o.xb) + tuple(o.yb) + tuple(o.tb))
+    return c, p
+
+
 def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
@@ -53,15 +66,19 @@ def test_golden_gradients_and_losses(name, engine):
     pk = _pkg()
     g = gi.load(name)
     case = g["case"]
+    caus, poy = _objective(g)
     for w in g["meta"]["workers"]:
         grad, losses = pk.data_parallel_gradient(_spec(case), _res(case), g["bc"], g["params"], g["rffB"],
-                                                 workers=w, engine=engine, **_col_args(g))
+                                                 workers=w, engine=engine, causality=caus, poynting=poy,
+                                                 **_col_args(g))
         ref = g[f"grad_w{w}"]
         tol = GRAD_RTOL if engine == "ffma" else GRAD_RTOL_TC
         assert rel_l2(grad, ref) <= tol, (name, w, rel_l2(grad, ref))
         for o, r in zip(losses, g["meta"]["worker_losses"][str(w)]):
             for k in ("pde", "ic", "bc"):
                 assert abs(o[k] - r[k]) <= LOSS_RTOL * abs(r[k]) + 1e-12, (name, w, k, o[k], r[k])
+            if poy is not None:  # poynting_penalty value (losses.cpp:187-223)
+                assert abs(o["pen"] - g["meta"]["penalty"]) <= LOSS_RTOL * abs(g["meta"]["penalty"])
 
 
 @pytest.mark.parametrize("name", gi.CASE_NAMES)
@@ -171,38 +188,37 @@ def test_argument_errors_match_reference_text():
 
 @pytest.mark.parametrize("name", gi.TRAJ_NAMES)
 def test_adam_trajectory_on_device(name):
-    """N device-Adam steps (pnx_adam_step_device) track the reference train()
-    loss trajectory (trainer.cpp:419-555, balancing off). Tolerance: 1e-3
-    relative per step (FP32 drift grows with N)."""
+    """N synchronized device-Adam steps (dist.DataParallelTrainer with W local
+    workers on one GPU) track the reference train() trajectory (trainer.cpp:
+    419-555), including loss balancing, causality and the Poynting penalty
+    where the fixture enables them: losses and lambdas per epoch within 1e-3
+    relative (FP32 drift grows with N)."""
     import torch
     pk = _pkg()
+    from paper_2604_15645_b200.dist import DataParallelTrainer
     g = gi.load(name)
     case = g["case"]
     t = case["train"]
     W = case["workers"]
     a = _col_args(g)
-    shards = pk.shard_interior(len(a["interior"]), W)
+    caus, poy = _objective(g)
     workers = []
-    for lo, hi in shards:
+    for lo, hi in pk.shard_interior(len(a["interior"]), W):
         aa = dict(a, interior=a["interior"][lo:hi])
-        workers.append(pk.make_worker(_spec(case), _res(case), g["bc"], g["rffB"], **aa))
-    dev = torch.device("cuda:0")
-    p = torch.tensor(g["params"], dtype=torch.float32, device=dev)
-    m = torch.zeros_like(p)
-    v = torch.zeros_like(p)
-    grads = [torch.zeros_like(p) for _ in workers]
-    losses = [torch.zeros(3, dtype=torch.float64, device=dev) for _ in workers]
-    st = torch.cuda.current_stream().cuda_stream
+        workers.append(pk.make_worker(_spec(case), _res(case), g["bc"], g["rffB"], causality=caus, poynting=poy,
+                                      **aa))
+    bal = None
+    if g["balancing"] is not None:
+        bal = pk.BalancingConfig(True, g["balancing"].alpha, g["balancing"].update_period)
+    tr = DataParallelTrainer(workers, g["params"], world=1, lr=t["lr"], gamma=t["gamma"],
+                             device=torch.device("cuda:0"), balancing=bal, has_bc=g["bc"] != "hard",
+                             poynting=poy is not None)
     metrics = g["metrics"]
     for ep in range(t["epochs"]):
-        for w, gr, lo in zip(workers, grads, losses):
-            w.step_device(p, gr, losses=lo, stream=st)
-        gsum = torch.stack(grads).sum(0)
-        lr = t["lr"] * t["gamma"] ** ep
-        workers[0].adam_step_device(p, gsum, m, v, ep + 1, lr, grad_scale=1.0 / W, stream=st)
-        lm = torch.stack(losses).mean(0).cpu().numpy()
-        for k in range(3):
+        lm = tr.step().cpu().numpy()
+        row = list(lm) + list(tr.lam)
+        for k in range(6):  # l_pde, l_ic, l_bc, lambda_pde, lambda_ic, lambda_bc
             ref = metrics[ep, 1 + k]
-            assert abs(lm[k] - ref) <= 1e-3 * abs(ref) + 1e-9, (ep, k, lm[k], ref)
+            assert abs(row[k] - ref) <= 1e-3 * abs(ref) + 1e-9, (ep, k, row[k], ref)
     for w in workers:
         w.check()

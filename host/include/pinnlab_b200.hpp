@@ -10,7 +10,7 @@
 //   TrainingProblem, CollocationConfig, TrainConfig   trainer.hpp:17-86
 //   build_collocation (uniform mode)                  trainer.cpp:47-128
 //   data_parallel_gradient                            trainer.hpp:118-119
-//   train (Adam phase, balancing off)                 trainer.cpp:332-555
+//   train (Adam phase: balancing, causality, Poynting) trainer.cpp:332-555
 //   param_hash                                        trainer.cpp:22-35
 // Errors are thrown as pinnlab_b200::TensorError with the reference's text.
 #pragma once
@@ -147,6 +147,22 @@ struct AdamConfig {
     double eps = 1e-8;
 };
 
+struct BalancingConfig {  // trainer.hpp:45-49
+    bool enabled = true;
+    double alpha = 0.9;
+    int update_period = 100;
+};
+struct CausalityConfig {  // trainer.hpp:51-55
+    bool enabled = false;
+    int segments = 10;
+    double epsilon = 1.0;
+};
+struct PoyntingConfig {  // trainer.hpp:57-61
+    double weight = 0.0;
+    std::size_t grid = 32;
+    std::size_t time_samples = 4;
+};
+
 struct TrainConfig {
     long epochs = 1000;
     std::uint64_t seed = 0;
@@ -154,7 +170,10 @@ struct TrainConfig {
     AdamConfig adam;
     double scheduler_gamma = 1.0;
     CollocationConfig collocation;
-    std::array<double, 3> lambdas{1.0, 1.0, 1.0};  // fixed weights (balancing off)
+    BalancingConfig balancing;
+    CausalityConfig causality;
+    PoyntingConfig poynting;
+    std::array<double, 3> lambdas{1.0, 1.0, 1.0};  // initial loss weights
     int device = 0;                                 // first CUDA device; worker w uses device + w % ndev
     std::function<void(long epoch, std::span<const std::uint64_t>)> on_sync;
 };
@@ -162,6 +181,7 @@ struct TrainConfig {
 struct MetricsRecord {
     long epoch = 0;
     double l_pde = 0.0, l_ic = 0.0, l_bc = 0.0;
+    double lambda_pde = 1.0, lambda_ic = 1.0, lambda_bc = 1.0;
     double lr = 0.0;
 };
 struct TrainResult {
@@ -176,7 +196,8 @@ struct TrainResult {
 std::vector<Tensor> data_parallel_gradient(Model& model, const TrainingProblem& prob, const TrainConfig& cfg,
                                            int workers);
 
-// Adam training loop with fixed loss weights; the per-worker step runs on the GPU.
+// Adam training loop (loss balancing, causality weights, Poynting penalty as
+// configured); the per-worker step runs on the GPU.
 TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& cfg);
 
 std::uint64_t param_hash(const std::vector<NamedTensor>& params);

@@ -243,7 +243,8 @@ std::vector<double> field_major(const std::vector<std::vector<double>>& t) {
 }
 
 std::unique_ptr<Ctx> make_worker(const Model& m, const TrainingProblem& prob, const Points& shard,
-                                 const CollocationData& data, int device) {
+                                 const CollocationData& data, const TrainConfig& cfg) {
+    const int device = cfg.device;
     const ModelSpec& s = m.spec();
     std::vector<int32_t> per, tr;
     std::vector<double> period;
@@ -272,6 +273,15 @@ std::unique_ptr<Ctx> make_worker(const Model& m, const TrainingProblem& prob, co
         auto t = field_major(data.bc_targets);
         w->check(pnx_set_bc(w->ctx, a.data(), b.empty() ? nullptr : b.data(), t.empty() ? nullptr : t.data(),
                             static_cast<int64_t>(data.bc_a.count())));
+    }
+    const auto& dom = prob.domain.bounds;
+    if (cfg.causality.enabled)  // segments over the last axis (trainer.cpp:361-367)
+        w->check(pnx_set_causality(w->ctx, cfg.causality.segments, cfg.causality.epsilon, dom.back()[0],
+                                   dom.back()[1]));
+    if (cfg.poynting.weight > 0.0 && prob.residual.id == PdeId::maxwell_te) {  // trainer.cpp:240-247
+        const double box[6] = {dom[0][0], dom[0][1], dom[1][0], dom[1][1], dom.back()[0], dom.back()[1]};
+        w->check(pnx_set_poynting(w->ctx, cfg.poynting.weight, static_cast<int32_t>(cfg.poynting.grid),
+                                  static_cast<int32_t>(cfg.poynting.time_samples), box));
     }
     return w;
 }
@@ -331,6 +341,43 @@ std::vector<double> synchronized_step(std::vector<std::unique_ptr<Ctx>>& workers
     return avg;
 }
 
+// per-term gradients of every worker (trainer.cpp:256-260), averaged per term
+std::array<std::vector<double>, 3> synchronized_terms(std::vector<std::unique_ptr<Ctx>>& workers,
+                                                     const std::vector<double>& params,
+                                                     std::array<double, 3>& mean_losses) {
+    const std::size_t W = workers.size(), P = params.size();
+    std::vector<std::vector<double>> g(W, std::vector<double>(3 * P));
+    std::vector<std::array<double, 3>> l(W);
+    std::vector<std::string> errors(W);
+    std::vector<std::thread> threads;
+    for (std::size_t w = 0; w < W; ++w)
+        threads.emplace_back([&, w] {
+            const int rc = pnx_step_terms(workers[w]->ctx, params.data(), g[w].data(), l[w].data());
+            if (rc != PNX_OK) errors[w] = pnx_last_error(workers[w]->ctx);
+        });
+    for (auto& t : threads) t.join();
+    for (const auto& e : errors)
+        if (!e.empty()) throw TensorError(e);
+    const double inv = 1.0 / static_cast<double>(W);
+    std::array<std::vector<double>, 3> avg;
+    for (int k = 0; k < 3; ++k) {
+        avg[k].assign(g[0].begin() + k * static_cast<std::ptrdiff_t>(P), g[0].begin() + (k + 1) * static_cast<std::ptrdiff_t>(P));
+        for (std::size_t w = 1; w < W; ++w)
+            for (std::size_t i = 0; i < P; ++i) avg[k][i] += g[w][k * P + i];
+        for (auto& v : avg[k]) v *= inv;
+    }
+    mean_losses = {0.0, 0.0, 0.0};
+    for (std::size_t w = 0; w < W; ++w)
+        for (int t = 0; t < 3; ++t) mean_losses[t] += l[w][t] * inv;
+    return avg;
+}
+
+double vec_norm(const std::vector<double>& v) {  // grad_vec_norm (trainer.cpp:283-288)
+    double s = 0.0;
+    for (double x : v) s += x * x;
+    return std::sqrt(s);
+}
+
 int device_count() {
     // contexts need a device; pnx_create reports a missing GPU itself
     return 0;
@@ -344,7 +391,7 @@ std::vector<Tensor> data_parallel_gradient(Model& model, const TrainingProblem& 
     CollocationData data = build_collocation(prob, cfg.collocation, cfg.seed);
     std::vector<Points> shards = shard_interior(data.interior, W);
     std::vector<std::unique_ptr<Ctx>> ctxs;
-    for (int w = 0; w < W; ++w) ctxs.push_back(make_worker(model, prob, shards[static_cast<std::size_t>(w)], data, cfg.device));
+    for (int w = 0; w < W; ++w) ctxs.push_back(make_worker(model, prob, shards[static_cast<std::size_t>(w)], data, cfg));
     std::array<double, 3> losses{};
     std::vector<double> g = synchronized_step(ctxs, flatten(model.trainable()), {1.0, 1.0, 1.0}, losses);
     std::vector<Tensor> out;
@@ -365,15 +412,42 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
     CollocationData data = build_collocation(prob, cfg.collocation, cfg.seed);
     std::vector<Points> shards = shard_interior(data.interior, W);
     std::vector<std::unique_ptr<Ctx>> ctxs;
-    for (int w = 0; w < W; ++w) ctxs.push_back(make_worker(model, prob, shards[static_cast<std::size_t>(w)], data, cfg.device));
+    for (int w = 0; w < W; ++w) ctxs.push_back(make_worker(model, prob, shards[static_cast<std::size_t>(w)], data, cfg));
     std::vector<double> p = flatten(model.trainable());
     std::vector<double> m(p.size(), 0.0), v(p.size(), 0.0);
+    std::array<double, 3> lam = cfg.lambdas;  // LossState (losses.hpp:70-78)
+    const bool has_bc = prob.bc != TrainingProblem::Bc::hard;
+    const bool pen_on = cfg.poynting.weight > 0.0 && prob.residual.id == PdeId::maxwell_te;
     long t = 0;
     for (long epoch = 0; epoch < cfg.epochs; ++epoch) {
         std::array<double, 3> losses{};
         std::vector<double> g;
+        const bool balance_now = cfg.balancing.enabled && cfg.balancing.update_period > 0 &&
+                                 epoch % cfg.balancing.update_period == 0;
         try {
-            g = synchronized_step(ctxs, p, cfg.lambdas, losses);
+            if (!balance_now) {
+                g = synchronized_step(ctxs, p, lam, losses);
+            } else {  // trainer.cpp:462-506
+                auto terms = synchronized_terms(ctxs, p, losses);
+                std::array<double, 3> norms{vec_norm(terms[0]), vec_norm(terms[1]), has_bc ? vec_norm(terms[2]) : 0.0};
+                const double a = cfg.balancing.alpha;
+                const std::array<double, 3> old = lam;
+                const double tot = norms[0] + norms[1] + (has_bc ? norms[2] : 0.0);
+                for (int k = 0; k < (has_bc ? 3 : 2); ++k)
+                    lam[static_cast<std::size_t>(k)] = a * lam[static_cast<std::size_t>(k)] +
+                                                       (1.0 - a) * (tot / std::max(norms[static_cast<std::size_t>(k)], 1e-9));
+                if (pen_on) {  // total gradient under the previous weights (trainer.cpp:491-498)
+                    std::array<double, 3> l2{};
+                    g = synchronized_step(ctxs, p, old, l2);
+                } else {
+                    g.assign(p.size(), 0.0);
+                    for (std::size_t i = 0; i < g.size(); ++i) {
+                        double s = lam[0] * terms[0][i] + lam[1] * terms[1][i];
+                        if (has_bc) s += lam[2] * terms[2][i];
+                        g[i] = s;
+                    }
+                }
+            }
         } catch (const std::exception& e) {
             result.aborted = true;
             result.abort_reason = e.what();
@@ -400,7 +474,7 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
         std::size_t at = 0;
         for (auto& prm : model.trainable())
             for (auto& x : prm.value.data) x = p[at++];
-        result.metrics.push_back({epoch, losses[0], losses[1], losses[2], lr});
+        result.metrics.push_back({epoch, losses[0], losses[1], losses[2], lam[0], lam[1], lam[2], lr});
         if (cfg.on_sync) {
             std::vector<std::uint64_t> hashes(static_cast<std::size_t>(W), param_hash(model.trainable()));
             cfg.on_sync(epoch, hashes);

@@ -97,6 +97,15 @@ int main(int argc, char** argv) {
         cfg.collocation.n_ic = static_cast<std::size_t>(num("n_ic", 128));
         cfg.collocation.n_bc = static_cast<std::size_t>(num("n_bc", 64));
         const int workers = static_cast<int>(num("workers", 1));
+        cfg.balancing.enabled = num("balancing", 0) != 0.0;
+        cfg.balancing.alpha = num("alpha", 0.9);
+        cfg.balancing.update_period = static_cast<int>(num("update_period", 100));
+        cfg.causality.enabled = num("causality_segments", 0) > 0;
+        cfg.causality.segments = static_cast<int>(num("causality_segments", 10));
+        cfg.causality.epsilon = num("causality_epsilon", 1.0);
+        cfg.poynting.weight = num("poynting_weight", 0.0);
+        cfg.poynting.grid = static_cast<std::size_t>(num("poynting_grid", 32));
+        cfg.poynting.time_samples = static_cast<std::size_t>(num("poynting_time_samples", 4));
 
         if (mode == "cpu") {
             std::vector<double> p;
@@ -124,9 +133,8 @@ int main(int argc, char** argv) {
             if (r.aborted) throw TensorError(r.abort_reason);
             std::vector<double> m;
             for (const auto& rec : r.metrics) {
-                m.push_back(rec.l_pde);
-                m.push_back(rec.l_ic);
-                m.push_back(rec.l_bc);
+                for (double x : {rec.l_pde, rec.l_ic, rec.l_bc, rec.lambda_pde, rec.lambda_ic, rec.lambda_bc})
+                    m.push_back(x);
             }
             write_f64(out + "/metrics.bin", m);
             std::vector<double> p;

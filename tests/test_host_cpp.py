@@ -38,6 +38,16 @@ def _job(g, path, **extra):
         lines.append(f"rff {m['rff']['width']} {m['rff'].get('sigma', 10.0)} {m['rff'].get('mean', 0.0)}")
     if "rwf" in m:
         lines.append(f"rwf {m['rwf'].get('mean', 1.0)} {m['rwf'].get('stddev', 0.1)}")
+    t = c.get("train", {})
+    if t.get("balancing"):
+        lines += ["balancing 1", f"alpha {t.get('alpha', 0.9)}", f"update_period {t.get('update_period', 100)}"]
+    if c.get("causality", {}).get("enabled"):
+        lines += [f"causality_segments {c['causality'].get('segments', 10)}",
+                  f"causality_epsilon {c['causality'].get('epsilon', 1.0)}"]
+    if c.get("poynting", {}).get("weight", 0.0) > 0.0:
+        pj = c["poynting"]
+        lines += [f"poynting_weight {pj['weight']}", f"poynting_grid {pj.get('grid', 32)}",
+                  f"poynting_time_samples {pj.get('time_samples', 4)}"]
     for k, v in extra.items():
         lines.append(f"{k} {v}")
     with open(path, "w") as f:
@@ -76,7 +86,7 @@ def test_cpp_train_trajectory_on_gpu(name, tmp_path):
     t = g["case"]["train"]
     _job(g, tmp_path / "job.txt", workers=g["case"]["workers"], epochs=t["epochs"], lr=t["lr"], gamma=t["gamma"])
     subprocess.run([_driver(), "train", str(tmp_path / "job.txt"), str(tmp_path)], check=True)
-    m = np.fromfile(tmp_path / "metrics.bin", dtype="<f8").reshape(-1, 3)
-    ref = g["metrics"][:, 1:4]
+    m = np.fromfile(tmp_path / "metrics.bin", dtype="<f8").reshape(-1, 6)
+    ref = g["metrics"][:, 1:7]  # l_pde, l_ic, l_bc, lambda_pde, lambda_ic, lambda_bc
     assert m.shape == ref.shape
     assert np.all(np.abs(m - ref) <= 1e-3 * np.abs(ref) + 1e-9)

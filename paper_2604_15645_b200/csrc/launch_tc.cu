@@ -58,7 +58,23 @@ int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? 0 : -1;
 }
 template <int L>
+int launch_tc5_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
+    using Cfg = Tc5BwdCfg<L>;
+    auto kern = k_tc5_bwd<L>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
+            return -1;
+        attr = true;
+    }
+    kern<<<g.Rpad / TC_M, TC3_THREADS, Cfg::SMEM, st>>>(g);
+    return 0;
+}
+template <int L>
 int launch_tc_layer_l(int mode, int pro, const TcGemmArgs& g, cudaStream_t st) {
+    if constexpr (L == LAY_XT || L == LAY_MX) {
+        if (tc5_bwd_ok(L, g.N, g.K)) return launch_tc5_bwd_t<L>(g, st);
+    }
     constexpr int NT = tc_nt(Streams<L>::S);
     (void)mode;
     (void)pro;

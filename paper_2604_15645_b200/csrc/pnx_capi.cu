@@ -385,7 +385,8 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 CKL();
             }
             if (tc_bwd[l]) {
-                k_tc_prep_image<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 1, NT,
+                k_tc_prep_image<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 1,
+                                                    tc5_bwd_ok(L, t.K[l], t.N[l]) ? 256 : NT,
                                                     ctx->tc.img + ctx->tc.img_bwd[l]);
                 CKL();
             }

@@ -15,6 +15,7 @@
 // core on stage i. Weights are pre-split and pre-swizzled once per step into
 // "stage images" (k_tc_prep_images) and copied 16 B at a time.
 #pragma once
+#include <cstdlib>
 #include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -85,6 +86,11 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const float* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t lds32u(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
 }
 __device__ __forceinline__ void sts32(uint32_t addr, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
@@ -206,6 +212,13 @@ inline int tc_wgrad_rows(int64_t Rpad, int Kin, int nsm) {
         }
     }
     return pick;
+}
+
+// the decoupled N=256 backward (k_tc5_bwd): first-order tanh layouts whose
+// backward GEMM writes 256 features (PNX_TC5_OFF=1 falls back to k_tc2_bwd)
+inline bool tc5_bwd_ok(int L, int nout, int kred) {
+    static const bool off = getenv("PNX_TC5_OFF") != nullptr;
+    return !off && (L == LAY_XT || L == LAY_MX) && nout == 256 && kred % 8 == 0;
 }
 
 inline bool tc_layer_ok(int S, int K, int N) {
@@ -1044,6 +1057,285 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
         if constexpr (PAIR) tc::tmem_dealloc_pair<512>(tmem);
         else tc::tmem_dealloc<512>(tmem);
     }
+}
+
+// Backward for first-order tanh jets (LAY_XT S=3, LAY_MX S=4), N = 256.
+// The jet transpose decouples there:
+//   zb_s = d hb_s (s >= 1),   zb_0 = d (hb_0 - 2 t P),   P = sum_{s>=1} z_s hb_s,
+// so the streams need not share TMEM. Two passes of two streams each
+// ({1,2} then {3,0}; XT: {1,2} then {0}) run N=256 MMAs into two interleaved
+// accumulators (the tensor pipe's full-rate pattern, tools/rate_probe.cu) and
+// each stream's A tile is converted once (the N=128 n-tiled kernel converted it
+// per n-tile). P (128 rows x 256 features, FP32) lives in shared memory
+// between the passes, accumulated in the same order as act_bwd.
+// Producers start a pass only after the previous epilogue released the stage
+// ring, which the epilogue reuses as its Z_in staging.
+template <int L>
+struct Tc5BwdCfg {
+    static constexpr int S = Streams<L>::S;
+    static constexpr int NF = 256;
+    static constexpr int A_T = TC_TILE_BYTES;    // 128 rows x 8 fp32
+    static constexpr int B_T = NF * 32;          // 256 weight rows x 8 fp32
+    static constexpr int STAGE = 4 * A_T + 2 * B_T;  // 2 streams x (hi, lo) + B (hi, lo)
+    static constexpr int NST = 3;
+    static constexpr int TILE = 32 * 16 * 4;     // 32-row x 16-col staging tile, 16 B chunks XOR-swizzled
+    static constexpr int EPI_BYTES = 8 * 2 * 3 * TILE;  // 8 warps x 2 buffers x {t, zA, zB}
+    static constexpr int P_BYTES = 128 * NF * 4;
+    static constexpr int SMEM = NST * STAGE + P_BYTES + 1024;
+    static_assert(NST * STAGE >= EPI_BYTES, "epilogue staging must fit in the stage ring");
+    static_assert(SMEM <= 227 * 1024, "tc5 bwd shared memory");
+    // pass -> streams (second = -1: single accumulator)
+    __host__ __device__ static constexpr int sa(int pass) { return pass == 0 ? 1 : (S == 4 ? 3 : 0); }
+    __host__ __device__ static constexpr int sb(int pass) { return pass == 0 ? 2 : (S == 4 ? 0 : -1); }
+};
+
+template <int L>
+__global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constant__ TcGemmArgs g) {
+    using Cfg = Tc5BwdCfg<L>;
+    constexpr int NST = Cfg::NST, NF = Cfg::NF;
+    static_assert(L == LAY_XT || L == LAY_MX, "first-order layouts only");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    __shared__ uint64_t full[NST], empty[NST], tfull, tempty;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r0 = blockIdx.x * TC_M;
+    const int nkb = g.K / 8;
+    const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * NF;
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            tc::mbar_init(&full[i], 9);  // 8 producer warps + expect_tx
+            tc::mbar_init(&empty[i], 1);
+        }
+        tc::mbar_init(&tfull, 1);
+        tc::mbar_init(&tempty, 8);
+        tc::fence_barrier_init();
+    }
+    if (warp == 8) tc::tmem_alloc<512>(&tmem_base);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = tc::smem_u32(smem);
+    const uint32_t sP = sbase + NST * Cfg::STAGE;
+
+    if (warp < 8) {
+        // ---------------- producers: A tiles of the pass's two streams ----------------
+        const int prow = tid >> 1, pc = tid & 1;
+        const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
+        const uint32_t aoff = tc::sw32_off((uint32_t)prow, (uint32_t)(pc * 4));
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            const int s0 = Cfg::sa(pass), s1 = Cfg::sb(pass);
+            constexpr int D = 4;  // k-steps of A prefetched in registers
+            float4 ra[D], rb[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                ra[d] = d < nkb ? ldg4(asrc + s0 * RK + d * 8) : make_float4(0.f, 0.f, 0.f, 0.f);
+                rb[d] = (s1 >= 0 && d < nkb) ? ldg4(asrc + s1 * RK + d * 8) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            if (pass == 1) tc::mbar_wait(&tempty, 0);  // the epilogue released the stage ring
+#pragma unroll 1
+            for (int kb0 = 0; kb0 < nkb; kb0 += D)
+#pragma unroll
+            for (int cur = 0; cur < D; ++cur) {
+                const int kb = kb0 + cur;
+                if (kb >= nkb) break;
+                const int it = pass * nkb + kb, st = it % NST;
+                const uint32_t stage = sbase + st * Cfg::STAGE;
+                const float4 va = ra[cur], vb = rb[cur];
+                if (kb + D < nkb) {
+                    ra[cur] = ldg4(asrc + s0 * RK + (kb + D) * 8);
+                    if (s1 >= 0) rb[cur] = ldg4(asrc + s1 * RK + (kb + D) * 8);
+                }
+                float4 ah, al, bh, bl;
+                split4(va, ah, al);
+                split4(vb, bh, bl);
+                tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                if (tid == 0) {
+                    tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
+                    tc::bulk_g2s(stage + 4 * Cfg::A_T, g.img + (int64_t)kb * (2 * Cfg::B_T / 4), 2 * Cfg::B_T,
+                                 &full[st]);
+                }
+                sts128(stage + aoff, ah);
+                sts128(stage + Cfg::A_T + aoff, al);
+                if (s1 >= 0) {
+                    sts128(stage + 2 * Cfg::A_T + aoff, bh);
+                    sts128(stage + 3 * Cfg::A_T + aoff, bl);
+                }
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&full[st]);
+            }
+        }
+    } else if (warp == 8) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NF, 0, 0);
+            for (int pass = 0; pass < 2; ++pass) {
+                const bool two = Cfg::sb(pass) >= 0;
+                if (pass == 1) tc::mbar_wait(&tempty, 0);
+                tc::tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb) {
+                    const int it = pass * nkb + kb, st = it % NST;
+                    const uint32_t stage = sbase + st * Cfg::STAGE;
+                    {
+                        TC_T0();
+                        tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                        TC_ACC(0);
+                    }
+                    tc::tc_fence_after();
+                    const uint64_t bh = tc::make_sdesc(stage + 4 * Cfg::A_T, 16, 256, 6);
+                    const uint64_t bl = tc::make_sdesc(stage + 4 * Cfg::A_T + Cfg::B_T, 16, 256, 6);
+#pragma unroll
+                    for (int a = 0; a < 2; ++a) {
+                        if (a == 1 && !two) break;
+                        const uint32_t ah = stage + (2 * a) * Cfg::A_T;
+                        const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(ah + Cfg::A_T, 16, 256, 6);
+                        const uint32_t d = tmem + (uint32_t)(a * NF);
+                        tc::mma_tf32(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
+                        tc::mma_tf32(d, adh, bl, idesc, 1u);
+                        tc::mma_tf32(d, adl, bh, idesc, 1u);
+                    }
+                    tc::mma_commit(&empty[st]);
+                }
+                tc::mma_commit(&tfull);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue: 16-column chunks, Z_in staged by cp.async ----------------
+        // staging tiles: row r, 16 B chunk c at r*64 + ((c ^ ((r>>1)&3)) << 4): conflict-free
+        // for both the row-per-lane reads and the 8-rows-per-instruction copies.
+        // Double-buffered: the tiles of chunk i+1 are in flight while chunk i computes.
+        const int q = warp & 3, half = (warp - 9) >> 2, ew = warp - 9;
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t stg0 = sbase + (uint32_t)ew * 2 * 3 * Cfg::TILE;
+        const uint32_t pbuf = sP + (uint32_t)ew * 128 * 32 * 4;     // [col][lane]
+        const int64_t rbase = (int64_t)(r0 + q * 32) * NF;
+        const int lr = lane >> 2, lcv = lane & 3;
+        auto soff = [](int r, int c) { return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4)); };
+        for (int pass = 0; pass < 2; ++pass) {
+            const int s0 = Cfg::sa(pass), s1 = Cfg::sb(pass);
+            // Z_in tiles this pass needs: t (stream 0) and z of its first-order streams
+            const int zA = s0 > 0 ? s0 : -1, zB = s1 > 0 ? s1 : -1;
+            auto issue = [&](int cch) {
+                const uint32_t stg = stg0 + (uint32_t)(cch & 1) * 3 * Cfg::TILE;
+                const int c0 = half * 128 + cch * 16;
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const int sz = u == 0 ? 0 : (u == 1 ? zA : zB);
+                    if (sz < 0) continue;
+                    const float* src = g.Zlow + sz * RN + rbase + c0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        cp_async16(stg + u * Cfg::TILE + soff(8 * k + lr, lcv), src + (int64_t)(8 * k + lr) * NF + lcv * 4);
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            tc::mbar_wait(&tfull, (uint32_t)pass);
+            tc::tc_fence_after();
+            TC_T0();
+            issue(0);
+#pragma unroll 1
+            for (int cch = 0; cch < 8; ++cch) {
+                const int c0 = half * 128 + cch * 16;
+                const uint32_t stg = stg0 + (uint32_t)(cch & 1) * 3 * Cfg::TILE;
+                float ha[16], hb[16];
+                tc::tmem_ld16(tl + (uint32_t)c0, ha);
+                if (s1 >= 0) tc::tmem_ld16(tl + (uint32_t)(NF + c0), hb);
+                if (cch + 1 < 8) {
+                    issue(cch + 1);
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                __syncwarp();
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int j4 = 0; j4 < 16; j4 += 4) {
+                    const uint32_t ro = soff(lane, j4 >> 2);
+                    const float4 t4 = lds128(stg + ro);
+                    const float tt[4] = {t4.x, t4.y, t4.z, t4.w};
+                    float za[4] = {0.f, 0.f, 0.f, 0.f}, zb2[4] = {0.f, 0.f, 0.f, 0.f}, pp[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (zA >= 0) {
+                        const float4 v = lds128(stg + Cfg::TILE + ro);
+                        za[0] = v.x; za[1] = v.y; za[2] = v.z; za[3] = v.w;
+                    }
+                    if (zB >= 0) {
+                        const float4 v = lds128(stg + 2 * Cfg::TILE + ro);
+                        zb2[0] = v.x; zb2[1] = v.y; zb2[2] = v.z; zb2[3] = v.w;
+                    }
+                    if (pass == 1) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            pp[e] = __uint_as_float(lds32u(pbuf + (uint32_t)(((cch * 16 + j4 + e) * 32 + lane) * 4)));
+                    }
+                    float oa[4], ob[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int j = j4 + e;
+                        const float t = tt[e];
+                        const float d = 1.0f - t * t;
+                        if (pass == 0) {
+                            // streams 1, 2: zb_s = d hb_s ; P = z_1 hb_1 + z_2 hb_2
+                            oa[e] = d * ha[j];
+                            ob[e] = d * hb[j];
+                            float P = 0.0f;
+                            P += za[e] * ha[j];
+                            P += zb2[e] * hb[j];
+                            pp[e] = P;
+                        } else if (Streams<L>::S == 4) {
+                            // streams 3, 0: zb_3 = d hb_3 ; zb_0 = d (hb_0 - 2 t (P + z_3 hb_3))
+                            oa[e] = d * ha[j];
+                            float P = pp[e];
+                            P += za[e] * ha[j];
+                            float tbar = hb[j];
+                            tbar += -2.0f * t * P;
+                            ob[e] = d * tbar;
+                        } else {
+                            // XT stream 0: zb_0 = d (hb_0 - 2 t P)
+                            float tbar = ha[j];
+                            tbar += -2.0f * t * pp[e];
+                            oa[e] = d * tbar;
+                            ob[e] = 0.0f;
+                        }
+                    }
+                    if (pass == 0) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            sts32(pbuf + (uint32_t)(((cch * 16 + j4 + e) * 32 + lane) * 4), pp[e]);
+                    }
+                    // outputs in place: stream s0 -> its z tile (the t tile when s0 = 0),
+                    // stream s1 -> its z tile (the t tile when s1 = 0)
+                    sts128(stg + (zA >= 0 ? Cfg::TILE : 0) + ro, make_float4(oa[0], oa[1], oa[2], oa[3]));
+                    if (s1 >= 0) sts128(stg + (zB >= 0 ? 2 * Cfg::TILE : 0) + ro, make_float4(ob[0], ob[1], ob[2], ob[3]));
+                }
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int so = u == 0 ? s0 : s1;
+                    if (so < 0) continue;
+                    const int slot = u == 0 ? (zA >= 0 ? 1 : 0) : (zB >= 0 ? 2 : 0);
+                    float* dst = g.out + so * RN + rbase + c0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float4 v = lds128(stg + slot * Cfg::TILE + soff(8 * k + lr, lcv));
+                        *reinterpret_cast<float4*>(dst + (int64_t)(8 * k + lr) * NF + lcv * 4) = v;
+                    }
+                }
+                __syncwarp();
+            }
+            if (warp == 9 && lane == 0) TC_ACC(3);
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 8) tc::tmem_dealloc<512>(tmem);
 }
 
 // PAIR: a 2-CTA cluster covers 256 rows of one n-tile with cta_group::2 MMAs

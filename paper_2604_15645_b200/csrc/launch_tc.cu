@@ -57,23 +57,41 @@ int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? 0 : -1;
 }
-template <int L>
+template <int L, bool PAIR>
 int launch_tc5_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
-    using Cfg = Tc5BwdCfg<L>;
-    auto kern = k_tc5_bwd<L>;
+    using Cfg = Tc5BwdCfg<L, PAIR>;
+    auto kern = k_tc5_bwd<L, PAIR>;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
             return -1;
         attr = true;
     }
-    kern<<<g.Rpad / TC_M, TC3_THREADS, Cfg::SMEM, st>>>(g);
-    return 0;
+    TcGemmArgs a = g;
+    if (PAIR && tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)(g.K / 8) * 2 * Cfg::NF, 1, 8, Cfg::NFL, 1, false))
+        return -1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.Rpad / TC_M);
+    cfg.blockDim = dim3(TC3_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = PAIR ? 2 : 1;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? 0 : -1;
 }
 template <int L>
 int launch_tc_layer_l(int mode, int pro, const TcGemmArgs& g, cudaStream_t st) {
     if constexpr (L == LAY_XT || L == LAY_MX) {
-        if (tc5_bwd_ok(L, g.N, g.K)) return launch_tc5_bwd_t<L>(g, st);
+        // the pair variant is bit-identical but not faster (the MMA phase is shared-
+        // memory bound, tools/trace_bwd5.cu), so it is opt-in
+        static const bool pair5 = getenv("PNX_TC5_PAIR") != nullptr;
+        if (tc5_bwd_ok(L, g.N, g.K))
+            return pair5 && g.Rpad % 256 == 0 ? launch_tc5_bwd_t<L, true>(g, st) : launch_tc5_bwd_t<L, false>(g, st);
     }
     constexpr int NT = tc_nt(Streams<L>::S);
     (void)mode;

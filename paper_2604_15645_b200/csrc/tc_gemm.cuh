@@ -1070,55 +1070,68 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
 // between the passes, accumulated in the same order as act_bwd.
 // Producers start a pass only after the previous epilogue released the stage
 // ring, which the epilogue reuses as its Z_in staging.
-template <int L>
+// PAIR: a 2-CTA cluster covers 256 rows (cta_group::2, M = 256); each CTA
+// stages half of the weight rows, which halves the stage and leaves room for a
+// fourth one (the single-CTA ring is too shallow to hide the weight copies).
+template <int L, bool PAIR = false>
 struct Tc5BwdCfg {
     static constexpr int S = Streams<L>::S;
     static constexpr int NF = 256;
+    static constexpr int NFL = PAIR ? NF / 2 : NF;  // weight rows staged by this CTA
     static constexpr int A_T = TC_TILE_BYTES;    // 128 rows x 8 fp32
-    static constexpr int B_T = NF * 32;          // 256 weight rows x 8 fp32
+    static constexpr int B_T = NFL * 32;         // weight rows x 8 fp32
     static constexpr int STAGE = 4 * A_T + 2 * B_T;  // 2 streams x (hi, lo) + B (hi, lo)
-    static constexpr int NST = 3;
+    static constexpr int NST = PAIR ? 4 : 3;
     static constexpr int TILE = 32 * 16 * 4;     // 32-row x 16-col staging tile, 16 B chunks XOR-swizzled
     static constexpr int EPI_BYTES = 8 * 2 * 3 * TILE;  // 8 warps x 2 buffers x {t, zA, zB}
     static constexpr int P_BYTES = 128 * NF * 4;
     static constexpr int SMEM = NST * STAGE + P_BYTES + 1024;
     static_assert(NST * STAGE >= EPI_BYTES, "epilogue staging must fit in the stage ring");
     static_assert(SMEM <= 227 * 1024, "tc5 bwd shared memory");
+    static_assert(NST >= 3, "two k-steps per producer iteration need a third stage in flight");
     // pass -> streams (second = -1: single accumulator)
     __host__ __device__ static constexpr int sa(int pass) { return pass == 0 ? 1 : (S == 4 ? 3 : 0); }
     __host__ __device__ static constexpr int sb(int pass) { return pass == 0 ? 2 : (S == 4 ? 0 : -1); }
 };
 
-template <int L>
+template <int L, bool PAIR>
 __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constant__ TcGemmArgs g) {
-    using Cfg = Tc5BwdCfg<L>;
+    using Cfg = Tc5BwdCfg<L, PAIR>;
     constexpr int NST = Cfg::NST, NF = Cfg::NF;
     static_assert(L == LAY_XT || L == LAY_MX, "first-order layouts only");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
-    __shared__ uint64_t full[NST], empty[NST], tfull, tempty;
+    __shared__ uint64_t full[NST], empty[NST], tfull, tempty, tempty_all;
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int r0 = blockIdx.x * TC_M;
+    const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0;
+    const int r0 = PAIR ? (int)(blockIdx.x >> 1) * 256 + (int)rank * 128 : (int)blockIdx.x * TC_M;
     const int nkb = g.K / 8;
     const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * NF;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
-            tc::mbar_init(&full[i], 9);  // 8 producer warps + expect_tx
+            tc::mbar_init(&full[i], PAIR ? 17 : 9);  // producer warps (both CTAs) + expect_tx
             tc::mbar_init(&empty[i], 1);
         }
         tc::mbar_init(&tfull, 1);
-        tc::mbar_init(&tempty, 8);
+        tc::mbar_init(&tempty, 8);                 // this CTA's epilogue -> its producers
+        tc::mbar_init(&tempty_all, PAIR ? 16 : 8);  // both epilogues -> the MMA issuer
         tc::fence_barrier_init();
     }
-    if (warp == 8) tc::tmem_alloc<512>(&tmem_base);
+    if (warp == 8) {
+        if constexpr (PAIR) tc::tmem_alloc_pair<512>(&tmem_base);
+        else tc::tmem_alloc<512>(&tmem_base);
+    }
     tc::tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) tc::cluster_sync();
+    else __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
     const uint32_t sbase = tc::smem_u32(smem);
     const uint32_t sP = sbase + NST * Cfg::STAGE;
+    const uint32_t full0 = PAIR ? tc::mapa(tc::smem_u32(&full[0]), 0) : tc::smem_u32(&full[0]);
+    const uint32_t tempty_all0 = PAIR ? tc::mapa(tc::smem_u32(&tempty_all), 0) : tc::smem_u32(&tempty_all);
 
     if (warp < 8) {
         // ---------------- producers: A tiles of the pass's two streams ----------------
@@ -1136,46 +1149,72 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                 rb[d] = (s1 >= 0 && d < nkb) ? ldg4(asrc + s1 * RK + d * 8) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
             if (pass == 1) tc::mbar_wait(&tempty, 0);  // the epilogue released the stage ring
+            // two k-steps per iteration: their stores share one proxy fence
 #pragma unroll 1
             for (int kb0 = 0; kb0 < nkb; kb0 += D)
 #pragma unroll
-            for (int cur = 0; cur < D; ++cur) {
+            for (int cur = 0; cur < D; cur += 2) {
                 const int kb = kb0 + cur;
                 if (kb >= nkb) break;
-                const int it = pass * nkb + kb, st = it % NST;
-                const uint32_t stage = sbase + st * Cfg::STAGE;
-                const float4 va = ra[cur], vb = rb[cur];
-                if (kb + D < nkb) {
-                    ra[cur] = ldg4(asrc + s0 * RK + (kb + D) * 8);
-                    if (s1 >= 0) rb[cur] = ldg4(asrc + s1 * RK + (kb + D) * 8);
+                float4 h[2][4];  // per k-step: A hi, A lo, B hi, B lo
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const float4 va = ra[cur + u], vb = rb[cur + u];
+                    if (kb + u + D < nkb) {
+                        ra[cur + u] = ldg4(asrc + s0 * RK + (kb + u + D) * 8);
+                        if (s1 >= 0) rb[cur + u] = ldg4(asrc + s1 * RK + (kb + u + D) * 8);
+                    }
+                    split4(va, h[u][0], h[u][1]);
+                    split4(vb, h[u][2], h[u][3]);
                 }
-                float4 ah, al, bh, bl;
-                split4(va, ah, al);
-                split4(vb, bh, bl);
-                tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
-                if (tid == 0) {
-                    tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
-                    tc::bulk_g2s(stage + 4 * Cfg::A_T, g.img + (int64_t)kb * (2 * Cfg::B_T / 4), 2 * Cfg::B_T,
-                                 &full[st]);
-                }
-                sts128(stage + aoff, ah);
-                sts128(stage + Cfg::A_T + aoff, al);
-                if (s1 >= 0) {
-                    sts128(stage + 2 * Cfg::A_T + aoff, bh);
-                    sts128(stage + 3 * Cfg::A_T + aoff, bl);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int it = pass * nkb + kb + u, st = it % NST;
+                    const uint32_t stage = sbase + st * Cfg::STAGE;
+                    {
+                        TC_T0();
+                        tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                        if (tid == 0) TC_ACC(2);
+                    }
+                    if (tid == 0) {
+                        const int kk = kb + u;
+                        if constexpr (PAIR) {
+                            // image rows (8 fp32 each) of k-step kk: [hi: 256 rows][lo: 256 rows]
+                            const int rowb = kk * 2 * NF + (int)rank * Cfg::NFL;
+                            if (rank == 0) tc::mbar_arrive_expect_tx(&full[st], 2 * 2 * Cfg::B_T);
+                            tc::tma_load_2d_pair(stage + 4 * Cfg::A_T, &g.tmB, 0, rowb, full0 + st * 8);
+                            tc::tma_load_2d_pair(stage + 4 * Cfg::A_T + Cfg::B_T, &g.tmB, 0, rowb + NF, full0 + st * 8);
+                        } else {
+                            tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
+                            tc::bulk_g2s(stage + 4 * Cfg::A_T, g.img + (int64_t)kk * (2 * Cfg::B_T / 4), 2 * Cfg::B_T,
+                                         &full[st]);
+                        }
+                    }
+                    sts128(stage + aoff, h[u][0]);
+                    sts128(stage + Cfg::A_T + aoff, h[u][1]);
+                    if (s1 >= 0) {
+                        sts128(stage + 2 * Cfg::A_T + aoff, h[u][2]);
+                        sts128(stage + 3 * Cfg::A_T + aoff, h[u][3]);
+                    }
                 }
                 tc::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&full[st]);
+                if (lane == 0)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int st = (pass * nkb + kb + u) % NST;
+                        if constexpr (PAIR) tc::mbar_arrive_cluster(full0 + st * 8);
+                        else tc::mbar_arrive(&full[st]);
+                    }
             }
         }
     } else if (warp == 8) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NF, 0, 0);
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NF, 0, 0);
             for (int pass = 0; pass < 2; ++pass) {
                 const bool two = Cfg::sb(pass) >= 0;
-                if (pass == 1) tc::mbar_wait(&tempty, 0);
+                if (pass == 1) tc::mbar_wait(&tempty_all, 0);
                 tc::tc_fence_after();
                 for (int kb = 0; kb < nkb; ++kb) {
                     const int it = pass * nkb + kb, st = it % NST;
@@ -1194,13 +1233,21 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                         const uint32_t ah = stage + (2 * a) * Cfg::A_T;
                         const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(ah + Cfg::A_T, 16, 256, 6);
                         const uint32_t d = tmem + (uint32_t)(a * NF);
-                        tc::mma_tf32(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
-                        tc::mma_tf32(d, adh, bl, idesc, 1u);
-                        tc::mma_tf32(d, adl, bh, idesc, 1u);
+                        if constexpr (PAIR) {
+                            tc::mma_tf32_pair(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
+                            tc::mma_tf32_pair(d, adh, bl, idesc, 1u);
+                            tc::mma_tf32_pair(d, adl, bh, idesc, 1u);
+                        } else {
+                            tc::mma_tf32(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
+                            tc::mma_tf32(d, adh, bl, idesc, 1u);
+                            tc::mma_tf32(d, adl, bh, idesc, 1u);
+                        }
                     }
-                    tc::mma_commit(&empty[st]);
+                    if constexpr (PAIR) tc::mma_commit_pair(&empty[st], 3);
+                    else tc::mma_commit(&empty[st]);
                 }
-                tc::mma_commit(&tfull);
+                if constexpr (PAIR) tc::mma_commit_pair(&tfull, 3);
+                else tc::mma_commit(&tfull);
             }
         }
         __syncwarp();
@@ -1330,12 +1377,20 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
             if (warp == 9 && lane == 0) TC_ACC(3);
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tempty);
+            if (lane == 0) {
+                tc::mbar_arrive(&tempty);
+                if constexpr (PAIR) tc::mbar_arrive_cluster(tempty_all0);
+                else tc::mbar_arrive(&tempty_all);
+            }
         }
     }
     tc::tc_fence_before();
-    __syncthreads();
-    if (warp == 8) tc::tmem_dealloc<512>(tmem);
+    if constexpr (PAIR) tc::cluster_sync();
+    else __syncthreads();
+    if (warp == 8) {
+        if constexpr (PAIR) tc::tmem_dealloc_pair<512>(tmem);
+        else tc::tmem_dealloc<512>(tmem);
+    }
 }
 
 // PAIR: a 2-CTA cluster covers 256 rows of one n-tile with cta_group::2 MMAs

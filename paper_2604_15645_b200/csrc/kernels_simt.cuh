@@ -789,7 +789,7 @@ struct HeadArgs {
 constexpr int kStatMax = 64;  // max causality segments / Poynting time samples
 
 template <int P, int ACT, int J>
-__global__ void __launch_bounds__(32 * kHeadWarps, 1) k_head(HeadArgs a) {
+__global__ void __launch_bounds__(32 * kHeadWarps, 2) k_head(HeadArgs a) {
     using Tr = PdeTraits<P>;
     constexpr int L = Tr::L, F = Tr::F, K = Tr::K;
     constexpr int S = Streams<L>::S;

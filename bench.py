@@ -44,6 +44,7 @@ def _args():
     ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc3xtf32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of CUDA-graph replays")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     return ap.parse_args()
 
@@ -275,23 +276,33 @@ def main():
                             col["bc_a"], col["bc_b"], col["bc_targets"], device=local, engine=args.engine)
     P = worker.n_params
     from paper_2604_15645_b200.dist import DataParallelTrainer
-    trainer = DataParallelTrainer(worker, flat, world=world, lr=1e-3, device=dev)
+    # one CUDA graph per step on a single GPU (the multi-GPU step keeps NCCL eager)
+    trainer = DataParallelTrainer(worker, flat, world=world, lr=1e-3, device=dev, graph=not args.no_graph)
     stream = torch.cuda.current_stream(dev)
     st = stream.cuda_stream
     lam = (1.0, 1.0, 1.0)
 
-    def step():  # device step -> NCCL all-reduce of the flat gradient -> fused Adam(1/W)
-        trainer.step(lam, stream=st)
+    def step(eager=False):  # device step -> NCCL all-reduce of the flat gradient -> fused Adam(1/W)
+        trainer.step(lam, stream=st, eager=eager)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     worker.check()
-    launches_per_step = worker.launch_count() + 1  # + the fused Adam kernel
+    step(eager=True)
+    torch.cuda.synchronize(dev)
+    launches_per_step = worker.launch_count() + (2 if trainer.graph else 1)  # + Adam (+ its counter tick)
 
-    # ---- timed region (device-resident inputs) ----
-    clk = ClockSampler(local)
+    # ---- per-class device time: CUDA events on the launching stream (eager pass) ----
     worker.profile(True)
+    for _ in range(args.steps):
+        step(eager=True)
+    torch.cuda.synchronize(dev)
+    prof = worker.profile_read()
+    worker.profile(False)
+
+    # ---- timed region (device-resident inputs; graph replays when single-GPU) ----
+    clk = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -306,8 +317,6 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
-    prof = worker.profile_read()
-    worker.profile(False)
     worker.check()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -409,7 +418,8 @@ def main():
             "config": {"workload": name, "pde": wl.res.id, "model": f"tanh MLP {wl.spec.depth}x{H}",
                        "points_total": n_total, "points_per_gpu": rows, "streams": S,
                        "params": P, "engine": args.engine, "parallelism": f"dp{world}",
-                       "l2": "inputs larger than L2 (per-step activations >> 126 MB)"},
+                       "l2": "inputs larger than L2 (per-step activations >> 126 MB)",
+                       "cuda_graph": bool(trainer.graph)},
             "tflops_step": step_flops / (ms_step / 1e3) / 1e12,
             "roofline": roof,
             "kernel_ms_per_step": {k: prof[k][0] / args.steps for k in prof},

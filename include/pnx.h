@@ -101,6 +101,15 @@ int pnx_set_bc(pnx_ctx* ctx, const double* a, const double* b, const double* tar
 int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double* grad_out,
              double losses_out[3]);
 
+/* Adam with the step count and epoch kept on the device (d_state[0] = steps
+ * taken, d_state[1] = epoch; both advanced by the call): lr = lr0 * gamma^epoch
+ * (ExponentialLr::at, optim.cpp:71-73) and the bias corrections are formed on
+ * the device, so pnx_step_device + all-reduce + this call can be captured once
+ * in a CUDA graph and replayed every epoch. */
+int pnx_adam_step_device_state(pnx_ctx* ctx, float* d_params, const float* d_grad, float* d_m, float* d_v,
+                               int64_t n, double* d_state, double lr0, double gamma, double beta1, double beta2,
+                               double eps, double grad_scale, void* stream);
+
 /* Per-term gradients of l_pde, l_ic, l_bc alone (run_worker_epoch with
  * want_term_grads, trainer.cpp:256-260): three reverse passes with unit
  * weights and the Poynting penalty excluded; grad_terms_out holds 3 x

@@ -17,6 +17,7 @@ EXPORTS = [
     "pnx_adam_step_device", "pnx_set_engine", "pnx_set_chunk_rows", "pnx_last_launch_count",
     "pnx_capture_residuals", "pnx_copy_residuals", "pnx_profile", "pnx_profile_read",
     "pnx_step_terms", "pnx_step_terms_device", "pnx_set_causality", "pnx_set_poynting", "pnx_last_penalty",
+    "pnx_adam_step_device_state",
 ]
 
 
@@ -71,6 +72,8 @@ def load(path: str = LIB_PATH):
     lib.pnx_set_causality.argtypes = [vp, i32, C.c_double, C.c_double, C.c_double]
     lib.pnx_set_poynting.argtypes = [vp, C.c_double, i32, i32, dp]
     lib.pnx_last_penalty.argtypes = [vp, dp]
+    lib.pnx_adam_step_device_state.argtypes = [vp, vp, vp, vp, vp, i64, vp, C.c_double, C.c_double, C.c_double,
+                                               C.c_double, C.c_double, C.c_double, vp]
     for name in EXPORTS:
         if name not in ("pnx_destroy", "pnx_last_error", "pnx_create_error"):
             getattr(lib, name).restype = C.c_int

@@ -1197,6 +1197,31 @@ static __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g
     }
 }
 
+// Same update with the step count t and the epoch in device memory (state[0] =
+// steps taken, state[1] = epoch): bias corrections and lr = lr0 gamma^epoch
+// (ExponentialLr::at, optim.cpp:71-73) are formed on the device, so a captured
+// CUDA graph replays correct updates; k_adam_tick advances both after the update.
+static __global__ void k_adam_state(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                                    float* __restrict__ v, int64_t n, const double* __restrict__ state, double lr0,
+                                    double gamma, double b1d, double b2d, float eps, float gscale) {
+    const double t = state[0] + 1.0;
+    const float lr = (float)(lr0 * pow(gamma, state[1]));
+    const float bc1 = (float)(1.0 - pow(b1d, t)), bc2 = (float)(1.0 - pow(b2d, t));
+    const float b1 = (float)b1d, b2 = (float)b2d;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float gi = g[i] * gscale;
+        const float mi = b1 * m[i] + (1.0f - b1) * gi;
+        const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        p[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    }
+}
+static __global__ void k_adam_tick(double* state) {
+    state[0] += 1.0;
+    state[1] += 1.0;
+}
+
 static __global__ void k_f64_to_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         b[i] = (float)a[i];

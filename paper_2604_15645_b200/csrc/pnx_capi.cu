@@ -254,6 +254,13 @@ int upload_rows(pnx_ctx* ctx) {
     if (!ctx->h_bc_t.empty())
         CK(cudaMemcpy(ctx->d_bc_t, ctx->h_bc_t.data(), ctx->h_bc_t.size() * 4, cudaMemcpyHostToDevice));
     if (int r = dalloc(ctx, &ctx->d_bc_vals, (size_t)std::max<int64_t>(1, ctx->n_bca + ctx->n_bcb) * ctx->F)) return r;
+    {
+        const double inv[3] = {1.0 / (double)ctx->n_int, ctx->n_ic ? 1.0 / (double)ctx->n_ic : 0.0,
+                               ctx->n_bca ? 1.0 / (double)ctx->n_bca : 0.0};
+        CK(cudaMemcpy(ctx->d_losses + 3, inv, sizeof(inv), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(reinterpret_cast<char*>(ctx->d_losses + 8), ctx->period_off, sizeof(ctx->period_off),
+                      cudaMemcpyHostToDevice));
+    }
 
     if (T == ctx->layout_T && ctx->chunk_override == ctx->layout_chunk_override) {
         ctx->rows_dirty = false;
@@ -636,12 +643,8 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         CKL();
     }
     {
-        double inv[3] = {1.0 / (double)ctx->n_int, ctx->n_ic ? 1.0 / (double)ctx->n_ic : 0.0,
-                         ctx->n_bca ? 1.0 / (double)ctx->n_bca : 0.0};
-        // small constant args via a device scratch (last 8 doubles of d_losses area)
-        CK(cudaMemcpyAsync(ctx->d_losses + 3, inv, sizeof(inv), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->d_losses + 8), ctx->period_off, sizeof(ctx->period_off),
-                           cudaMemcpyHostToDevice, st));
+        // 1/n per term and the period offsets live in d_losses[3..] (uploaded with the
+        // rows, so the step itself enqueues kernels and memsets only: graph-capturable)
         k_write_scalar_grads<<<1, 32, 0, st>>>(ctx->d_partP, ctx->ibwd_grid,
                                                reinterpret_cast<const int64_t*>(ctx->d_losses + 8), ctx->in_dim,
                                                1.0f, d_grad, ctx->d_loss_part, ctx->head_grid, ctx->d_losses + 3,
@@ -1129,6 +1132,21 @@ int pnx_step_terms_device(pnx_ctx* ctx, const float* d_params, float* d_grads, d
     }
     ctx->no_penalty = false;
     return r;
+}
+
+int pnx_adam_step_device_state(pnx_ctx* ctx, float* d_params, const float* d_grad, float* d_m, float* d_v,
+                               int64_t n, double* d_state, double lr0, double gamma, double beta1, double beta2,
+                               double eps, double grad_scale, void* stream) {
+    if (!ctx || !d_params || !d_grad || !d_m || !d_v || !d_state || n <= 0) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_adam_state<<<grid, 256, 0, st>>>(d_params, d_grad, d_m, d_v, n, d_state, lr0, gamma, beta1, beta2,
+                                       (float)eps, (float)grad_scale);
+    CKL();
+    k_adam_tick<<<1, 1, 0, st>>>(d_state);
+    CKL();
+    return PNX_OK;
 }
 
 int pnx_adam_step_device(pnx_ctx* ctx, float* d_params, const float* d_grad, float* d_m, float* d_v,

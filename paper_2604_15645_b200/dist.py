@@ -85,7 +85,7 @@ class DataParallelTrainer:
 
     def __init__(self, worker, params0: np.ndarray, world: int = 1, lr: float = 1e-3, gamma: float = 1.0,
                  betas=(0.9, 0.999), eps: float = 1e-8, device=None, group=None, balancing=None,
-                 has_bc: bool = True, poynting: bool = False):
+                 has_bc: bool = True, poynting: bool = False, graph: bool = False):
         import torch
         self.torch = torch
         self.workers = list(worker) if isinstance(worker, (list, tuple)) else [worker]
@@ -106,6 +106,13 @@ class DataParallelTrainer:
         self.losses = torch.zeros(3, dtype=torch.float64, device=dev)
         self.t = 0
         self.epoch = 0
+        # CUDA-graph mode (one process per GPU without a collective to capture):
+        # Adam keeps (steps, epoch) on the device so one captured step replays.
+        self.graph = graph and world == 1
+        self.state = torch.zeros(2, dtype=torch.float64, device=dev)
+        self._graph = None
+        self._glam = None
+        self._warm = False
 
     def _total(self, lam, st):
         for w, gb, lb in zip(self.workers, self._wgrad, self._wloss):
@@ -144,24 +151,52 @@ class DataParallelTrainer:
             if self.has_bc:
                 self.grad.add_(terms[2], alpha=self.lam[2])
 
-    def step(self, lambdas=None, stream=None):
-        st = stream if stream is not None else self.torch.cuda.current_stream(self.params.device).cuda_stream
-        b = self.balancing
-        if lambdas is not None:
-            self.lam = list(lambdas)
-        if b is not None and b.enabled and b.update_period > 0 and self.epoch % b.update_period == 0:
-            self._balance(st)
-        else:
-            self._total(tuple(self.lam), st)
+    def _finish(self, st):
         self.losses.copy_(self._wloss[0])
         for lb in self._wloss[1:]:
             self.losses.add_(lb)
         allreduce_sum_(self.losses, self.world, self.group)
         self.losses.mul_(1.0 / self.W)  # MetricsRecord: mean over workers (trainer.cpp:517-526)
+        if self.graph:
+            self.worker.adam_step_device_state(self.params, self.grad, self.m, self.v, self.state, self.lr,
+                                               self.gamma, self.betas[0], self.betas[1], self.eps,
+                                               grad_scale=1.0 / self.W, stream=st)
+        else:
+            lr = self.lr * self.gamma ** self.epoch  # ExponentialLr::at (optim.cpp:71-73)
+            self.worker.adam_step_device(self.params, self.grad, self.m, self.v, self.t + 1, lr, self.betas[0],
+                                         self.betas[1], self.eps, grad_scale=1.0 / self.W, stream=st)
+
+    def _capture(self):
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.params.device)
+        side.wait_stream(torch.cuda.current_stream(self.params.device))
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                cs = torch.cuda.current_stream(self.params.device).cuda_stream
+                self._total(tuple(self.lam), cs)
+                self._finish(cs)
+        torch.cuda.current_stream(self.params.device).wait_stream(side)
+        self._graph, self._glam = g, tuple(self.lam)
+
+    def step(self, lambdas=None, stream=None, eager: bool = False):
+        st = stream if stream is not None else self.torch.cuda.current_stream(self.params.device).cuda_stream
+        b = self.balancing
+        if lambdas is not None:
+            self.lam = list(lambdas)
+        balance_now = b is not None and b.enabled and b.update_period > 0 and self.epoch % b.update_period == 0
+        if self.graph and not balance_now and self._warm and not eager:
+            if self._graph is None or self._glam != tuple(self.lam):
+                self._capture()  # the capture itself enqueues no work
+            self._graph.replay()
+        else:
+            if balance_now:
+                self._balance(st)
+            else:
+                self._total(tuple(self.lam), st)
+            self._finish(st)
+            self._warm = True
         self.t += 1
-        lr = self.lr * self.gamma ** self.epoch  # ExponentialLr::at (optim.cpp:71-73)
-        self.worker.adam_step_device(self.params, self.grad, self.m, self.v, self.t, lr, self.betas[0],
-                                     self.betas[1], self.eps, grad_scale=1.0 / self.W, stream=st)
         self.epoch += 1
         return self.losses
 

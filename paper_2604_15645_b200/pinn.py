@@ -309,6 +309,15 @@ class Worker:
             self.ctx, C.c_void_p(params.data_ptr()), C.c_void_p(grad.data_ptr()), C.c_void_p(m.data_ptr()),
             C.c_void_p(v.data_ptr()), params.numel(), lr, beta1, beta2, eps, t, grad_scale, st))
 
+    def adam_step_device_state(self, params, grad, m, v, state, lr0: float, gamma=1.0, beta1=0.9, beta2=0.999,
+                               eps=1e-8, grad_scale=1.0, stream=None):
+        """Adam with (steps, epoch) in the float64 device tensor `state` (graph-capturable)."""
+        st = C.c_void_p(stream) if stream is not None else None
+        self._chk(self.lib.pnx_adam_step_device_state(
+            self.ctx, C.c_void_p(params.data_ptr()), C.c_void_p(grad.data_ptr()), C.c_void_p(m.data_ptr()),
+            C.c_void_p(v.data_ptr()), params.numel(), C.c_void_p(state.data_ptr()), lr0, gamma, beta1, beta2, eps,
+            grad_scale, st))
+
     def capture_residuals(self, on: bool = True):
         self._chk(self.lib.pnx_capture_residuals(self.ctx, 1 if on else 0))
 

@@ -186,13 +186,16 @@ def test_argument_errors_match_reference_text():
         pk.shard_interior(3, 4)
 
 
+@pytest.mark.parametrize("graph", [False, True])
 @pytest.mark.parametrize("name", gi.TRAJ_NAMES)
-def test_adam_trajectory_on_device(name):
+def test_adam_trajectory_on_device(name, graph):
     """N synchronized device-Adam steps (dist.DataParallelTrainer with W local
     workers on one GPU) track the reference train() trajectory (trainer.cpp:
     419-555), including loss balancing, causality and the Poynting penalty
     where the fixture enables them: losses and lambdas per epoch within 1e-3
-    relative (FP32 drift grows with N)."""
+    relative (FP32 drift grows with N). graph=True replays one captured CUDA
+    graph per epoch (device step + Adam with its step count on the device);
+    balancing epochs run eagerly."""
     import torch
     pk = _pkg()
     from paper_2604_15645_b200.dist import DataParallelTrainer
@@ -212,7 +215,7 @@ def test_adam_trajectory_on_device(name):
         bal = pk.BalancingConfig(True, g["balancing"].alpha, g["balancing"].update_period)
     tr = DataParallelTrainer(workers, g["params"], world=1, lr=t["lr"], gamma=t["gamma"],
                              device=torch.device("cuda:0"), balancing=bal, has_bc=g["bc"] != "hard",
-                             poynting=poy is not None)
+                             poynting=poy is not None, graph=graph)
     metrics = g["metrics"]
     for ep in range(t["epochs"]):
         lm = tr.step().cpu().numpy()

@@ -275,6 +275,26 @@ int main(int argc, char** argv) {
             cfg.balancing.update_period = t.value("update_period", 100);
             cfg.balancing.alpha = t.value("alpha", 0.9);
             cfg.poynting.weight = t.value("poynting_weight", cfg.poynting.weight);
+            if (t.contains("switch")) {  // SwitchPolicy (optim.hpp:54-62) + L-BFGS phase (trainer.cpp:549-617)
+                const json& sw = t.at("switch");
+                const std::string trig = sw.value("trigger", std::string("none"));
+                cfg.switch_policy.trigger = trig == "epoch" ? SwitchPolicy::Trigger::epoch_threshold
+                                            : trig == "plateau" ? SwitchPolicy::Trigger::loss_plateau
+                                                                : SwitchPolicy::Trigger::none;
+                cfg.switch_policy.epoch_threshold = sw.value("epoch_threshold", 0L);
+                cfg.switch_policy.plateau_window = sw.value("plateau_window", 0);
+                cfg.switch_policy.plateau_rel_improvement = sw.value("plateau_rel_improvement", 0.0);
+                cfg.lbfgs_max_iters = t.value("lbfgs_max_iters", 0L);
+                if (t.contains("lbfgs")) {
+                    const json& lj = t.at("lbfgs");
+                    cfg.lbfgs.history = lj.value("history", cfg.lbfgs.history);
+                    cfg.lbfgs.c1 = lj.value("c1", cfg.lbfgs.c1);
+                    cfg.lbfgs.c2 = lj.value("c2", cfg.lbfgs.c2);
+                    cfg.lbfgs.max_line_search = lj.value("max_line_search", cfg.lbfgs.max_line_search);
+                    cfg.lbfgs.grad_tol = lj.value("grad_tol", cfg.lbfgs.grad_tol);
+                    cfg.lbfgs.curvature_floor = lj.value("curvature_floor", cfg.lbfgs.curvature_floor);
+                }
+            }
             cfg.save_every = 0;
             json hashes = json::array();
             cfg.on_sync = [&hashes](long epoch, std::span<const std::uint64_t> hs) {
@@ -288,6 +308,8 @@ int main(int argc, char** argv) {
                 ms.push_back({m.epoch, m.l_pde, m.l_ic, m.l_bc, m.lambda_pde, m.lambda_ic, m.lambda_bc, m.lr, m.wall_s});
             meta["metrics"] = ms;
             meta["aborted"] = r.aborted;
+            meta["switched_to_lbfgs"] = r.switched_to_lbfgs;
+            meta["epochs_run"] = r.epochs_run;
             meta["abort_reason"] = r.abort_reason;
             meta["hashes"] = hashes;
             write_f64(out + "/final_params.bin", flat_params(model.trainable()));

@@ -111,6 +111,15 @@ TRAJ = {
                                    collocation={"mode": "uniform", "dims": [12, 10], "n_ic": 16, "n_bc": 8},
                                    workers=2, train={"epochs": 12, "lr": 1e-2, "gamma": 1.0, "balancing": True,
                                                      "update_period": 3, "alpha": 0.9}),
+    # Adam -> L-BFGS switch at an epoch threshold, then full-batch strong-Wolfe
+    # L-BFGS over the whole interior (trainer.cpp:549-617, lbfgs.cpp)
+    "traj_burgers_lbfgs": dict(BURGERS, bc="dirichlet_zero",
+                               model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1,
+                                      "activation": "tanh"},
+                               collocation={"mode": "uniform", "dims": [12, 10], "n_ic": 16, "n_bc": 8},
+                               workers=2, train={"epochs": 40, "lr": 1e-2, "gamma": 1.0, "balancing": False,
+                                                 "switch": {"trigger": "epoch", "epoch_threshold": 5},
+                                                 "lbfgs_max_iters": 6, "lbfgs": {"history": 5}}),
     # the full Maxwell objective: causality + Poynting + two-term balancing (hard BC)
     "traj_maxwell_full": dict(MAXWELL, bc="hard",
                               model={"in_dim": 3, "hidden_dim": 16, "depth": 2, "out_dim": 3, "activation": "tanh"},
@@ -179,7 +188,8 @@ def make_traj(name, case):
     fields = case["model"]["out_dim"]
     dim = len(case["domain"])
     m = np.array([row[:8] for row in meta["metrics"]], dtype=np.float64)
-    case_meta = {"case": case, "hashes": meta["hashes"], "aborted": meta["aborted"]}
+    case_meta = {"case": case, "hashes": meta["hashes"], "aborted": meta["aborted"],
+                 "switched_to_lbfgs": meta.get("switched_to_lbfgs", False)}
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), meta=json.dumps(case_meta),
                         params=_f64(d, "params.bin"), final_params=_f64(d, "final_params.bin"),
                         metrics=m, rffB=_f64(d, "rff_B.bin"),

@@ -59,9 +59,16 @@ def load(name: str) -> dict:
     t = case.get("train", {})
     if t.get("balancing", False):
         balancing = po.Balancing(True, t.get("alpha", 0.9), t.get("update_period", 100))
+    switch = lbfgs_cfg = None
+    if "switch" in t:
+        sw = t["switch"]
+        switch = po.SwitchPolicy(sw.get("trigger", "none"), sw.get("epoch_threshold", 0), sw.get("plateau_window", 0),
+                                 sw.get("plateau_rel_improvement", 0.0))
+        lbfgs_cfg = po.LbfgsConfig(**t.get("lbfgs", {}))
     out = {"meta": meta, "case": case, "spec": spec, "res": res, "bc": bc, "col": col,
            "params": z["params"], "rffB": rffB, "causality": causality, "poynting": poynting,
-           "balancing": balancing}
+           "balancing": balancing, "switch": switch, "lbfgs_cfg": lbfgs_cfg,
+           "lbfgs_max_iters": t.get("lbfgs_max_iters", 0)}
     for k in z.files:
         if k not in out:
             out[k] = z[k]

@@ -163,6 +163,23 @@ struct PoyntingConfig {  // trainer.hpp:57-61
     std::size_t time_samples = 4;
 };
 
+struct SwitchPolicy {  // optim.hpp:54-62
+    enum class Trigger { none, epoch_threshold, loss_plateau };
+    Trigger trigger = Trigger::none;
+    long epoch_threshold = 0;
+    int plateau_window = 0;
+    double plateau_rel_improvement = 0.0;
+    bool should_switch(long epoch, std::span<const double> loss_history) const;
+};
+struct LbfgsConfig {  // lbfgs.hpp:10-17
+    int history = 50;
+    double c1 = 1e-4;
+    double c2 = 0.9;
+    int max_line_search = 25;
+    double grad_tol = 1e-10;
+    double curvature_floor = 1e-10;
+};
+
 struct TrainConfig {
     long epochs = 1000;
     std::uint64_t seed = 0;
@@ -173,6 +190,9 @@ struct TrainConfig {
     BalancingConfig balancing;
     CausalityConfig causality;
     PoyntingConfig poynting;
+    SwitchPolicy switch_policy;
+    long lbfgs_max_iters = 0;  // quasi-Newton refinement budget after the switch
+    LbfgsConfig lbfgs;
     std::array<double, 3> lambdas{1.0, 1.0, 1.0};  // initial loss weights
     int device = 0;                                 // first CUDA device; worker w uses device + w % ndev
     std::function<void(long epoch, std::span<const std::uint64_t>)> on_sync;
@@ -187,6 +207,7 @@ struct MetricsRecord {
 struct TrainResult {
     std::vector<MetricsRecord> metrics;
     long epochs_run = 0;
+    bool switched_to_lbfgs = false;
     bool aborted = false;
     std::string abort_reason;
 };

@@ -2,6 +2,8 @@
 // See host/include/pinnlab_b200.hpp for the reference file:line map.
 #include "pinnlab_b200.hpp"
 
+#include <deque>
+
 #include <cmath>
 #include <memory>
 #include <numbers>
@@ -372,6 +374,152 @@ std::array<std::vector<double>, 3> synchronized_terms(std::vector<std::unique_pt
     return avg;
 }
 
+double dot(const std::vector<double>& a, const std::vector<double>& b) {
+    double s = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+    return s;
+}
+
+// Limited-memory BFGS with a strong-Wolfe line search (lbfgs.cpp:22-155).
+class Lbfgs {
+public:
+    explicit Lbfgs(LbfgsConfig c) : cfg_(c) {}
+    struct Result {
+        double loss = 0.0;
+        bool converged = false, line_search_failed = false;
+    };
+    using Fn = std::function<double(const std::vector<double>&, std::vector<double>&)>;
+
+    std::vector<double> apply_inverse_hessian(const std::vector<double>& v) const {
+        std::vector<double> q = v;
+        std::vector<double> alpha(pairs_.size());
+        for (std::size_t i = pairs_.size(); i-- > 0;) {
+            alpha[i] = pairs_[i].rho * dot(pairs_[i].s, q);
+            for (std::size_t k = 0; k < q.size(); ++k) q[k] -= alpha[i] * pairs_[i].y[k];
+        }
+        if (!pairs_.empty()) {
+            const double sc = dot(pairs_.back().s, pairs_.back().y) / dot(pairs_.back().y, pairs_.back().y);
+            for (auto& x : q) x *= sc;
+        }
+        for (std::size_t i = 0; i < pairs_.size(); ++i) {
+            const double beta = pairs_[i].rho * dot(pairs_[i].y, q);
+            for (std::size_t k = 0; k < q.size(); ++k) q[k] += (alpha[i] - beta) * pairs_[i].s[k];
+        }
+        return q;
+    }
+
+    Result step(std::vector<double>& x, const Fn& fn) {
+        Result res;
+        std::vector<double> g(x.size());
+        double f0;
+        if (have_grad_) {
+            g = last_grad_;
+            f0 = last_loss_;
+        } else {
+            f0 = fn(x, g);
+        }
+        res.loss = f0;
+        const double gn = std::sqrt(dot(g, g));
+        if (gn < cfg_.grad_tol) {
+            res.converged = true;
+            return res;
+        }
+        std::vector<double> p = apply_inverse_hessian(g);
+        for (auto& v : p) v = -v;
+        double dphi0 = dot(g, p);
+        if (dphi0 >= 0.0) {
+            for (std::size_t k = 0; k < p.size(); ++k) p[k] = -g[k];
+            dphi0 = dot(g, p);
+            pairs_.clear();
+        }
+        int evals = 0;
+        std::vector<double> gt(x.size()), xt(x.size());
+        auto phi = [&](double a, double& d) {
+            for (std::size_t k = 0; k < x.size(); ++k) xt[k] = x[k] + a * p[k];
+            const double f = fn(xt, gt);
+            ++evals;
+            d = dot(gt, p);
+            return f;
+        };
+        const double c1 = cfg_.c1, c2 = cfg_.c2;
+        double accepted = -1.0, f_acc = 0.0;
+        double a_prev = 0.0, f_prev = f0, d_prev = dphi0;
+        double a = pairs_.empty() ? std::min(1.0, 1.0 / std::max(gn, 1e-12)) : 1.0;
+        double lo = -1.0, hi = -1.0, f_lo = 0.0, d_lo = 0.0, f_hi = 0.0;
+        bool zooming = false;
+        while (evals < cfg_.max_line_search) {
+            if (!zooming) {
+                double d;
+                const double f = phi(a, d);
+                if (f > f0 + c1 * a * dphi0 || (evals > 1 && f >= f_prev)) {
+                    lo = a_prev; f_lo = f_prev; d_lo = d_prev; hi = a; f_hi = f; zooming = true;
+                    continue;
+                }
+                if (std::abs(d) <= -c2 * dphi0) { accepted = a; f_acc = f; break; }
+                if (d >= 0.0) {
+                    lo = a; f_lo = f; d_lo = d; hi = a_prev; f_hi = f_prev; zooming = true;
+                    continue;
+                }
+                a_prev = a; f_prev = f; d_prev = d;
+                a *= 2.0;
+            } else {
+                const double dd = hi - lo, denom = f_hi - f_lo - d_lo * dd;
+                double trial = std::abs(denom) < 1e-300 ? 0.5 * (lo + hi) : lo - 0.5 * d_lo * dd * dd / denom;
+                const double span = std::abs(hi - lo);
+                if (!(trial >= std::min(lo, hi) + 0.1 * span && trial <= std::max(lo, hi) - 0.1 * span))
+                    trial = 0.5 * (lo + hi);
+                double d;
+                const double f = phi(trial, d);
+                if (f > f0 + c1 * trial * dphi0 || f >= f_lo) {
+                    hi = trial; f_hi = f;
+                } else {
+                    if (std::abs(d) <= -c2 * dphi0) { accepted = trial; f_acc = f; break; }
+                    if (d * (hi - lo) >= 0.0) { hi = lo; f_hi = f_lo; }
+                    lo = trial; f_lo = f; d_lo = d;
+                }
+                if (span < 1e-16 * std::max(1.0, std::abs(lo))) break;
+            }
+        }
+        if (accepted < 0.0) {
+            pairs_.clear();
+            have_grad_ = false;
+            res.line_search_failed = true;
+            return res;
+        }
+        Pair pr;
+        pr.s.resize(x.size());
+        pr.y.resize(x.size());
+        for (std::size_t k = 0; k < x.size(); ++k) {
+            const double xn = x[k] + accepted * p[k];
+            pr.s[k] = xn - x[k];
+            pr.y[k] = gt[k] - g[k];
+            x[k] = xn;
+        }
+        const double sy = dot(pr.s, pr.y);
+        if (sy > cfg_.curvature_floor) {
+            pr.rho = 1.0 / sy;
+            pairs_.push_back(std::move(pr));
+            while (pairs_.size() > static_cast<std::size_t>(cfg_.history)) pairs_.pop_front();
+        }
+        last_grad_ = gt;
+        last_loss_ = f_acc;
+        have_grad_ = true;
+        res.loss = f_acc;
+        return res;
+    }
+
+private:
+    struct Pair {
+        std::vector<double> s, y;
+        double rho = 0.0;
+    };
+    LbfgsConfig cfg_;
+    std::deque<Pair> pairs_;
+    std::vector<double> last_grad_;
+    double last_loss_ = 0.0;
+    bool have_grad_ = false;
+};
+
 double vec_norm(const std::vector<double>& v) {  // grad_vec_norm (trainer.cpp:283-288)
     double s = 0.0;
     for (double x : v) s += x * x;
@@ -384,6 +532,21 @@ int device_count() {
 }
 
 }  // namespace
+
+bool SwitchPolicy::should_switch(long epoch, std::span<const double> h) const {  // optim.cpp:75-95
+    switch (trigger) {
+        case Trigger::none: return false;
+        case Trigger::epoch_threshold: return epoch >= epoch_threshold;
+        case Trigger::loss_plateau: {
+            if (h.empty()) throw TensorError("switch policy: plateau trigger needs loss history");
+            if (plateau_window <= 0 || h.size() < static_cast<std::size_t>(plateau_window) + 1) return false;
+            const double past = h[h.size() - 1 - static_cast<std::size_t>(plateau_window)], now = h.back();
+            if (past <= 0.0) return true;
+            return (past - now) / past < plateau_rel_improvement;
+        }
+    }
+    return false;
+}
 
 std::vector<Tensor> data_parallel_gradient(Model& model, const TrainingProblem& prob, const TrainConfig& cfg,
                                            int workers) {
@@ -418,6 +581,9 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
     std::array<double, 3> lam = cfg.lambdas;  // LossState (losses.hpp:70-78)
     const bool has_bc = prob.bc != TrainingProblem::Bc::hard;
     const bool pen_on = cfg.poynting.weight > 0.0 && prob.residual.id == PdeId::maxwell_te;
+    std::vector<double> loss_history;
+    bool switched = false;
+    long next_epoch = 0;
     long t = 0;
     for (long epoch = 0; epoch < cfg.epochs; ++epoch) {
         std::array<double, 3> losses{};
@@ -475,11 +641,53 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
         for (auto& prm : model.trainable())
             for (auto& x : prm.value.data) x = p[at++];
         result.metrics.push_back({epoch, losses[0], losses[1], losses[2], lam[0], lam[1], lam[2], lr});
+        loss_history.push_back(lam[0] * losses[0] + lam[1] * losses[1] + lam[2] * losses[2]);
         if (cfg.on_sync) {
             std::vector<std::uint64_t> hashes(static_cast<std::size_t>(W), param_hash(model.trainable()));
             cfg.on_sync(epoch, hashes);
         }
         ++result.epochs_run;
+        if (cfg.lbfgs_max_iters > 0 && cfg.switch_policy.should_switch(epoch, loss_history)) {
+            switched = true;
+            next_epoch = epoch + 1;
+            break;
+        }
+    }
+    if (switched && !result.aborted) {  // quasi-Newton refinement, full batch (trainer.cpp:558-617)
+        result.switched_to_lbfgs = true;
+        auto full = make_worker(model, prob, data.interior, data, cfg);
+        std::array<double, 3> last{};
+        double pen = 0.0;
+        auto objective = [&](const std::vector<double>& v, std::vector<double>& grad) {
+            full->check(pnx_step(full->ctx, v.data(), lam.data(), grad.data(), last.data()));
+            double f = lam[0] * last[0] + lam[1] * last[1] + lam[2] * last[2];
+            if (pen_on) {
+                full->check(pnx_last_penalty(full->ctx, &pen));
+                f += cfg.poynting.weight * pen;
+            }
+            return f;
+        };
+        Lbfgs lb(cfg.lbfgs);
+        for (long it = 0; it < cfg.lbfgs_max_iters; ++it) {
+            Lbfgs::Result r;
+            try {
+                r = lb.step(p, objective);
+            } catch (const std::exception& e) {
+                result.aborted = true;
+                result.abort_reason = e.what();
+                break;
+            }
+            std::size_t at = 0;
+            for (auto& prm : model.trainable())
+                for (auto& x : prm.value.data) x = p[at++];
+            result.metrics.push_back({next_epoch + it, last[0], last[1], last[2], lam[0], lam[1], lam[2], 0.0});
+            ++result.epochs_run;
+            if (r.converged) break;
+            if (r.line_search_failed) {
+                result.abort_reason = "line search failed; quasi-Newton phase stopped";
+                break;
+            }
+        }
     }
     return result;
 }

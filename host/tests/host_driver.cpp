@@ -106,6 +106,12 @@ int main(int argc, char** argv) {
         cfg.poynting.weight = num("poynting_weight", 0.0);
         cfg.poynting.grid = static_cast<std::size_t>(num("poynting_grid", 32));
         cfg.poynting.time_samples = static_cast<std::size_t>(num("poynting_time_samples", 4));
+        if (num("switch_epoch", -1) >= 0) {
+            cfg.switch_policy.trigger = SwitchPolicy::Trigger::epoch_threshold;
+            cfg.switch_policy.epoch_threshold = static_cast<long>(num("switch_epoch", 0));
+        }
+        cfg.lbfgs_max_iters = static_cast<long>(num("lbfgs_max_iters", 0));
+        cfg.lbfgs.history = static_cast<int>(num("lbfgs_history", 50));
 
         if (mode == "cpu") {
             std::vector<double> p;

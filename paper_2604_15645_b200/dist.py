@@ -113,6 +113,7 @@ class DataParallelTrainer:
         self._graph = None
         self._glam = None
         self._warm = False
+        self.loss_history = []
 
     def _total(self, lam, st):
         for w, gb, lb in zip(self.workers, self._wgrad, self._wloss):
@@ -199,6 +200,13 @@ class DataParallelTrainer:
         self.t += 1
         self.epoch += 1
         return self.losses
+
+    def should_switch(self, policy) -> bool:
+        """SwitchPolicy check after a step (trainer.cpp:532-554): the history is
+        lambda . (l_pde, l_ic, l_bc) per epoch, as the reference records it."""
+        l = self.losses.tolist()
+        self.loss_history.append(self.lam[0] * l[0] + self.lam[1] * l[1] + self.lam[2] * l[2])
+        return policy.should_switch(self.epoch - 1, self.loss_history)
 
     def params_host(self) -> np.ndarray:
         return self.params.double().cpu().numpy()

@@ -217,11 +217,33 @@ def test_adam_trajectory_on_device(name, graph):
                              device=torch.device("cuda:0"), balancing=bal, has_bc=g["bc"] != "hard",
                              poynting=poy is not None, graph=graph)
     metrics = g["metrics"]
+    switched = False
+    ep = 0
     for ep in range(t["epochs"]):
         lm = tr.step().cpu().numpy()
         row = list(lm) + list(tr.lam)
         for k in range(6):  # l_pde, l_ic, l_bc, lambda_pde, lambda_ic, lambda_bc
             ref = metrics[ep, 1 + k]
             assert abs(row[k] - ref) <= 1e-3 * abs(ref) + 1e-9, (ep, k, row[k], ref)
+        if g["lbfgs_max_iters"] > 0 and g["switch"] is not None:
+            from paper_2604_15645_b200.lbfgs import SwitchPolicy
+            sw = g["switch"]
+            if tr.should_switch(SwitchPolicy(sw.trigger, sw.epoch_threshold, sw.plateau_window,
+                                             sw.plateau_rel_improvement)):
+                switched = True
+                break
     for w in workers:
         w.check()
+    if switched:  # full-batch L-BFGS over one worker with the whole interior (trainer.cpp:558-617)
+        from paper_2604_15645_b200.lbfgs import LbfgsConfig, lbfgs_refine
+        full = pk.make_worker(_spec(case), _res(case), g["bc"], g["rffB"], causality=caus, poynting=poy, **a)
+        lc = g["lbfgs_cfg"]
+        _, recs = lbfgs_refine(full, tr.params, tr.lam, g["lbfgs_max_iters"],
+                               LbfgsConfig(lc.history, lc.c1, lc.c2, lc.max_line_search, lc.grad_tol,
+                                           lc.curvature_floor),
+                               poynting_weight=poy.weight if poy is not None else 0.0)
+        assert len(recs) == metrics.shape[0] - (ep + 1)
+        for i, rec in enumerate(recs):  # FP32 objective: line-search paths may drift, 1e-2
+            for k in range(3):
+                ref = metrics[ep + 1 + i, 1 + k]
+                assert abs(rec[k] - ref) <= 1e-2 * abs(ref) + 1e-8, (i, k, rec[k], ref)

@@ -48,6 +48,9 @@ def _job(g, path, **extra):
         pj = c["poynting"]
         lines += [f"poynting_weight {pj['weight']}", f"poynting_grid {pj.get('grid', 32)}",
                   f"poynting_time_samples {pj.get('time_samples', 4)}"]
+    if t.get("switch", {}).get("trigger") == "epoch":
+        lines += [f"switch_epoch {t['switch']['epoch_threshold']}", f"lbfgs_max_iters {t.get('lbfgs_max_iters', 0)}",
+                  f"lbfgs_history {t.get('lbfgs', {}).get('history', 50)}"]
     for k, v in extra.items():
         lines.append(f"{k} {v}")
     with open(path, "w") as f:
@@ -89,4 +92,7 @@ def test_cpp_train_trajectory_on_gpu(name, tmp_path):
     m = np.fromfile(tmp_path / "metrics.bin", dtype="<f8").reshape(-1, 6)
     ref = g["metrics"][:, 1:7]  # l_pde, l_ic, l_bc, lambda_pde, lambda_ic, lambda_bc
     assert m.shape == ref.shape
-    assert np.all(np.abs(m - ref) <= 1e-3 * np.abs(ref) + 1e-9)
+    n_adam = ref.shape[0] if not g["meta"].get("switched_to_lbfgs") else int(t["switch"]["epoch_threshold"]) + 1
+    assert np.all(np.abs(m[:n_adam] - ref[:n_adam]) <= 1e-3 * np.abs(ref[:n_adam]) + 1e-9)
+    # L-BFGS rows: FP32 objective, line-search paths may drift
+    assert np.all(np.abs(m[n_adam:] - ref[n_adam:]) <= 1e-2 * np.abs(ref[n_adam:]) + 1e-8)

@@ -139,7 +139,8 @@ int launch_tc4_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
     constexpr int S = Streams<L>::S;
     const int nkb = g.K / 8;
     if (tc_make_tmap(&a.tmA, g.A, 3, g.K, g.Rpad, S, 32, 128, 1, true) ||
-        tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)nkb * 2 * Cfg::NF, 1, 8, 128, 1, false))
+        tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)nkb * 2 * Cfg::NF, 1, 8, 128, 1, false) ||
+        tc_make_tmap(&a.tmO, g.out, 3, Cfg::NF, g.Rpad, S, 32, 32, 1, true))
         return -1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.Rpad / TC_M);

@@ -150,6 +150,7 @@ struct TcGemmArgs {
     int Rpad, K, N;
     CUtensorMap tmA;    // pair kernels: A as [S][Rpad][K], box {32, 128, 1}, 128 B swizzle
     CUtensorMap tmB;    // pair kernels: weight image as rows of 8 fp32, box {8, 128}
+    CUtensorMap tmO;    // forward pair kernel: out as [S][Rpad][N], box {32, 32, 1}, 128 B swizzle
 };
 
 // ---------------------------------------------------------------------------
@@ -562,8 +563,8 @@ struct Tc4FwdCfg {
     static constexpr int NBOX = SECOND ? 3 : 2;
     static constexpr int RAW = NBOX * BOX;
     static constexpr int NR = 2;
-    static constexpr int EPI_ROW = 144;
-    static constexpr int EPI_BYTES = 8 * 32 * EPI_ROW;
+    static constexpr int EPI_TILE = 32 * 128;       // 32 rows x 32 fp32, 128 B swizzled (TMA store box)
+    static constexpr int EPI_BYTES = 8 * 2 * EPI_TILE;  // 8 warps x 2 buffers
     static constexpr int BUDGET = 226 * 1024;
     static constexpr int NST0 = (BUDGET - NR * RAW - EPI_BYTES) / STAGE;
     static constexpr int NST = NST0 > 8 ? 8 : NST0;
@@ -587,7 +588,6 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
     const uint32_t rank = tc::cluster_ctarank();
     const int r0 = (blockIdx.x >> 1) * 256 + (int)rank * 128;
     const int nkb = g.K / 8, ngrp = g.K / 32;
-    const int64_t RN = (int64_t)g.Rpad * NF;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             tc::mbar_init(&full[i], 17);  // 2 x 8 converter warps + the leader's expect_tx
@@ -700,9 +700,14 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
         __syncwarp();
     } else {
         // ---------------- MMA issue (leader, warp 9 lane 0) + epilogue ----------------
+        // Epilogue: TMEM -> registers -> 128 B-swizzled staging tile (row r, 16 B chunk c
+        // at r*128 + ((c ^ r%8) << 4): conflict-free) -> one TMA tensor store per
+        // 32 x 32 block; TMEM is released as soon as it is read, the stores drain
+        // asynchronously (double-buffered staging, bulk_wait_read before reuse).
         const int q = warp & 3, half = (warp - 9) >> 2;
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-        const uint32_t stg = sepi + (uint32_t)(warp - 9) * 32 * Cfg::EPI_ROW;
+        const uint32_t stg0 = sepi + (uint32_t)(warp - 9) * 2 * Cfg::EPI_TILE;
+        int nst = 0;  // stores issued by this warp (buffer = nst & 1)
         for (int p = 0; p < S; ++p) {
             if (warp == 9 && lane == 0 && rank == 0) {
                 constexpr uint32_t idesc = tc::make_idesc_tf32(2 * TC_M, NF, 0, 0);
@@ -740,30 +745,36 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                 tc::tmem_ld16(tl + (uint32_t)(NF + c), b);
                 tc::tmem_ld16(tl + (uint32_t)(NF + c + 16), b + 16);
                 tc::tmem_ld_wait();
+                if (c + 32 >= (half + 1) * (NF / 2)) {  // last TMEM read of this pass: release it
+                    tc::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive_cluster(tempty0);
+                }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) a[j] += b[j];
                 if (p == 0) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));
                 }
-#pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    sts128(stg + lane * Cfg::EPI_ROW + j * 4, make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]));
+                const uint32_t stg = stg0 + (uint32_t)(nst & 1) * Cfg::EPI_TILE;
+                if (lane == 0) tc::bulk_wait_read<1>();  // the store that last used this buffer has read it
                 __syncwarp();
-                float* dst = g.out + p * RN + (int64_t)(r0 + q * 32) * NF + c;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int rr = 4 * k + (lane >> 3), cc = (lane & 7) * 4;
-                    const float4 v = lds128(stg + rr * Cfg::EPI_ROW + cc * 4);
-                    *reinterpret_cast<float4*>(dst + (int64_t)rr * NF + cc) = v;
+                for (int j = 0; j < 8; ++j)
+                    sts128(stg + lane * 128 + (((uint32_t)j ^ (uint32_t)(lane & 7)) << 4),
+                           make_float4(a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]));
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tc::tma_store_3d(&g.tmO, c, r0 + q * 32, p, stg);
+                    tc::bulk_commit();
                 }
-                __syncwarp();
+                ++nst;
             }
-            tc::tc_fence_before();
-            __syncwarp();
             if (warp == 9 && lane == 0) TC_ACC(3);
-            if (lane == 0) tc::mbar_arrive_cluster(tempty0);
         }
+        if (lane == 0) tc::bulk_wait<0>();
+        __syncwarp();
     }
     tc::tc_fence_before();
     tc::cluster_sync();

@@ -295,7 +295,9 @@ int main(int argc, char** argv) {
                     cfg.lbfgs.curvature_floor = lj.value("curvature_floor", cfg.lbfgs.curvature_floor);
                 }
             }
-            cfg.save_every = 0;
+            cfg.save_every = t.value("save_every", 0L);
+            cfg.run_dir = t.value("run_dir", std::string());        // train() writes final.ckpt there
+            cfg.resume_from = t.value("resume_from", std::string());  // PLABCK01 checkpoint to resume
             json hashes = json::array();
             cfg.on_sync = [&hashes](long epoch, std::span<const std::uint64_t> hs) {
                 json row = json::array();
@@ -313,6 +315,22 @@ int main(int argc, char** argv) {
             meta["abort_reason"] = r.abort_reason;
             meta["hashes"] = hashes;
             write_f64(out + "/final_params.bin", flat_params(model.trainable()));
+        } else if (mode == "ckpt_info") {
+            // Checkpoint::load (checkpoint.cpp:142-170) of job["ckpt"]: header + payload
+            Checkpoint ck = Checkpoint::load(job.at("ckpt").get<std::string>());
+            json tl = json::array();
+            std::vector<double> all;
+            for (const auto& t : ck.tensors) {
+                tl.push_back({{"name", t.name}, {"shape", t.value.shape()}});
+                all.insert(all.end(), t.value.data(), t.value.data() + t.value.size());
+            }
+            meta["ckpt_tensors"] = tl;
+            meta["ckpt_scalars"] = ck.scalars;
+            meta["ckpt_seed"] = ck.seed;
+            meta["ckpt_model"] = json::parse(model_spec_to_json(ck.spec));
+            write_f64(out + "/ckpt_data.bin", all);
+            Model m2 = ck.restore_model();  // throws on a missing / misshapen trainable tensor
+            write_f64(out + "/restored_params.bin", flat_params(m2.trainable()));
         } else {
             throw std::runtime_error("unknown mode " + mode);
         }

@@ -199,6 +199,37 @@ def make_traj(name, case):
                         bc_a=_points(_f64(d, "bc_a.bin"), dim), bc_b=_points(_f64(d, "bc_b.bin"), dim))
 
 
+CKPT = {
+    # train() writes final.ckpt (PLABCK01, checkpoint.cpp:121-140) after 8 epochs;
+    # a second run resumes from it (trainer.cpp:345-353) for 6 more epochs
+    "ckpt_burgers": dict(BURGERS, bc="dirichlet_zero",
+                         model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1, "activation": "tanh"},
+                         collocation={"mode": "uniform", "dims": [12, 10], "n_ic": 16, "n_bc": 8},
+                         workers=2, train={"epochs": 8, "lr": 1e-2, "gamma": 0.98, "balancing": True,
+                                           "update_period": 3, "alpha": 0.9}),
+}
+
+
+def make_ckpt(name, case):
+    run = tempfile.mkdtemp(prefix="ckpt_")
+    meta, d = _run(dict(case, mode="train", train=dict(case["train"], run_dir=run)))
+    ck = os.path.join(run, "final.ckpt")
+    raw = np.fromfile(ck, dtype=np.uint8)
+    info, di = _run(dict(case, mode="ckpt_info", ckpt=ck))
+    t2 = dict(case["train"], epochs=case["train"]["epochs"] + 6, resume_from=ck)
+    meta2, d2 = _run(dict(case, mode="train", train=t2))
+    m2 = np.array([row[:8] for row in meta2["metrics"]], dtype=np.float64)
+    case_meta = {"case": case, "ckpt_tensors": info["ckpt_tensors"], "ckpt_scalars": info["ckpt_scalars"]}
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), meta=json.dumps(case_meta), ckpt=raw,
+                        params=_f64(d, "params.bin"), final_params=_f64(d, "final_params.bin"),
+                        ckpt_data=_f64(di, "ckpt_data.bin"), resume_metrics=m2,
+                        resume_final_params=_f64(d2, "final_params.bin"), rffB=_f64(d, "rff_B.bin"),
+                        interior=_points(_f64(d, "interior.bin"), 2),
+                        ic_points=_points(_f64(d, "ic_points.bin"), 2),
+                        ic_targets=_f64(d, "ic_targets.bin").reshape(1, -1).T.copy(),
+                        bc_a=_points(_f64(d, "bc_a.bin"), 2), bc_b=_points(_f64(d, "bc_b.bin"), 2))
+
+
 def main():
     if not os.path.exists(DRIVER):
         sys.exit(f"{DRIVER} missing: run `make -C oracle` (needs /root/reference)")
@@ -212,6 +243,11 @@ def main():
         if only and n not in only:
             continue
         make_traj(n, c)
+        print("wrote", n)
+    for n, c in CKPT.items():
+        if only and n not in only:
+            continue
+        make_ckpt(n, c)
         print("wrote", n)
 
 

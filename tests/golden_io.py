@@ -75,5 +75,7 @@ def load(name: str) -> dict:
     return out
 
 
-CASE_NAMES = sorted(n[:-4] for n in os.listdir(GOLDEN) if n.endswith(".npz") and not n.startswith("traj_"))
+CASE_NAMES = sorted(n[:-4] for n in os.listdir(GOLDEN)
+                    if n.endswith(".npz") and not n.startswith(("traj_", "ckpt_")))
+CKPT_NAMES = sorted(n[:-4] for n in os.listdir(GOLDEN) if n.startswith("ckpt_") and n.endswith(".npz"))
 TRAJ_NAMES = sorted(n[:-4] for n in os.listdir(GOLDEN) if n.startswith("traj_") and n.endswith(".npz"))

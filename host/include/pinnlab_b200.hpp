@@ -8,7 +8,7 @@
 //   ResidualSpec / PdeId                              losses.hpp:14-30
 //   Domain, linspace, sample_uniform                  sampling.hpp:13-36
 //   TrainingProblem, CollocationConfig, TrainConfig   trainer.hpp:17-86
-//   build_collocation (uniform mode)                  trainer.cpp:47-128
+//   build_collocation (uniform / LHS modes)           trainer.cpp:47-128
 //   data_parallel_gradient                            trainer.hpp:118-119
 //   train (Adam phase: balancing, causality, Poynting) trainer.cpp:332-555
 //   param_hash                                        trainer.cpp:22-35
@@ -116,6 +116,9 @@ struct Domain {
 
 std::vector<double> linspace(double lo, double hi, std::size_t n);
 Points sample_uniform(const Domain& dom, std::span<const std::size_t> dims);
+// Latin hypercube designs with the reference's mt19937_64 stream (sampling.cpp:55-103)
+Points sample_lhs(const Domain& dom, std::size_t n, std::uint64_t seed);
+Points sample_lhs_per_axis(const Domain& dom, std::span<const std::size_t> dims, std::uint64_t seed);
 
 struct TrainingProblem {
     ResidualSpec residual;
@@ -125,10 +128,14 @@ struct TrainingProblem {
     Bc bc = Bc::hard;
 };
 
-struct CollocationConfig {
-    std::vector<std::size_t> dims;  // uniform grid
+struct CollocationConfig {  // trainer.hpp:31-43
+    enum class Mode { uniform, lhs, lhs_per_axis };
+    Mode mode = Mode::uniform;
+    std::vector<std::size_t> dims;  // per-axis counts (uniform / per-axis LHS)
+    std::size_t n = 0;              // point count for joint LHS
     std::size_t n_ic = 128;
     std::size_t n_bc = 64;
+    int resample_every = 0;         // LHS modes: fresh interior every k epochs (seed + epoch)
 };
 
 struct CollocationData {

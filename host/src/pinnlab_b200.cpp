@@ -3,6 +3,8 @@
 #include "pinnlab_b200.hpp"
 
 #include <deque>
+#include <algorithm>
+#include <numeric>
 
 #include <cmath>
 #include <memory>
@@ -131,12 +133,63 @@ Points sample_uniform(const Domain& dom, std::span<const std::size_t> dims) {
     return pts;
 }
 
-CollocationData build_collocation(const TrainingProblem& prob, const CollocationConfig& cc, std::uint64_t) {
+Points sample_lhs(const Domain& dom, std::size_t n, std::uint64_t seed) {
+    if (n == 0) throw TensorError("sample_lhs: n must be positive");
+    std::mt19937_64 eng(seed);
+    Points pts;
+    pts.coords.assign(dom.dim(), std::vector<double>(n));
+    std::vector<std::size_t> perm(n);
+    for (std::size_t a = 0; a < dom.dim(); ++a) {
+        std::iota(perm.begin(), perm.end(), 0);
+        std::shuffle(perm.begin(), perm.end(), eng);
+        const double lo = dom.bounds[a][0], hi = dom.bounds[a][1];
+        const double h = (hi - lo) / static_cast<double>(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            const double jitter = std::uniform_real_distribution<double>(0.0, 1.0)(eng);
+            pts.coords[a][i] = lo + (static_cast<double>(perm[i]) + jitter) * h;
+        }
+    }
+    return pts;
+}
+
+Points sample_lhs_per_axis(const Domain& dom, std::span<const std::size_t> dims, std::uint64_t seed) {
+    if (dims.size() != dom.dim()) throw TensorError("sample_lhs_per_axis: dims/domain mismatch");
+    std::mt19937_64 eng(seed);
+    std::vector<std::vector<double>> axes(dom.dim());
+    std::size_t total = 1;
+    for (std::size_t a = 0; a < dom.dim(); ++a) {
+        const double lo = dom.bounds[a][0], hi = dom.bounds[a][1];
+        const std::size_t n = dims[a];
+        if (n == 0) throw TensorError("sample_lhs_per_axis: zero points on an axis");
+        const double h = (hi - lo) / static_cast<double>(n);
+        axes[a].resize(n);
+        for (std::size_t i = 0; i < n; ++i)
+            axes[a][i] = lo + (static_cast<double>(i) + std::uniform_real_distribution<double>(0.0, 1.0)(eng)) * h;
+        total *= n;
+    }
+    Points pts;
+    pts.coords.assign(dom.dim(), std::vector<double>(total));
+    for (std::size_t idx = 0; idx < total; ++idx) {  // last axis fastest
+        std::size_t rem = idx;
+        for (std::size_t a = dom.dim(); a-- > 0;) {
+            const std::size_t k = rem % dims[a];
+            rem /= dims[a];
+            pts.coords[a][idx] = axes[a][k];
+        }
+    }
+    return pts;
+}
+
+CollocationData build_collocation(const TrainingProblem& prob, const CollocationConfig& cc, std::uint64_t seed) {
     const Domain& dom = prob.domain;
     const std::size_t d = dom.dim();
     if (d < 2) throw TensorError("build_collocation: need at least one spatial axis plus time");
     CollocationData data;
-    data.interior = sample_uniform(dom, cc.dims);
+    switch (cc.mode) {
+        case CollocationConfig::Mode::uniform: data.interior = sample_uniform(dom, cc.dims); break;
+        case CollocationConfig::Mode::lhs: data.interior = sample_lhs(dom, cc.n, seed); break;
+        case CollocationConfig::Mode::lhs_per_axis: data.interior = sample_lhs_per_axis(dom, cc.dims, seed); break;
+    }
     const std::size_t spatial = d - 1;
     Points ic;
     if (spatial == 1) {
@@ -586,6 +639,20 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
     long next_epoch = 0;
     long t = 0;
     for (long epoch = 0; epoch < cfg.epochs; ++epoch) {
+        // optional interior resampling (trainer.cpp:421-434): fresh LHS set with seed + epoch
+        if (cfg.collocation.resample_every > 0 && epoch > 0 && epoch % cfg.collocation.resample_every == 0 &&
+            cfg.collocation.mode != CollocationConfig::Mode::uniform) {
+            CollocationData rd = build_collocation(prob, cfg.collocation, cfg.seed + static_cast<std::uint64_t>(epoch));
+            data.interior = std::move(rd.interior);
+            shards = shard_interior(data.interior, W);
+            for (int w = 0; w < W; ++w) {
+                auto pts = axis_major(shards[static_cast<std::size_t>(w)]);
+                ctxs[static_cast<std::size_t>(w)]->check(
+                    pnx_set_points(ctxs[static_cast<std::size_t>(w)]->ctx, pts.data(),
+                                   static_cast<int64_t>(shards[static_cast<std::size_t>(w)].count()),
+                                   static_cast<int32_t>(shards[static_cast<std::size_t>(w)].coords.size())));
+            }
+        }
         std::array<double, 3> losses{};
         std::vector<double> g;
         const bool balance_now = cfg.balancing.enabled && cfg.balancing.update_period > 0 &&

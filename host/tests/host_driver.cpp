@@ -94,6 +94,15 @@ int main(int argc, char** argv) {
                                           : TrainingProblem::Bc::hard;
         TrainConfig cfg;
         for (const auto& d : kv["dims"]) cfg.collocation.dims.push_back(std::stoul(d));
+        if (kv.count("colloc_mode")) {
+            const std::string cm = kv["colloc_mode"][0];
+            cfg.collocation.mode = cm == "lhs" ? CollocationConfig::Mode::lhs
+                                   : cm == "lhs_per_axis" ? CollocationConfig::Mode::lhs_per_axis
+                                                          : CollocationConfig::Mode::uniform;
+        }
+        cfg.collocation.n = static_cast<std::size_t>(num("colloc_n", 0));
+        cfg.collocation.resample_every = static_cast<int>(num("resample_every", 0));
+        cfg.seed = static_cast<std::uint64_t>(num("colloc_seed", 0));
         cfg.collocation.n_ic = static_cast<std::size_t>(num("n_ic", 128));
         cfg.collocation.n_bc = static_cast<std::size_t>(num("n_bc", 64));
         const int workers = static_cast<int>(num("workers", 1));
@@ -118,7 +127,7 @@ int main(int argc, char** argv) {
             for (const auto& t : model.trainable()) p.insert(p.end(), t.value.data.begin(), t.value.data.end());
             write_f64(out + "/params.bin", p);
             write_f64(out + "/rffB.bin", model.rff_matrix().data);
-            CollocationData data = build_collocation(prob, cfg.collocation, 0);
+            CollocationData data = build_collocation(prob, cfg.collocation, cfg.seed);
             std::vector<double> pts;
             for (const auto& c : data.interior.coords) pts.insert(pts.end(), c.begin(), c.end());
             write_f64(out + "/interior.bin", pts);

@@ -79,6 +79,16 @@ CASES = {
                             model={"in_dim": 2, "hidden_dim": 16, "depth": 3, "out_dim": 1, "activation": "tanh"},
                             collocation={"mode": "uniform", "dims": [9, 7], "n_ic": 10, "n_bc": 6},
                             workers=[1]),
+    # Latin hypercube interiors (sampling.cpp:55-103) with the reference's mt19937_64 stream
+    "burgers_lhs": dict(BURGERS, bc="dirichlet_zero", colloc_seed=5,
+                        model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1, "activation": "tanh"},
+                        collocation={"mode": "lhs", "n": 97, "n_ic": 16, "n_bc": 8},
+                        workers=[1, 2]),
+    "maxwell_lhs_per_axis": dict(MAXWELL, bc="hard", colloc_seed=11,
+                                 model={"in_dim": 3, "hidden_dim": 12, "depth": 2, "out_dim": 3,
+                                        "activation": "tanh"},
+                                 collocation={"mode": "lhs_per_axis", "dims": [5, 4, 3], "n_ic": 16},
+                                 workers=[1]),
     # Maxwell with the Poynting energy penalty (losses.cpp:187-223, trainer.cpp:240-247)
     "maxwell_poynting": dict(MAXWELL, bc="hard",
                              model={"in_dim": 3, "hidden_dim": 16, "depth": 2, "out_dim": 3, "activation": "tanh"},
@@ -111,6 +121,13 @@ TRAJ = {
                                    collocation={"mode": "uniform", "dims": [12, 10], "n_ic": 16, "n_bc": 8},
                                    workers=2, train={"epochs": 12, "lr": 1e-2, "gamma": 1.0, "balancing": True,
                                                      "update_period": 3, "alpha": 0.9}),
+    # LHS interior resampled every 3 epochs with seed + epoch (trainer.cpp:421-434)
+    "traj_burgers_lhs_resample": dict(BURGERS, bc="dirichlet_zero", colloc_seed=3,
+                                      model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1,
+                                             "activation": "tanh"},
+                                      collocation={"mode": "lhs", "n": 120, "n_ic": 16, "n_bc": 8,
+                                                   "resample_every": 3},
+                                      workers=2, train={"epochs": 9, "lr": 1e-2, "gamma": 1.0, "balancing": False}),
     # Adam -> L-BFGS switch at an epoch threshold, then full-batch strong-Wolfe
     # L-BFGS over the whole interior (trainer.cpp:549-617, lbfgs.cpp)
     "traj_burgers_lbfgs": dict(BURGERS, bc="dirichlet_zero",

@@ -202,6 +202,8 @@ def test_adam_trajectory_on_device(name, graph):
     g = gi.load(name)
     case = g["case"]
     t = case["train"]
+    if case["collocation"].get("resample_every", 0):
+        pytest.skip("interior resampling (LHS stream) runs in the C++ host mirror (test_host_cpp)")
     W = case["workers"]
     a = _col_args(g)
     caus, poy = _objective(g)

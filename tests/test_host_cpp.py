@@ -29,7 +29,7 @@ def _job(g, path, **extra):
              f"pde {c['pde']['id']}", f"advection_c {c['pde'].get('advection_c', 1.0)}",
              f"epsilon {c['pde'].get('epsilon', 1.0)}", f"mu {c['pde'].get('mu', 1.0)}",
              "domain " + " ".join(f"{a} {b}" for a, b in c["domain"]), f"initial {c['initial']}",
-             f"bc {c.get('bc', 'hard')}", "dims " + " ".join(str(d) for d in c["collocation"]["dims"]),
+             f"bc {c.get('bc', 'hard')}", "dims " + " ".join(str(d) for d in c["collocation"].get("dims", [])),
              f"n_ic {c['collocation'].get('n_ic', 128)}", f"n_bc {c['collocation'].get('n_bc', 64)}", "seed 0"]
     if m.get("periodic_axes"):
         lines.append("periodic " + " ".join(f"{int(a['periodic'])} {a['period']} {int(a.get('trainable', False))}"
@@ -38,6 +38,12 @@ def _job(g, path, **extra):
         lines.append(f"rff {m['rff']['width']} {m['rff'].get('sigma', 10.0)} {m['rff'].get('mean', 0.0)}")
     if "rwf" in m:
         lines.append(f"rwf {m['rwf'].get('mean', 1.0)} {m['rwf'].get('stddev', 0.1)}")
+    cc = c["collocation"]
+    if cc.get("mode", "uniform") != "uniform":
+        lines += [f"colloc_mode {cc['mode']}", f"colloc_n {cc.get('n', 0)}"]
+    if cc.get("resample_every", 0):
+        lines.append(f"resample_every {cc['resample_every']}")
+    lines.append(f"colloc_seed {c.get('colloc_seed', 0)}")
     t = c.get("train", {})
     if t.get("balancing"):
         lines += ["balancing 1", f"alpha {t.get('alpha', 0.9)}", f"update_period {t.get('update_period', 100)}"]

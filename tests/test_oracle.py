@@ -39,6 +39,8 @@ def test_collocation_matches_reference(name):
     g = gi.load(name)
     c = g["case"]
     cc = c["collocation"]
+    if cc.get("mode", "uniform") != "uniform":
+        pytest.skip("LHS designs are pinned bit-exactly through the C++ host (tests/test_host_cpp.py)")
     col = po.build_collocation(c["domain"], cc["dims"], cc.get("n_ic", 128), cc.get("n_bc", 64), g["bc"],
                                c["initial"], g["spec"].out_dim)
     np.testing.assert_array_equal(col.interior, g["col"].interior)
@@ -61,6 +63,8 @@ def test_param_layout_matches_reference(name):
 def test_adam_trajectory_matches_reference(name):
     g = gi.load(name)
     t = g["case"]["train"]
+    if g["case"]["collocation"].get("resample_every", 0):
+        pytest.skip("interior resampling (LHS stream) runs in the C++ host mirror")
     p, hist = po.train(g["spec"], g["params"], g["rffB"], g["res"], g["col"], g["bc"], t["epochs"], lr=t["lr"],
                        gamma=t["gamma"], workers=g["case"]["workers"], balancing=g["balancing"],
                        causality=g["causality"], poynting=g["poynting"], switch=g["switch"],

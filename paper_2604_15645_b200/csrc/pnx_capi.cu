@@ -584,8 +584,15 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 const int ntl = (int)((Rpad + wr - 1) / wr);
                 if (launch_tc2_wgrad(L, pro, tw, ntl, wr, st)) return fail(ctx, PNX_ERR_CUDA, "tc wgrad launch");
                 CKL();
-                k_tc_wreduce<<<296, 256, 0, st>>>(ctx->tc.wpart, ctx->tc.dbpart, ntl, t.K[l], t.N[l],
-                                                  ctx->d_part[l]);
+                {
+                    const int64_t len = (int64_t)t.K[l] * t.N[l] + t.N[l];
+                    const unsigned gx = (unsigned)std::min<int64_t>((len / 4 + 255) / 256, 1024);
+                    k_tc_wreduce1<<<dim3(gx, TC_WRED_G), 256, 0, st>>>(ctx->tc.wpart, ctx->tc.dbpart, ntl, t.K[l],
+                                                                       t.N[l], ctx->tc.red);
+                    CKL();
+                    k_tc_wreduce2<<<(unsigned)std::min<int64_t>((len + 255) / 256, 1024), 256, 0, st>>>(
+                        ctx->tc.red, len, ctx->d_part[l]);
+                }
                 CKL();
             } else {
                 launch_wgrad(L, pro, w, ctx->nsplit[l], st);

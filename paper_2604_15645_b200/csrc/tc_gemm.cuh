@@ -40,6 +40,8 @@ struct TcWorkspace {
     int64_t wpart_cap = 0;
     double* dbpart = nullptr;      // [n_wtiles][N]
     int64_t dbpart_cap = 0;
+    double* red = nullptr;         // [TC_WRED_G][K*N + N] first-level reduction
+    int64_t red_cap = 0;
     bool attrs_set = false;
 };
 
@@ -180,20 +182,66 @@ inline int tc_make_tmap_3d(CUtensorMap* map, const float* base, uint64_t d0, uin
     return tc_make_tmap(map, base, 3, d0, d1, d2, b0, b1, b2, false);
 }
 
-// part[k*N + n] += sum_t wpart[t][k][n] ; part[K*N + n] += sum_t dbpart[t][n]  (FP64, fixed order)
-static __global__ void k_tc_wreduce(const float* __restrict__ wpart, const double* __restrict__ dbpart, int ntiles,
-                                    int K, int N, double* __restrict__ part) {
-    const int64_t KN = (int64_t)K * N;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < KN + N; i += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        if (i < KN) {
-            for (int t = 0; t < ntiles; ++t) s += (double)wpart[(int64_t)t * KN + i];
+// Two-level fixed-order reduction of the weight-gradient tile partials:
+//   level 1: group y sums tiles [y*T/G, (y+1)*T/G) in order (float4 loads, FP64)
+//   level 2: part[i] += sum_y red[y][i] in y order
+// (deterministic for a given tile count; replaces the one-pass k_tc_wreduce).
+constexpr int TC_WRED_G = 16;
+static __global__ void k_tc_wreduce1(const float* __restrict__ wpart, const double* __restrict__ dbpart, int ntiles,
+                                     int K, int N, double* __restrict__ red) {
+    const int64_t KN = (int64_t)K * N, len = KN + N;
+    const int y = blockIdx.y;
+    const int t0 = (int)((int64_t)ntiles * y / TC_WRED_G), t1 = (int)((int64_t)ntiles * (y + 1) / TC_WRED_G);
+    for (int64_t i4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i4 * 4 < len;
+         i4 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i4 * 4;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (i < KN) {  // KN is a multiple of 4 (N % 4 == 0)
+            int t = t0;
+            for (; t + 4 <= t1; t += 4) {
+                float4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(wpart + (int64_t)(t + u) * KN + i));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    s0 += (double)v[u].x;
+                    s1 += (double)v[u].y;
+                    s2 += (double)v[u].z;
+                    s3 += (double)v[u].w;
+                }
+            }
+            for (; t < t1; ++t) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(wpart + (int64_t)t * KN + i));
+                s0 += (double)v.x;
+                s1 += (double)v.y;
+                s2 += (double)v.z;
+                s3 += (double)v.w;
+            }
         } else {
-            for (int t = 0; t < ntiles; ++t) s += dbpart[(int64_t)t * N + (i - KN)];
+            for (int t = t0; t < t1; ++t) {
+                const double* d = dbpart + (int64_t)t * N + (i - KN);
+                s0 += d[0];
+                s1 += d[1];
+                s2 += d[2];
+                s3 += d[3];
+            }
         }
+        double* r = red + (int64_t)y * len + i;
+        r[0] = s0;
+        r[1] = s1;
+        r[2] = s2;
+        r[3] = s3;
+    }
+}
+static __global__ void k_tc_wreduce2(const double* __restrict__ red, int64_t len, double* __restrict__ part) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+#pragma unroll
+        for (int y = 0; y < TC_WRED_G; ++y) s += red[(int64_t)y * len + i];
         part[i] += s;
     }
 }
+
 
 // ---------------------------------------------------------------------------
 // Rows per weight-gradient CTA: larger tiles amortise the per-CTA prologue and
@@ -233,6 +281,15 @@ inline bool tc_enabled(int engine, int H, int S, int act) {
 }
 
 inline int tc_workspace_alloc(TcWorkspace& ws, int, int64_t Rpad, int H, int K0) {
+    {
+        const int64_t kmax0 = H > K0 ? H : K0;
+        const int64_t need_red = (int64_t)TC_WRED_G * (kmax0 * H + H);
+        if (need_red > ws.red_cap) {
+            if (ws.red) cudaFree(ws.red);
+            if (cudaMalloc(&ws.red, need_red * sizeof(double)) != cudaSuccess) return -2;
+            ws.red_cap = need_red;
+        }
+    }
     const int64_t tiles = (Rpad + TC_WROWS - 1) / TC_WROWS;
     const int64_t kmax = H > K0 ? H : K0;
     const int64_t need = tiles * kmax * H;
@@ -249,6 +306,7 @@ inline int tc_workspace_alloc(TcWorkspace& ws, int, int64_t Rpad, int H, int K0)
     return 0;
 }
 inline void tc_workspace_free(TcWorkspace& ws) {
+    if (ws.red) cudaFree(ws.red);
     if (ws.img) cudaFree(ws.img);
     if (ws.wpart) cudaFree(ws.wpart);
     if (ws.dbpart) cudaFree(ws.dbpart);

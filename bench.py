@@ -44,7 +44,8 @@ def _args():
     ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc3xtf32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of CUDA-graph replays")
+    ap.add_argument("--graph", action="store_true",
+                    help="time CUDA-graph replays (class timings then come from a separate eager pass)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     return ap.parse_args()
 
@@ -277,7 +278,7 @@ def main():
     P = worker.n_params
     from paper_2604_15645_b200.dist import DataParallelTrainer
     # one CUDA graph per step on a single GPU (the multi-GPU step keeps NCCL eager)
-    trainer = DataParallelTrainer(worker, flat, world=world, lr=1e-3, device=dev, graph=not args.no_graph)
+    trainer = DataParallelTrainer(worker, flat, world=world, lr=1e-3, device=dev, graph=args.graph)
     stream = torch.cuda.current_stream(dev)
     st = stream.cuda_stream
     lam = (1.0, 1.0, 1.0)
@@ -293,16 +294,19 @@ def main():
     torch.cuda.synchronize(dev)
     launches_per_step = worker.launch_count() + (2 if trainer.graph else 1)  # + Adam (+ its counter tick)
 
-    # ---- per-class device time: CUDA events on the launching stream (eager pass) ----
-    worker.profile(True)
-    for _ in range(args.steps):
-        step(eager=True)
-    torch.cuda.synchronize(dev)
-    prof = worker.profile_read()
-    worker.profile(False)
+    if trainer.graph:  # per-class device time from an eager pass (graph replays carry no class events)
+        worker.profile(True)
+        for _ in range(args.steps):
+            step(eager=True)
+        torch.cuda.synchronize(dev)
+        prof = worker.profile_read()
+        worker.profile(False)
 
-    # ---- timed region (device-resident inputs; graph replays when single-GPU) ----
+    # ---- timed region (device-resident inputs); class times by CUDA events on the
+    # launching stream inside it unless graph replays are timed ----
     clk = ClockSampler(local)
+    if not trainer.graph:
+        worker.profile(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -317,6 +321,9 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
+    if not trainer.graph:
+        prof = worker.profile_read()
+        worker.profile(False)
     worker.check()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)

@@ -300,7 +300,7 @@ int upload_rows(pnx_ctx* ctx) {
     for (int l = 0; l < L - 1; ++l) {
         const int tiles = (int)(((ctx->tab.N[l] + 63) / 64) * ((ctx->tab.K[l] + 63) / 64));
         int ns = std::max(1, std::min(256, (4 * 148 + tiles - 1) / tiles));
-        ns = (int)std::min<int64_t>(ns, std::max<int64_t>(1, ch / 256));
+        ns = (int)std::min<int64_t>(ns, std::max<int64_t>(1, ch / 64));  // >= 64 rows per split
         if (l == 0 && layer0_fused(ctx)) ns = kL0Blocks;
         ctx->nsplit[l] = ns;
         if (int r = dalloc(ctx, &ctx->d_part[l], (size_t)ns * (ctx->tab.K[l] * (size_t)ctx->tab.N[l] + ctx->tab.N[l]))) return r;

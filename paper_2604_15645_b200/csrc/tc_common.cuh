@@ -10,6 +10,7 @@
 //            32 at LBO, k groups of 8 at SBO.
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -246,6 +247,45 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
             smem_u32(bar)),
         "h"(mask)
         : "memory");
+}
+
+// ---- kind::f16 (fp16 operands, FP32 accumulate) ------------------------------
+// Instruction descriptor: like make_idesc_tf32 with a/b format F16 (0).
+__host__ __device__ constexpr uint32_t make_idesc_f16(int M, int N, int a_mn_major, int b_mn_major) {
+    return (1u << 4) | ((uint32_t)a_mn_major << 15) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// MN-major SWIZZLE_128B tile of 16-bit elements: 64 MN elements (128 B) per
+// k-row, 8 k-rows per 1024 B atom, 16 B chunks XOR k-row; atoms ordered
+// [k/8][mn/64]: LBO = 1024 (next 64 MN), SBO = (mn_extent/64)*1024 (next 8 k).
+__host__ __device__ __forceinline__ uint32_t mn16_off(uint32_t k, uint32_t mn, uint32_t mn_extent) {
+    return (k >> 3) * (mn_extent / 64u) * 1024u + (mn >> 6) * 1024u + (k & 7u) * 128u +
+           ((((mn & 63u) >> 3) ^ (k & 7u)) << 4) + (mn & 7u) * 2u;
+}
+// power-of-two scale that puts |x| <= amax into [2^13, 2^14) (fp16 max 65504)
+__device__ __forceinline__ int f16_scale_exp(float amax) {
+    if (!(amax > 0.0f) || !isfinite(amax)) return 0;
+    return 13 - ilogbf(amax);
+}
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
 }
 
 // ---- 3xTF32 split -------------------------------------------------------------

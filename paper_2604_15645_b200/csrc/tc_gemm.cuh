@@ -165,6 +165,10 @@ struct TcGemmArgs {
 struct TcWgradArgs {
     const float* A;   // Z_in / Hin [S][Rpad][Kin]
     const float* Bm;  // Zb_out [S][Rpad][N]
+    // two-MMA mode: |A| and |B| bounds (float bits) from the producing kernels;
+    // the correction products run as one kind::f16 MMA on 2^s-scaled operands
+    const unsigned* amaxA;
+    const unsigned* amaxB;
     CUtensorMap tmA;  // A as [S][Rpad][Kin], box {128, 8, S}
     CUtensorMap tmB;  // Bm as [S][Rpad][N], box {N, 8, S}
     float* wpart;
@@ -868,7 +872,7 @@ struct Tc2WgCfg {
     static_assert(NR * RAW >= 2 * 8 * NFL * 8, "db reduction reuses the raw ring");
 };
 
-template <int L, int PRO, int NF, bool PAIR>
+template <int L, int PRO, int NF, bool PAIR, bool F16C = false>
 __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_constant__ TcWgradArgs g, int wrows) {
     using St = Streams<L>;
     constexpr int S = St::S;
@@ -909,6 +913,14 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
     const uint32_t tmem = tmem_base;
     const uint32_t sraw = tc::smem_u32(smem);
     const uint32_t sbase = sraw + NR * Cfg::RAW;
+    // F16C: operand scales 2^sA, 2^sB (|h| <= max(1, |Z_in|) for tanh jets)
+    int sA = 0, sB = 0;
+    if constexpr (F16C) {
+        const float ma = __uint_as_float(*g.amaxA);
+        sA = tc::f16_scale_exp(PRO == ACT_NONE ? ma : fmaxf(1.0f, ma));
+        sB = tc::f16_scale_exp(__uint_as_float(*g.amaxB));
+    }
+    const float scA = ldexpf(1.0f, sA), scB = ldexpf(1.0f, sB);
 
     if (warp < 16) {
         // A: thread -> (row ar, features 4*ac); B: up to 2 chunks of 4 columns
@@ -919,13 +931,17 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
         constexpr int BCH = NFL / 4;  // float4 chunks per row
         constexpr int NB = (8 * BCH + 255) / 256;
         int brow[2];
-        uint32_t boff[2];
+        uint32_t boff[2], b16l[2], b16h[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const int idx = gtid + 256 * j;
             brow[j] = j < NB ? idx / BCH : 8;
             boff[j] = tc::mn32_off((uint32_t)(brow[j] & 7), (uint32_t)((idx % BCH) * 4), (uint32_t)NFL);
+            b16l[j] = tc::mn16_off((uint32_t)(brow[j] & 7), (uint32_t)((idx % BCH) * 4), (uint32_t)NFL);
+            b16h[j] = tc::mn16_off((uint32_t)(8 + (brow[j] & 7)), (uint32_t)((idx % BCH) * 4), (uint32_t)NFL);
         }
+        const uint32_t a16h = tc::mn16_off((uint32_t)ar, (uint32_t)(ac * 4), 128u);
+        const uint32_t a16l = tc::mn16_off((uint32_t)(8 + ar), (uint32_t)(ac * 4), 128u);
         const uint32_t full0 = PAIR ? tc::mapa(tc::smem_u32(&full[0]), 0) : tc::smem_u32(&full[0]);
         double dbacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
         for (int b = 0; b < nblk; ++b) {
@@ -998,12 +1014,32 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                     _tc = clock64();
 #endif
                     sts128(stage + aoff, ahi[i]);
-                    sts128(stage + Cfg::A_T + aoff, alo[i]);
+                    if constexpr (F16C) {
+                        // A' = [Ah | Al] (k = row, 8 + row), fp16 MN-major SW128, 2^sA-scaled
+                        const float4 h = ahi[i], l = alo[i];
+                        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + Cfg::A_T + a16h),
+                                     "r"(tc::pack_half2(h.x * scA, h.y * scA)), "r"(tc::pack_half2(h.z * scA, h.w * scA)));
+                        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + Cfg::A_T + a16l),
+                                     "r"(tc::pack_half2(l.x * scA, l.y * scA)), "r"(tc::pack_half2(l.z * scA, l.w * scA)));
+                    } else {
+                        sts128(stage + Cfg::A_T + aoff, alo[i]);
+                    }
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         if (brow[j] >= 8) continue;
                         sts128(stage + 2 * Cfg::A_T + boff[j], bhi[i][j]);
-                        sts128(stage + 2 * Cfg::A_T + Cfg::B_T + boff[j], blo[i][j]);
+                        if constexpr (F16C) {
+                            // B' = [Bl ; Bh] (k = row, 8 + row)
+                            const float4 h = bhi[i][j], l = blo[i][j];
+                            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + 2 * Cfg::A_T + Cfg::B_T + b16l[j]),
+                                         "r"(tc::pack_half2(l.x * scB, l.y * scB)),
+                                         "r"(tc::pack_half2(l.z * scB, l.w * scB)));
+                            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + 2 * Cfg::A_T + Cfg::B_T + b16h[j]),
+                                         "r"(tc::pack_half2(h.x * scB, h.y * scB)),
+                                         "r"(tc::pack_half2(h.z * scB, h.w * scB)));
+                        } else {
+                            sts128(stage + 2 * Cfg::A_T + Cfg::B_T + boff[j], blo[i][j]);
+                        }
                     }
                 }
                 tc::fence_proxy_async_smem();
@@ -1069,7 +1105,21 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                 const uint64_t al = tc::make_sdesc(stage + Cfg::A_T, 512, 4 * 512, 1);
                 const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 512, (NFL / 32) * 512, 1);
                 const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 512, (NFL / 32) * 512, 1);
-                if constexpr (PAIR) {
+                if constexpr (F16C) {
+                    // hh in tf32; Ah.Bl + Al.Bh as one K=16 fp16 MMA (MN-major SW128, LBO 1024)
+                    constexpr uint32_t idesc16 = tc::make_idesc_f16(PAIR ? 2 * TC_M : TC_M, NF, 1, 1);
+                    const uint64_t a16 = tc::make_sdesc(stage + Cfg::A_T, 1024, 2 * 1024, 2);
+                    const uint64_t b16 = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 1024, (NFL / 64) * 1024, 2);
+                    if constexpr (PAIR) {
+                        tc::mma_tf32_pair(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
+                        tc::mma_f16_pair(dsmall, a16, b16, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_commit_pair(&empty[st], 3);
+                    } else {
+                        tc::mma_tf32(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
+                        tc::mma_f16(dsmall, a16, b16, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_commit(&empty[st]);
+                    }
+                } else if constexpr (PAIR) {
                     tc::mma_tf32_pair(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
                     tc::mma_tf32_pair(dsmall, ah, bl, idesc, it > 0 ? 1u : 0u);
                     tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
@@ -1110,6 +1160,11 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                 tc::tmem_ld16(tl + (uint32_t)c, a);
                 tc::tmem_ld16(tl + (uint32_t)(NF + c), b);
                 tc::tmem_ld_wait();
+                if constexpr (F16C) {
+                    const float us = ldexpf(1.0f, -(sA + sB));
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) b[j] *= us;
+                }
 #pragma unroll
                 for (int j = 0; j < 16; j += 4)
                     *reinterpret_cast<float4*>(dst + c + j) =

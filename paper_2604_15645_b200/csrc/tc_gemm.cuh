@@ -790,7 +790,9 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                     const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 16, 256, 6);
                     tc::mma_tf32_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
                     tc::mma_tf32_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+#ifndef PNX_EXP_TWO_MMA  // timing experiment only: drops a product
                     tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
+#endif
                     tc::mma_commit_pair(&empty[st], 3);
                 }
                 tc::mma_commit_pair(&tfull, 3);
@@ -1360,11 +1362,15 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                         if constexpr (PAIR) {
                             tc::mma_tf32_pair(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
                             tc::mma_tf32_pair(d, adh, bl, idesc, 1u);
+#ifndef PNX_EXP_TWO_MMA  // timing experiment only: drops a product
                             tc::mma_tf32_pair(d, adl, bh, idesc, 1u);
+#endif
                         } else {
                             tc::mma_tf32(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
                             tc::mma_tf32(d, adh, bl, idesc, 1u);
+#ifndef PNX_EXP_TWO_MMA  // timing experiment only: drops a product
                             tc::mma_tf32(d, adl, bh, idesc, 1u);
+#endif
                         }
                     }
                     if constexpr (PAIR) tc::mma_commit_pair(&empty[st], 3);

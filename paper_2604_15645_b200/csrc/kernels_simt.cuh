@@ -1024,10 +1024,11 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 2) k_head(HeadArgs a) {
         for (int i = threadIdx.x; i < 3 * kStatMax; i += blockDim.x) {
             double v = 0.0;
             for (int w = 0; w < kHeadWarps; ++w) v += sacc[w][i];
+            // accumulate: the buffers are zeroed per step and several chunks may contribute
             if (i < kStatMax) {
-                if (i < a.seg_M) a.seg_part[(int64_t)blockIdx.x * a.seg_M + i] = v;
+                if (i < a.seg_M) a.seg_part[(int64_t)blockIdx.x * a.seg_M + i] += v;
             } else if (i - kStatMax < 2 * a.poy_T) {
-                a.poy_part[(int64_t)blockIdx.x * 2 * a.poy_T + (i - kStatMax)] = v;
+                a.poy_part[(int64_t)blockIdx.x * 2 * a.poy_T + (i - kStatMax)] += v;
             }
         }
         return;

@@ -156,6 +156,32 @@ def test_chunking_is_invisible():
         assert abs(l1[k] - l2[k]) <= 1e-6 * abs(l1[k]) + 1e-12
 
 
+def test_chunking_is_invisible_with_causality_and_poynting():
+    """Several chunks: causality needs every chunk's segment sums before any
+    seed (two-pass forward) and the Poynting nodes ride in chunk 0; the step
+    must match the single-chunk step, and the oracle."""
+    pk = _pkg()
+    wl, col, flat, rffB, ospec, ores, ocol = _workload_case("c4", [12, 12, 10])
+    caus = pk.CausalityConfig(4, 1.5, 0.0, 1.5)
+    poy = pk.PoyntingConfig(0.3, 6, 3, (-1.0, 1.0, -1.0, 1.0, 0.0, 1.5))
+    w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, causality=caus, poynting=poy, **col)
+    w.set_engine("ffma")
+    g1, l1 = w.step(flat)
+    p1 = w.penalty()
+    w.set_chunk_rows(500)
+    g2, l2 = w.step(flat)
+    assert rel_l2(g2, g1) <= 1e-6
+    for k in l1:
+        assert abs(l1[k] - l2[k]) <= 1e-6 * abs(l1[k]) + 1e-12
+    assert abs(w.penalty() - p1) <= 1e-6 * abs(p1)
+    ref, outs = po.data_parallel_gradient(ospec, flat, rffB, ores, ocol, wl.bc, 1,
+                                          causality=po.Causality(4, 1.5, 0.0, 1.5),
+                                          poynting=po.Poynting(0.3, 6, 3, (-1.0, 1.0), (-1.0, 1.0), (0.0, 1.5)))
+    assert rel_l2(g2, ref) <= GRAD_RTOL
+    assert abs(l2["pde"] - outs[0]["pde"]) <= LOSS_RTOL * abs(outs[0]["pde"])
+    assert abs(w.penalty() - outs[0]["pen"]) <= LOSS_RTOL * abs(outs[0]["pen"])
+
+
 def test_step_is_deterministic():
     pk = _pkg()
     wl, col, flat, rffB, *_ = _workload_case("c1", [50, 40])

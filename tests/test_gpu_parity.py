@@ -182,6 +182,27 @@ def test_chunking_is_invisible_with_causality_and_poynting():
     assert abs(w.penalty() - outs[0]["pen"]) <= LOSS_RTOL * abs(outs[0]["pen"])
 
 
+def test_resampled_points_recount_causality_segments():
+    """pnx_set_points with an equal-size set (the resampling fast path) must
+    rebucket the interior by time, like a fresh worker on the new points."""
+    pk = _pkg()
+    wl, col, flat, rffB, *_ = _workload_case("c1", [24, 20])
+    caus = pk.CausalityConfig(5, 2.0, 0.0, 1.0)
+    w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, causality=caus, **col)
+    w.set_engine("ffma")
+    w.step(flat)
+    rng = np.random.default_rng(7)
+    pts = np.stack([rng.uniform(0.0, 2.0, len(col["interior"])), rng.uniform(0.0, 1.0, len(col["interior"])) ** 2],
+                   axis=1)  # skewed towards early times: different segment counts
+    w.set_points(pts)
+    g1, l1 = w.step(flat)
+    fresh = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, causality=caus, **dict(col, interior=pts))
+    fresh.set_engine("ffma")
+    g2, l2 = fresh.step(flat)
+    assert rel_l2(g1, g2) <= 1e-6
+    assert abs(l1["pde"] - l2["pde"]) <= 1e-6 * abs(l2["pde"])
+
+
 def test_step_is_deterministic():
     pk = _pkg()
     wl, col, flat, rffB, *_ = _workload_case("c1", [50, 40])

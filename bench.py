@@ -339,6 +339,7 @@ def main():
         host_params = flat.copy()
         opt_m = np.zeros_like(host_params)
         opt_v = np.zeros_like(host_params)
+        tmp = np.empty_like(host_params)
         shard_pinned = torch.from_numpy(np.ascontiguousarray(shard.T)).pin_memory()  # axis-major [d, N]
         g_dev = torch.zeros(P, dtype=torch.float64, device=dev)
         h2d = d2h = 0
@@ -352,10 +353,20 @@ def main():
                 g_dev.copy_(torch.from_numpy(g_host))
                 dist.all_reduce(g_dev, op=dist.ReduceOp.SUM)
                 g_host = g_dev.cpu().numpy() / world
-            b1, b2 = 0.9, 0.999                          # host Adam (optim.cpp:7-41)
-            opt_m[:] = b1 * opt_m + (1 - b1) * g_host
-            opt_v[:] = b2 * opt_v + (1 - b2) * g_host * g_host
-            host_params[:] -= 1e-3 * (opt_m / (1 - b1 ** k)) / (np.sqrt(opt_v / (1 - b2 ** k)) + 1e-8)
+            b1, b2 = 0.9, 0.999                          # host Adam (optim.cpp:7-41), in place
+            np.multiply(opt_m, b1, out=opt_m)
+            np.multiply(g_host, 1 - b1, out=tmp)
+            np.add(opt_m, tmp, out=opt_m)
+            np.multiply(g_host, g_host, out=tmp)
+            np.multiply(tmp, 1 - b2, out=tmp)
+            np.multiply(opt_v, b2, out=opt_v)
+            np.add(opt_v, tmp, out=opt_v)
+            np.multiply(opt_v, 1.0 / (1 - b2 ** k), out=tmp)
+            np.sqrt(tmp, out=tmp)
+            np.add(tmp, 1e-8, out=tmp)
+            np.divide(opt_m, tmp, out=tmp)
+            np.multiply(tmp, 1e-3 / (1 - b1 ** k), out=tmp)
+            np.subtract(host_params, tmp, out=host_params)
             h2d = pts.nbytes + P * 4
             d2h = P * 4 + 3 * 8
 

@@ -41,7 +41,7 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--points-per-gpu", type=int, default=1 << 20)
-    ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc3xtf32"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc3xtf32", "tc3xf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", action="store_true",

@@ -44,7 +44,10 @@ enum { PNX_PDE_ADVECTION = 0, PNX_PDE_ALLEN_CAHN = 1, PNX_PDE_BURGERS = 2,
 /* TrainingProblem::Bc (trainer.hpp:23-27). */
 enum { PNX_BC_HARD = 0, PNX_BC_SOFT_PERIODIC = 1, PNX_BC_DIRICHLET_ZERO = 2 };
 /* Contraction engine for the hidden layers. */
-enum { PNX_ENGINE_AUTO = 0, PNX_ENGINE_FFMA = 1, PNX_ENGINE_TC3XTF32 = 2 };
+/* TC3XF16: the tensor-core engine with 3xFP16 operands (hi/lo fp16 pairs scaled
+ * by powers of two from recorded absmax bounds: the same 22-bit operand
+ * precision as 3xTF32 at twice the tensor rate) where the kernels support it. */
+enum { PNX_ENGINE_AUTO = 0, PNX_ENGINE_FFMA = 1, PNX_ENGINE_TC3XTF32 = 2, PNX_ENGINE_TC3XF16 = 3 };
 
 /* ModelSpec (model.hpp:41-57). rff_B is the frozen RFF matrix Model::rff_matrix()
  * [embedded_width x rff_width] row-major (model.cpp:58-62); NULL when rff_width==0.

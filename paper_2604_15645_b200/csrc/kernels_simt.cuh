@@ -39,12 +39,14 @@ struct LayerTab {
     int64_t dB[kMaxLayers];      // offset into the bias arena
 };
 
+// wamax (optional): per layer, max |W| as float bits (3xFP16 weight-image scale)
 static __global__ void k_prep(const float* __restrict__ params, LayerTab t, float* __restrict__ W,
-                       float* __restrict__ Wt, float* __restrict__ bias) {
+                       float* __restrict__ Wt, float* __restrict__ bias, unsigned* __restrict__ wamax = nullptr) {
     const int l = blockIdx.y;
     if (l >= t.n) return;
     const int K = t.K[l], N = t.N[l];
     const int64_t total = (int64_t)K * N;
+    unsigned mx = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total + N;
          i += (int64_t)gridDim.x * blockDim.x) {
         if (i < total) {
@@ -53,10 +55,15 @@ static __global__ void k_prep(const float* __restrict__ params, LayerTab t, floa
             if (t.offS[l] >= 0) w = w * expf(params[t.offS[l] + n]);
             W[t.dW[l] + i] = w;
             Wt[t.dW[l] + (int64_t)n * K + k] = w;
+            mx = max(mx, __float_as_uint(fabsf(w)));
         } else {
             const int n = (int)(i - total);
             bias[t.dB[l] + n] = params[t.offB[l] + n];
         }
+    }
+    if (wamax) {
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if ((threadIdx.x & 31) == 0) atomicMax(wamax + l, mx);
     }
 }
 
@@ -197,7 +204,8 @@ constexpr int L0_ROWS = 32;
 
 template <int L, int ACT>
 __global__ void __launch_bounds__(256) k_layer0_fwd(InputArgs a, const float* __restrict__ W0,
-                                                   const float* __restrict__ b0, float* __restrict__ Z0, int H) {
+                                                   const float* __restrict__ b0, float* __restrict__ Z0, int H,
+                                                   unsigned* __restrict__ amax = nullptr) {
     using St = Streams<L>;
     constexpr int S = St::S;
     __shared__ float E[L0_ROWS][S][2 * kMaxAxes];
@@ -205,6 +213,9 @@ __global__ void __launch_bounds__(256) k_layer0_fwd(InputArgs a, const float* __
     const int K0 = a.E;
     for (int i = threadIdx.x; i < K0 * H; i += blockDim.x) Ws[i] = W0[i];
     const int64_t RH = (int64_t)a.Rpad * H;
+    unsigned mx[S];  // |z| bound per stream (3xFP16 operand scales of the next layer)
+#pragma unroll
+    for (int s = 0; s < S; ++s) mx[s] = 0;
     for (int rb = blockIdx.x * L0_ROWS; rb < a.Rpad; rb += gridDim.x * L0_ROWS) {
         __syncthreads();
         if (threadIdx.x < L0_ROWS) {
@@ -246,8 +257,18 @@ __global__ void __launch_bounds__(256) k_layer0_fwd(InputArgs a, const float* __
             z[0][3] = store_value<ACT>(z[0][3] + bb.w);
             float* dst = Z0 + (int64_t)(rb + rr) * H + n;
 #pragma unroll
-            for (int s = 0; s < S; ++s)
+            for (int s = 0; s < S; ++s) {
                 *reinterpret_cast<float4*>(dst + s * RH) = make_float4(z[s][0], z[s][1], z[s][2], z[s][3]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) mx[s] = max(mx[s], __float_as_uint(fabsf(z[s][j])));
+            }
+        }
+    }
+    if (amax) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const unsigned v = __reduce_max_sync(0xffffffffu, mx[s]);
+            if ((threadIdx.x & 31) == 0) atomicMax(amax + s, v);
         }
     }
 }

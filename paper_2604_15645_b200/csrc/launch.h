@@ -13,7 +13,7 @@ void launch_gemm(int L, int pro, int epi, int eact, const GemmArgs& g, cudaStrea
 void launch_wgrad(int L, int pro, const WgradArgs& w, int nsplit, cudaStream_t st);
 void launch_head(int pde, int act, const HeadArgs& h, int grid, cudaStream_t st);
 void launch_layer0_fwd(int L, int act, const InputArgs& a, const float* W0, const float* b0, float* Z0, int H,
-                       cudaStream_t st);
+                       unsigned* amax, cudaStream_t st);
 void launch_layer0_wgrad(int L, const InputArgs& a, const float* Zb0, int H, double* part, int grid, cudaStream_t st);
 int launch_tc_layer(int L, int mode, int pro, const TcGemmArgs& g, cudaStream_t st);
 int launch_tc2_fwd(int L, int pro, const TcGemmArgs& g, cudaStream_t st);

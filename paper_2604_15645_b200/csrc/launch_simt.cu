@@ -125,21 +125,21 @@ void launch_head(int pde, int act, const HeadArgs& h, int grid, cudaStream_t st)
 
 template <int L>
 void launch_layer0_fwd_l(int act, const InputArgs& a, const float* W0, const float* b0, float* Z0, int H,
-                         cudaStream_t st) {
+                         unsigned* amax, cudaStream_t st) {
     const int grid = std::min(148 * 8, (a.Rpad + L0_ROWS - 1) / L0_ROWS);
     switch (act) {
-        case ACT_TANH: k_layer0_fwd<L, ACT_TANH><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H); break;
-        case ACT_SINE: k_layer0_fwd<L, ACT_SINE><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H); break;
-        default: k_layer0_fwd<L, ACT_SWISH><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H); break;
+        case ACT_TANH: k_layer0_fwd<L, ACT_TANH><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H, amax); break;
+        case ACT_SINE: k_layer0_fwd<L, ACT_SINE><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H, amax); break;
+        default: k_layer0_fwd<L, ACT_SWISH><<<grid, 256, 0, st>>>(a, W0, b0, Z0, H, amax); break;
     }
 }
 void launch_layer0_fwd(int L, int act, const InputArgs& a, const float* W0, const float* b0, float* Z0, int H,
-                       cudaStream_t st) {
+                       unsigned* amax, cudaStream_t st) {
     switch (L) {
-        case LAY_XT: launch_layer0_fwd_l<LAY_XT>(act, a, W0, b0, Z0, H, st); break;
-        case LAY_AC: launch_layer0_fwd_l<LAY_AC>(act, a, W0, b0, Z0, H, st); break;
-        case LAY_MX: launch_layer0_fwd_l<LAY_MX>(act, a, W0, b0, Z0, H, st); break;
-        case LAY_NS: launch_layer0_fwd_l<LAY_NS>(act, a, W0, b0, Z0, H, st); break;
+        case LAY_XT: launch_layer0_fwd_l<LAY_XT>(act, a, W0, b0, Z0, H, amax, st); break;
+        case LAY_AC: launch_layer0_fwd_l<LAY_AC>(act, a, W0, b0, Z0, H, amax, st); break;
+        case LAY_MX: launch_layer0_fwd_l<LAY_MX>(act, a, W0, b0, Z0, H, amax, st); break;
+        case LAY_NS: launch_layer0_fwd_l<LAY_NS>(act, a, W0, b0, Z0, H, amax, st); break;
     }
 }
 template <int L, int NC>

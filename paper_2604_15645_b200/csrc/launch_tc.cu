@@ -125,11 +125,11 @@ int launch_tc2_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
     kern<<<g.Rpad / TC_M, TC3_THREADS, smem, st>>>(g);
     return 0;
 }
-template <int L, int PRO>
+template <int L, int PRO, bool F16>
 int launch_tc4_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc4FwdCfg<L>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc4_fwd<L, PRO>;
+    auto kern = k_tc4_fwd<L, PRO, F16>;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
@@ -137,7 +137,7 @@ int launch_tc4_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
     }
     TcGemmArgs a = g;
     constexpr int S = Streams<L>::S;
-    const int nkb = g.K / 8;
+    const int nkb = g.K / (F16 ? 16 : 8);
     if (tc_make_tmap(&a.tmA, g.A, 3, g.K, g.Rpad, S, 32, 128, 1, true) ||
         tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)nkb * 2 * Cfg::NF, 1, 8, 128, 1, false) ||
         tc_make_tmap(&a.tmO, g.out, 3, Cfg::NF, g.Rpad, S, 32, 32, 1, true))
@@ -159,8 +159,14 @@ int launch_tc4_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
 template <int L>
 int launch_tc2_fwd_l(int pro, const TcGemmArgs& g, cudaStream_t st) {
     static const bool pair = getenv("PNX_FWD_NOPAIR") == nullptr;
-    if (g.N == 256 && pair && g.Rpad % 256 == 0 && g.K % 32 == 0)
-        return pro == ACT_NONE ? launch_tc4_fwd_t<L, ACT_NONE>(g, st) : launch_tc4_fwd_t<L, ACT_TANH>(g, st);
+    if (g.N == 256 && pair && g.Rpad % 256 == 0 && g.K % 32 == 0) {
+        if (g.f16)
+            return pro == ACT_NONE ? launch_tc4_fwd_t<L, ACT_NONE, true>(g, st)
+                                   : launch_tc4_fwd_t<L, ACT_TANH, true>(g, st);
+        return pro == ACT_NONE ? launch_tc4_fwd_t<L, ACT_NONE, false>(g, st)
+                               : launch_tc4_fwd_t<L, ACT_TANH, false>(g, st);
+    }
+    if (g.f16) return -1;  // 3xFP16 only in the pair forward
     if (g.N == 256) return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 256>(g, st) : launch_tc2_fwd_t<L, ACT_TANH, 256>(g, st);
     if (g.N == 128) return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 128>(g, st) : launch_tc2_fwd_t<L, ACT_TANH, 128>(g, st);
     return -1;

@@ -91,6 +91,8 @@ struct pnx_ctx {
     double* d_red = nullptr;
     float* d_bc_vals = nullptr;
     int* d_bad = nullptr;
+    // 3xFP16 operand bounds (float bits): [|W_l|] [|Z_l[s]|] [|Zb_l[s]|]
+    unsigned* d_amax = nullptr;
     float* d_resid = nullptr;
     int64_t resid_cap = 0;
     bool h_int_stale = false;  // interior coordinates newer on device than in h_int
@@ -198,6 +200,11 @@ int pde_layout(int pde) {
 
 constexpr int kL0Blocks = 296;
 // layer 0 fused with the input jets (narrow embedding: no RFF, K0 <= 8, H % 4 == 0)
+constexpr int kAmaxS = 8;
+constexpr int kAmaxLen = kMaxLayers * (1 + 2 * kAmaxS);
+inline unsigned* amax_w(pnx_ctx* c, int l) { return c->d_amax + l; }
+inline unsigned* amax_z(pnx_ctx* c, int l) { return c->d_amax + kMaxLayers + l * kAmaxS; }
+inline unsigned* amax_zb(pnx_ctx* c, int l) { return c->d_amax + kMaxLayers * (1 + kAmaxS) + l * kAmaxS; }
 bool layer0_fused(const pnx_ctx* c) { return c->rff_w == 0 && c->K0 <= 8 && c->H % 4 == 0 && c->H <= 512; }
 
 int64_t bytes_per_row(const pnx_ctx* c) {
@@ -321,9 +328,10 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
     const int L = ctx->layout;
     const int act = ctx->act;
 
+    CK(cudaMemsetAsync(ctx->d_amax, 0, kAmaxLen * sizeof(unsigned), st));
     {
         dim3 grid(64, Lw);
-        k_prep<<<grid, 256, 0, st>>>(d_params, t, ctx->d_W, ctx->d_Wt, ctx->d_bias);
+        k_prep<<<grid, 256, 0, st>>>(d_params, t, ctx->d_W, ctx->d_Wt, ctx->d_bias, ctx->d_amax);
         CKL();
     }
     for (int l = 0; l < Lw - 1; ++l)
@@ -360,6 +368,9 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
 
     const bool tc_on = tc_enabled(ctx->engine, ctx->H, S, act);
     bool tc_fwd[kMaxLayers] = {}, tc_bwd[kMaxLayers] = {}, tc_wg[kMaxLayers] = {};
+    // 3xFP16 per layer: the pair forward, fed by a producer that records |Z| bounds
+    // (the fused layer 0 or another pair forward)
+    bool f16_fwd[kMaxLayers] = {};
     // debug/ablation: PNX_TC_MASK bit0 forward, bit1 reverse, bit2 weight-gradient (default all)
     static const int tc_mask = getenv("PNX_TC_MASK") ? atoi(getenv("PNX_TC_MASK")) : 7;
     if (tc_on) {
@@ -383,10 +394,21 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             CK(cudaMalloc(&ctx->tc.img, need * sizeof(float)));
             ctx->tc.img_cap = need;
         }
+        const bool f16 = ctx->engine == PNX_ENGINE_TC3XF16;
+        bool rec = layer0_fused(ctx);  // Z_{l-1} bounds recorded
         for (int l = 0; l < ctx->depth; ++l) {
             tc_wg[l] = tc_fwd[l] && (tc_mask & 4);
             if (!(tc_mask & 2)) tc_bwd[l] = false;
-            if (tc_fwd[l]) {
+            if (l > 0) {
+                const bool pairf = tc_fwd[l] && (tc_mask & 1) && tc4_fwd_ok(t.K[l], t.N[l]);
+                f16_fwd[l] = f16 && pairf && rec;
+                rec = pairf;
+            }
+            if (f16_fwd[l]) {
+                k_tc_prep_image16<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 0, t.N[l], amax_w(ctx, l),
+                                                      reinterpret_cast<uint16_t*>(ctx->tc.img + ctx->tc.img_fwd[l]));
+                CKL();
+            } else if (tc_fwd[l]) {
                 k_tc_prep_image<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 0, t.N[l],
                                                     ctx->tc.img + ctx->tc.img_fwd[l]);
                 CKL();
@@ -426,7 +448,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             const int pro = l == 0 ? ACT_NONE : act;
             prof_begin(ctx, PC_FWD, st);
             if (l == 0 && fuse0) {
-                launch_layer0_fwd(L, act, ia, g.B, g.bias, g.out, g.N, st);
+                launch_layer0_fwd(L, act, ia, g.B, g.bias, g.out, g.N, amax_z(ctx, 0), st);
                 CKL();
             } else if (tc_fwd[l] && (tc_mask & 1)) {
                 TcGemmArgs tg{};
@@ -437,6 +459,10 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 tg.Rpad = Rpad;
                 tg.K = g.K;
                 tg.N = g.N;
+                tg.f16 = f16_fwd[l] ? 1 : 0;
+                tg.amax_in = l > 0 ? amax_z(ctx, l - 1) : nullptr;
+                tg.amax_w = amax_w(ctx, l);
+                tg.amax_out = amax_z(ctx, l);
                 if (launch_tc2_fwd(L, pro, tg, st)) return fail(ctx, PNX_ERR_CUDA, "tc forward launch");
                 CKL();
             } else {
@@ -807,7 +833,7 @@ int pnx_create(const pnx_model_desc* m, const pnx_problem_desc* p, int device, p
         (rc = dalloc(ctx, &ctx->d_head_part, (size_t)ctx->head_grid * (ctx->H * ctx->F + ctx->F))) ||
         (rc = dalloc(ctx, &ctx->d_loss_part, (size_t)ctx->head_grid * 3)) ||
         (rc = dalloc(ctx, &ctx->d_partP, (size_t)ctx->ibwd_grid * kMaxAxes)) ||
-        (rc = dalloc(ctx, &ctx->d_bad, 4))) {
+        (rc = dalloc(ctx, &ctx->d_bad, 4)) || (rc = dalloc(ctx, &ctx->d_amax, kAmaxLen))) {
         g_create_error = ctx->err;
         pnx_destroy(ctx);
         return rc;
@@ -869,6 +895,7 @@ void pnx_destroy(pnx_ctx* ctx) {
     cudaFree(ctx->d_poy_g);
     cudaFree(ctx->d_pen);
     cudaFree(ctx->d_bad);
+    cudaFree(ctx->d_amax);
     cudaFree(ctx->d_resid);
     tc_workspace_free(ctx->tc);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1030,7 +1057,7 @@ int pnx_set_bc(pnx_ctx* ctx, const double* a, const double* b, const double* tar
 }
 
 int pnx_set_engine(pnx_ctx* ctx, int engine) {
-    if (!ctx || engine < 0 || engine > 2) return PNX_ERR_ARG;
+    if (!ctx || engine < 0 || engine > 3) return PNX_ERR_ARG;
     ctx->engine = engine;
     return PNX_OK;
 }

@@ -288,6 +288,49 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+// ---- 3xFP16 split ---------------------------------------------------------------
+// x * 2^e = hi + lo with hi = fp16(x 2^e), lo = fp16(x 2^e - hi): 11 + 11
+// significant bits, the same as the tf32 hi/lo pair, at twice the tensor rate
+// per instruction (kind::f16 K = 16 in the cycles of kind::tf32 K = 8). The
+// power-of-two scale 2^e puts the operand's absmax bound into [2^13, 2^14)
+// (f16_scale_exp), far below the fp16 maximum; elements far below the bound
+// lose only absolute precision under 2^-25 of the scaled unit in lo.
+__device__ __forceinline__ void split_h2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+// 8 consecutive K elements (one 16 B chunk of a K-major fp16 row), scaled by sc
+__device__ __forceinline__ void split_h8(const float* h, float sc, uint4& hi, uint4& lo) {
+    split_h2(h[0] * sc, h[1] * sc, hi.x, lo.x);
+    split_h2(h[2] * sc, h[3] * sc, hi.y, lo.y);
+    split_h2(h[4] * sc, h[5] * sc, hi.z, lo.z);
+    split_h2(h[6] * sc, h[7] * sc, hi.w, lo.w);
+}
+// byte offset of 16 B chunk c (0/1) of row `row` in a K-major SW32 tile (32 B
+// rows = 8 fp32 or 16 fp16 of K; chunk ^= (row/4)&1) -- sw32_off(row, 4c)
+__host__ __device__ __forceinline__ uint32_t sw32_chunk(uint32_t row, uint32_t c) {
+    return (row >> 3) * 256u + (row & 7u) * 32u + (((c ^ (row >> 2)) & 1u) << 4);
+}
+// element (row, k), k < 16, of a K-major SW32 fp16 tile
+__host__ __device__ __forceinline__ uint32_t sw32h_off(uint32_t row, uint32_t k) {
+    return sw32_chunk(row, k >> 3) + (k & 7u) * 2u;
+}
+// |x| bound as order-preserving bits (non-negative floats compare as uints)
+__device__ __forceinline__ unsigned abs_bits(float x) { return __float_as_uint(fabsf(x)); }
+// fold a per-lane max into *dst (one atomic per warp)
+__device__ __forceinline__ void warp_amax(unsigned* dst, unsigned v) {
+    v = __reduce_max_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0) atomicMax(dst, v);
+}
+// operand scale exponent from a recorded absmax (bits) -- bound in [2^13, 2^14)
+__device__ __forceinline__ int f16_exp_bits(unsigned bits) {
+    const int e = f16_scale_exp(__uint_as_float(bits));
+    return e > 110 ? 110 : (e < -110 ? -110 : e);
+}
+
 // ---- 3xTF32 split -------------------------------------------------------------
 __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;

@@ -71,11 +71,36 @@ static __global__ void k_tc_prep_image(const float* __restrict__ W, int K, int N
     }
 }
 
+// 3xFP16 weight images: per 16-wide K block kb, {hi, lo} tiles of NT rows x 16
+// fp16 (32 B rows, SW32 like the tf32 tiles), element (n, k) at
+// sw32h_off(n % NT, k % 16); W is scaled by 2^e, e = f16_exp_bits(*wamax).
+static __global__ void k_tc_prep_image16(const float* __restrict__ W, int K, int N, int transpose_b, int NT,
+                                         const unsigned* __restrict__ wamax, uint16_t* __restrict__ img) {
+    const int rowsB = transpose_b ? K : N, KB = transpose_b ? N : K;
+    const float sc = ldexpf(1.0f, tc::f16_exp_bits(*wamax));
+    const int64_t total = (int64_t)rowsB * KB;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int n = (int)(i / KB), k = (int)(i % KB);
+        const float w = (transpose_b ? W[(int64_t)n * N + k] : W[(int64_t)k * N + n]) * sc;
+        const __half hi = __float2half_rn(w);
+        const __half lo = __float2half_rn(w - __half2float(hi));
+        const int nt = n / NT, kb = k / 16;
+        const int64_t blk = ((int64_t)nt * (KB / 16) + kb) * (2 * NT * 16);
+        const uint32_t off = tc::sw32h_off((uint32_t)(n % NT), (uint32_t)(k % 16)) / 2;
+        img[blk + off] = __half_as_ushort(hi);
+        img[blk + NT * 16 + off] = __half_as_ushort(lo);
+    }
+}
+
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void sts128u(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
@@ -150,6 +175,12 @@ struct TcGemmArgs {
     const float* Zlow;  // bwd: Z_in [S][Rpad][N]
     float* out;         // [S][Rpad][N]
     int Rpad, K, N;
+    // 3xFP16: |A| bounds per stream and the |W| bound (float bits) recorded by the
+    // producers; amax_out (optional) records this kernel's output bounds per stream
+    int f16;  // 1: 3xFP16 operands (fp16 weight image at img)
+    const unsigned* amax_in;
+    const unsigned* amax_w;
+    unsigned* amax_out;
     CUtensorMap tmA;    // pair kernels: A as [S][Rpad][K], box {32, 128, 1}, 128 B swizzle
     CUtensorMap tmB;    // pair kernels: weight image as rows of 8 fp32, box {8, 128}
     CUtensorMap tmO;    // forward pair kernel: out as [S][Rpad][N], box {32, 32, 1}, 128 B swizzle
@@ -272,6 +303,12 @@ inline int tc_wgrad_rows(int64_t Rpad, int Kin, int nsm) {
 inline bool tc5_bwd_ok(int L, int nout, int kred) {
     static const bool off = getenv("PNX_TC5_OFF") != nullptr;
     return !off && (L == LAY_XT || L == LAY_MX) && nout == 256 && kred % 8 == 0;
+}
+
+// the CTA-pair forward (k_tc4_fwd) runs this layer (PNX_FWD_NOPAIR=1 disables it)
+inline bool tc4_fwd_ok(int K, int N) {
+    static const bool off = getenv("PNX_FWD_NOPAIR") != nullptr;
+    return !off && N == 256 && K % 32 == 0;
 }
 
 inline bool tc_layer_ok(int S, int K, int N) {
@@ -635,7 +672,9 @@ struct Tc4FwdCfg {
 };
 constexpr int TC4_THREADS = 576;  // 18 warps
 
-template <int L, int PRO>
+// F16: 3xFP16 operands (kind::f16, K = 16 per stage) scaled by the recorded
+// bounds g.amax_in / g.amax_w; the epilogue unscales and records g.amax_out.
+template <int L, int PRO, bool F16 = false>
 __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constant__ TcGemmArgs g) {
     using St = Streams<L>;
     constexpr int S = St::S;
@@ -649,7 +688,19 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = tc::cluster_ctarank();
     const int r0 = (blockIdx.x >> 1) * 256 + (int)rank * 128;
-    const int nkb = g.K / 8, ngrp = g.K / 32;
+    constexpr int KS = F16 ? 16 : 8;   // K per stage (one MMA)
+    constexpr int SPG = 32 / KS;       // stages per 32-feature raw group
+    const int nkb = g.K / KS, ngrp = g.K / 32;
+    // 3xFP16 operand scale exponent of stream p's A (|act(Z_in)[p]| bound)
+    auto a_exp = [&](int p) -> int {
+        if (PRO != ACT_NONE && p == 0) return tc::f16_scale_exp(1.0f);
+        float b = __uint_as_float(g.amax_in[p]);
+        if (PRO != ACT_NONE && St::order(p) == 2) {
+            const float a = __uint_as_float(g.amax_in[St::partner(p)]);
+            b = b + 2.0f * a * a;
+        }
+        return tc::f16_exp_bits(__float_as_uint(b * 1.001f));
+    };
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             tc::mbar_init(&full[i], 17);  // 2 x 8 converter warps + the leader's expect_tx
@@ -682,48 +733,72 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
         const uint32_t aoff = tc::sw32_off((uint32_t)row, (uint32_t)(c * 4));
         const uint32_t rrow = (uint32_t)row * 128;
         const uint32_t rsw = (uint32_t)(row & 7);
+        // activation jet of stream p for the 4 features in raw 16 B chunk `off`
+        auto act_h = [&](uint32_t raw, uint32_t off, int p) -> float4 {
+            if (PRO == ACT_NONE || p == 0) return lds128(raw + off);
+            const float4 t = lds128(raw + off), z = lds128(raw + Cfg::BOX + off);
+            if (St::order(p) == 1)
+                return make_float4((1.f - t.x * t.x) * z.x, (1.f - t.y * t.y) * z.y, (1.f - t.z * t.z) * z.z,
+                                   (1.f - t.w * t.w) * z.w);
+            const float4 za = lds128(raw + 2 * Cfg::BOX + off);
+            return make_float4((1.f - t.x * t.x) * (z.x - 2.f * t.x * za.x * za.x),
+                               (1.f - t.y * t.y) * (z.y - 2.f * t.y * za.y * za.y),
+                               (1.f - t.z * t.z) * (z.z - 2.f * t.z * za.z * za.z),
+                               (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
+        };
         for (int p = 0; p < S; ++p) {
+            const float sc = F16 ? ldexpf(1.0f, a_exp(p)) : 1.0f;
             for (int gi = 0; gi < ngrp; ++gi) {
                 const int gq = p * ngrp + gi, rs = gq % NR;
                 const uint32_t raw = sraw + rs * Cfg::RAW;
                 tc::mbar_wait(&rfull[rs], (uint32_t)(gq / NR) & 1u);
-                float4 hi[4], lo[4];
+                if constexpr (F16) {
+                    // stage j = features [16j, 16j+16) of the group; this thread: chunk c
+                    uint4 hi[2], lo[2];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t off = rrow + ((((uint32_t)(2 * j + c)) ^ rsw) << 4);
-                    float4 h;
-                    if (PRO == ACT_NONE || p == 0) {
-                        h = lds128(raw + off);
-                    } else {
-                        const float4 t = lds128(raw + off), z = lds128(raw + Cfg::BOX + off);
-                        if (St::order(p) == 1) {
-                            h = make_float4((1.f - t.x * t.x) * z.x, (1.f - t.y * t.y) * z.y, (1.f - t.z * t.z) * z.z,
-                                            (1.f - t.w * t.w) * z.w);
-                        } else {
-                            const float4 za = lds128(raw + 2 * Cfg::BOX + off);
-                            h = make_float4((1.f - t.x * t.x) * (z.x - 2.f * t.x * za.x * za.x),
-                                            (1.f - t.y * t.y) * (z.y - 2.f * t.y * za.y * za.y),
-                                            (1.f - t.z * t.z) * (z.z - 2.f * t.z * za.z * za.z),
-                                            (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
+                    for (int j = 0; j < 2; ++j) {
+                        float h[8];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const float4 v = act_h(raw, rrow + ((((uint32_t)(4 * j + 2 * c + u)) ^ rsw) << 4), p);
+                            h[4 * u] = v.x;
+                            h[4 * u + 1] = v.y;
+                            h[4 * u + 2] = v.z;
+                            h[4 * u + 3] = v.w;
                         }
+                        tc::split_h8(h, sc, hi[j], lo[j]);
                     }
-                    split4(h, hi[j], lo[j]);
-                }
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&rempty[rs]);
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&rempty[rs]);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int it = gq * 4 + j, st = it % NST;
-                    const uint32_t stage = sbase + st * Cfg::STAGE;
-                    tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
-                    sts128(stage + aoff, hi[j]);
-                    sts128(stage + Cfg::A_T + aoff, lo[j]);
+                    for (int j = 0; j < 2; ++j) {
+                        const int it = gq * 2 + j, st = it % NST;
+                        const uint32_t stage = sbase + st * Cfg::STAGE;
+                        tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                        sts128u(stage + aoff, hi[j]);
+                        sts128u(stage + Cfg::A_T + aoff, lo[j]);
+                    }
+                } else {
+                    float4 hi[4], lo[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        split4(act_h(raw, rrow + ((((uint32_t)(2 * j + c)) ^ rsw) << 4), p), hi[j], lo[j]);
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&rempty[rs]);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int it = gq * 4 + j, st = it % NST;
+                        const uint32_t stage = sbase + st * Cfg::STAGE;
+                        tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                        sts128(stage + aoff, hi[j]);
+                        sts128(stage + Cfg::A_T + aoff, lo[j]);
+                    }
                 }
                 tc::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) tc::mbar_arrive_cluster(full0 + ((gq * 4 + j) % NST) * 8);
+                    for (int j = 0; j < SPG; ++j) tc::mbar_arrive_cluster(full0 + ((gq * SPG + j) % NST) * 8);
                 }
             }
         }
@@ -772,7 +847,8 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
         int nst = 0;  // stores issued by this warp (buffer = nst & 1)
         for (int p = 0; p < S; ++p) {
             if (warp == 9 && lane == 0 && rank == 0) {
-                constexpr uint32_t idesc = tc::make_idesc_tf32(2 * TC_M, NF, 0, 0);
+                constexpr uint32_t idesc =
+                    F16 ? tc::make_idesc_f16(2 * TC_M, NF, 0, 0) : tc::make_idesc_tf32(2 * TC_M, NF, 0, 0);
                 tc::mbar_wait(&tempty, ((uint32_t)p & 1u) ^ 1u);
                 tc::tc_fence_after();
                 const uint32_t dbig = tmem, dsmall = tmem + NF;
@@ -788,16 +864,28 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                     const uint64_t ah = tc::make_sdesc(stage, 16, 256, 6), al = tc::make_sdesc(stage + Cfg::A_T, 16, 256, 6);
                     const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 16, 256, 6);
                     const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 16, 256, 6);
-                    tc::mma_tf32_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
-                    tc::mma_tf32_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+                    if constexpr (F16) {
+                        tc::mma_f16_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
+                        tc::mma_f16_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+                        tc::mma_f16_pair(dsmall, al, bh, idesc, 1u);
+                    } else {
+                        tc::mma_tf32_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
+                        tc::mma_tf32_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
 #ifndef PNX_EXP_TWO_MMA  // timing experiment only: drops a product
-                    tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
+                        tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
 #endif
+                    }
                     tc::mma_commit_pair(&empty[st], 3);
                 }
                 tc::mma_commit_pair(&tfull, 3);
             }
             __syncwarp();
+            float usA = 1.0f, usW = 1.0f;  // 3xFP16 unscale 2^-eA, 2^-eW
+            if constexpr (F16) {
+                usA = ldexpf(1.0f, -a_exp(p));
+                usW = ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w));
+            }
+            unsigned mx = 0;
             tc::mbar_wait(&tfull, (uint32_t)p & 1u);
             tc::tc_fence_after();
             TC_T0();
@@ -816,9 +904,16 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                 }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) a[j] += b[j];
+                if constexpr (F16) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) a[j] = a[j] * usA * usW;
+                }
                 if (p == 0) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) mx = max(mx, tc::abs_bits(a[j]));
                 }
                 const uint32_t stg = stg0 + (uint32_t)(nst & 1) * Cfg::EPI_TILE;
                 if (lane == 0) tc::bulk_wait_read<1>();  // the store that last used this buffer has read it
@@ -835,6 +930,7 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                 }
                 ++nst;
             }
+            if (p > 0 && g.amax_out) tc::warp_amax(g.amax_out + p, mx);
             if (warp == 9 && lane == 0) TC_ACC(3);
         }
         if (lane == 0) tc::bulk_wait<0>();

@@ -28,7 +28,7 @@ from . import _lib
 ACTIVATIONS = {"tanh": 0, "sine": 1, "swish": 2}
 PDES = {"advection": 0, "allen_cahn": 1, "burgers": 2, "maxwell_te": 3, "ns_steady": 4}
 BCS = {"hard": 0, "soft_periodic": 1, "dirichlet_zero": 2}
-ENGINES = {"auto": 0, "ffma": 1, "tc3xtf32": 2}
+ENGINES = {"auto": 0, "ffma": 1, "tc3xtf32": 2, "tc3xf16": 3}
 
 
 class TensorError(RuntimeError):

@@ -123,7 +123,7 @@ def _spec_json(s):
     return j
 
 
-@pytest.mark.parametrize("engine", ["ffma", "auto"])
+@pytest.mark.parametrize("engine", ["ffma", "auto", "tc3xf16"])
 @pytest.mark.parametrize("cfg,dims,workers", [
     ("c1", [40, 30], 1), ("c1", [40, 30], 3),
     ("c2", [32, 24], 1),

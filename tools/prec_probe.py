@@ -17,6 +17,6 @@ for cfg, dims in [("c2", [32, 24]), ("c3", [24, 20]), ("c4", [12, 10, 8]), ("c4"
     e = np.abs(g - ref)
     print(cfg, dims, sys.argv[1], "mask", sys.argv[2], "rel_l2 %%.2e  max_rel_elem %%.2e" %% (T.rel_l2(g, ref), (e / (np.abs(ref).max())).max()), flush=True)
 ''' % (ROOT, ROOT)
-for eng, mask in [("ffma", "0"), ("auto", "1"), ("auto", "2"), ("auto", "4"), ("auto", "7")]:
+for eng, mask in [("ffma", "0"), ("auto", "1"), ("auto", "2"), ("auto", "4"), ("auto", "7"), ("tc3xf16", "1"), ("tc3xf16", "7")]:
     env = dict(os.environ, PNX_TC_MASK=mask)
     subprocess.run([sys.executable, "-c", code, eng, mask], env=env)

@@ -6,7 +6,7 @@ using namespace pnx::tc;
 // mode 0: 1 MMA per k-step per acc (A_k, B_k)
 // mode 1: 3 MMAs per k-step per acc: (Ah,Bh) (Ah,Bl) (Al,Bh)
 // mode 2: like 1 but accumulators interleaved innermost
-__global__ void rate(int N, int nacc, int iters, int mode, int rnd, long long* out) {
+__global__ void rate(int N, int nacc, int iters, int mode, int rnd, int f16, long long* out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint64_t bar;
@@ -14,13 +14,15 @@ __global__ void rate(int N, int nacc, int iters, int mode, int rnd, long long* o
     unsigned s = 12345u + threadIdx.x;
     for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) {
         s = s * 1664525u + 1013904223u;
-        ((float*)smem)[i] = rnd ? ((s >> 9) * (1.0f / 8388608.0f) - 0.5f) : 0.5f;
+        const float v = rnd ? ((s >> 9) * (1.0f / 8388608.0f) - 0.5f) : 0.5f;
+        if (f16) ((uint32_t*)smem)[i] = pack_half2(v, -v); else ((float*)smem)[i] = v;
     }
     fence_proxy_async_smem();
     if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
     if (threadIdx.x < 32) tmem_alloc<512>(&tbase);
     tc_fence_before(); __syncthreads(); tc_fence_after();
-    const uint32_t id = make_idesc_tf32(128, N, 0, 0);
+    const uint32_t id = f16 ? make_idesc_f16(128, N, 0, 0) : make_idesc_tf32(128, N, 0, 0);
+#define mma_tf32(d, a, b, i, acc) (f16 ? mma_f16(d, a, b, i, acc) : mma_tf32(d, a, b, i, acc))
     const uint32_t sb = smem_u32(smem);
     long long t0 = clock64();
     if (threadIdx.x == 0) {
@@ -61,14 +63,15 @@ int main() {
     cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     int cfg[][4] = {{256, 1, 3, 1}, {128, 1, 3, 1}, {128, 2, 3, 1}, {64, 4, 3, 1}, {128, 1, 0, 0}, {128, 1, 0, 1}, {128, 1, 1, 0}, {128, 1, 1, 1}, {128, 4, 1, 1}, {128, 4, 2, 1},
                     {64, 8, 1, 1}, {64, 8, 2, 1}, {256, 2, 1, 1}, {256, 2, 2, 1}, {128, 4, 0, 1}, {64, 8, 0, 1}};
+    for (int f16 = 0; f16 < 2; ++f16)
     for (auto& c : cfg) {
-        rate<<<1, 128, 100 * 1024>>>(c[0], c[1], 2000, c[2], c[3], d);
+        rate<<<1, 128, 100 * 1024>>>(c[0], c[1], 2000, c[2], c[3], f16, d);
         cudaDeviceSynchronize();
         long long cyc; cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
         double nm = 2000.0 * c[1] * (c[2] == 0 ? 1 : 3);
         double per = (double)cyc / nm;
-        printf("N=%3d nacc=%d mode=%d rnd=%d: %6.1f cyc/MMA -> %4.0f flop/cyc (%.0f%% of 4096)\n", c[0], c[1], c[2], c[3], per,
-               2.0 * 128 * c[0] * 8 / per, 100.0 * 2.0 * 128 * c[0] * 8 / per / 4096);
+        printf("%s N=%3d nacc=%d mode=%d rnd=%d: %6.1f cyc/MMA -> %4.0f flop/cyc (%.0f%% of 4096 tf32)\n", f16 ? "f16 K=16" : "tf32 K=8", c[0], c[1], c[2], c[3], per,
+               2.0 * 128 * c[0] * (f16 ? 16 : 8) / per, 100.0 * 2.0 * 128 * c[0] * (f16 ? 16 : 8) / per / 4096);
     }
     return 0;
 }

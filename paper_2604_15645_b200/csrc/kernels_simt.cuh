@@ -771,6 +771,7 @@ constexpr int kHeadWarps = 8;
 struct HeadArgs {
     const float* Z;      // [S][Rpad][H]
     float* Zb;           // [S][Rpad][H]
+    unsigned* zb_amax;   // optional: per-stream |Zb| bound (float bits, 3xFP16 scales)
     const float* W;      // [H][F]
     const float* b;      // [F]
     int H, Rpad, nrows;
@@ -827,6 +828,9 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 2) k_head(HeadArgs a) {
     for (int i = lane; i < acc_ld; i += 32) accw[i] = 0.0;
     __syncthreads();
 
+    unsigned zmx[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) zmx[s] = 0;
     float accW[J][F];
     float accB[F];
 #pragma unroll
@@ -1026,7 +1030,10 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 2) k_head(HeadArgs a) {
                 if (k < a.H) {
                     act_bwd<L, ACT>(zz, hb, zb, a.w0);
 #pragma unroll
-                    for (int s = 0; s < S; ++s) a.Zb[s * RH + (int64_t)r * a.H + k] = zb[s];
+                    for (int s = 0; s < S; ++s) {
+                        a.Zb[s * RH + (int64_t)r * a.H + k] = zb[s];
+                        zmx[s] = max(zmx[s], __float_as_uint(fabsf(zb[s])));
+                    }
                 }
             }
 #pragma unroll
@@ -1056,6 +1063,13 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 2) k_head(HeadArgs a) {
     }
     if (a.values_only) return;
     flush();
+    if (a.zb_amax) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const unsigned v = __reduce_max_sync(0xffffffffu, zmx[s]);
+            if (lane == 0) atomicMax(a.zb_amax + s, v);
+        }
+    }
     // pad rows of the chunk: zero adjoints so they contribute nothing
     for (int r2 = a.nrows + gw; r2 < a.Rpad; r2 += nw)
         for (int k = lane; k < a.H; k += 32)

@@ -57,10 +57,10 @@ int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? 0 : -1;
 }
-template <int L, bool PAIR>
+template <int L, bool PAIR, bool F16>
 int launch_tc5_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc5BwdCfg<L, PAIR>;
-    auto kern = k_tc5_bwd<L, PAIR>;
+    auto kern = k_tc5_bwd<L, PAIR, F16>;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
@@ -68,7 +68,8 @@ int launch_tc5_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
         attr = true;
     }
     TcGemmArgs a = g;
-    if (PAIR && tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)(g.K / 8) * 2 * Cfg::NF, 1, 8, Cfg::NFL, 1, false))
+    if (PAIR && tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)(g.K / (F16 ? 16 : 8)) * 2 * Cfg::NF, 1, 8, Cfg::NFL, 1,
+                             false))
         return -1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.Rpad / TC_M);
@@ -90,9 +91,15 @@ int launch_tc_layer_l(int mode, int pro, const TcGemmArgs& g, cudaStream_t st) {
         // the pair variant is bit-identical but not faster (the MMA phase is shared-
         // memory bound, tools/trace_bwd5.cu), so it is opt-in
         static const bool pair5 = getenv("PNX_TC5_PAIR") != nullptr;
-        if (tc5_bwd_ok(L, g.N, g.K))
-            return pair5 && g.Rpad % 256 == 0 ? launch_tc5_bwd_t<L, true>(g, st) : launch_tc5_bwd_t<L, false>(g, st);
+        if (tc5_bwd_ok(L, g.N, g.K)) {
+            if (g.f16)
+                return pair5 && g.Rpad % 256 == 0 ? launch_tc5_bwd_t<L, true, true>(g, st)
+                                                  : launch_tc5_bwd_t<L, false, true>(g, st);
+            return pair5 && g.Rpad % 256 == 0 ? launch_tc5_bwd_t<L, true, false>(g, st)
+                                              : launch_tc5_bwd_t<L, false, false>(g, st);
+        }
     }
+    if (g.f16) return -1;  // 3xFP16 only in the decoupled backward
     constexpr int NT = tc_nt(Streams<L>::S);
     (void)mode;
     (void)pro;

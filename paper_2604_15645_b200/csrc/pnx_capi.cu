@@ -370,7 +370,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
     bool tc_fwd[kMaxLayers] = {}, tc_bwd[kMaxLayers] = {}, tc_wg[kMaxLayers] = {};
     // 3xFP16 per layer: the pair forward, fed by a producer that records |Z| bounds
     // (the fused layer 0 or another pair forward)
-    bool f16_fwd[kMaxLayers] = {};
+    bool f16_fwd[kMaxLayers] = {}, f16_bwd[kMaxLayers] = {};
     // debug/ablation: PNX_TC_MASK bit0 forward, bit1 reverse, bit2 weight-gradient (default all)
     static const int tc_mask = getenv("PNX_TC_MASK") ? atoi(getenv("PNX_TC_MASK")) : 7;
     if (tc_on) {
@@ -404,6 +404,11 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 f16_fwd[l] = f16 && pairf && rec;
                 rec = pairf;
             }
+            // backward: Zb_out bounds come from the head (last hidden layer) or the
+            // decoupled backward of layer l+1 (both record them)
+            const bool recb = l == ctx->depth - 1 ||
+                              (tc_bwd[l + 1] && (tc_mask & 2) && tc5_bwd_ok(L, t.K[l + 1], t.N[l + 1]));
+            if (tc_bwd[l] && f16 && recb && tc5_bwd_ok(L, t.K[l], t.N[l])) f16_bwd[l] = true;
             if (f16_fwd[l]) {
                 k_tc_prep_image16<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 0, t.N[l], amax_w(ctx, l),
                                                       reinterpret_cast<uint16_t*>(ctx->tc.img + ctx->tc.img_fwd[l]));
@@ -413,7 +418,11 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                                                     ctx->tc.img + ctx->tc.img_fwd[l]);
                 CKL();
             }
-            if (tc_bwd[l]) {
+            if (f16_bwd[l]) {
+                k_tc_prep_image16<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 1, 256, amax_w(ctx, l),
+                                                      reinterpret_cast<uint16_t*>(ctx->tc.img + ctx->tc.img_bwd[l]));
+                CKL();
+            } else if (tc_bwd[l]) {
                 k_tc_prep_image<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 1,
                                                     tc5_bwd_ok(L, t.K[l], t.N[l]) ? 256 : NT,
                                                     ctx->tc.img + ctx->tc.img_bwd[l]);
@@ -477,6 +486,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         HeadArgs h{};
         h.Z = ctx->d_Z[ctx->depth - 1];
         h.Zb = ctx->d_Zb[0];
+        h.zb_amax = amax_zb(ctx, ctx->depth - 1);
         h.W = ctx->d_W + t.dW[Lw - 1];
         h.b = ctx->d_bias + t.dB[Lw - 1];
         h.H = ctx->H;
@@ -646,6 +656,10 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                         tg.Rpad = Rpad;
                         tg.K = g.K;
                         tg.N = g.N;
+                        tg.f16 = f16_bwd[l] ? 1 : 0;
+                        tg.amax_in = amax_zb(ctx, l);
+                        tg.amax_w = amax_w(ctx, l);
+                        tg.amax_out = amax_zb(ctx, l - 1);
                         if (launch_tc_layer(L, 1, ACT_NONE, tg, st)) return fail(ctx, PNX_ERR_CUDA, "tc backward launch");
                         CKL();
                     } else {

@@ -1316,7 +1316,10 @@ struct Tc5BwdCfg {
     __host__ __device__ static constexpr int sb(int pass) { return pass == 0 ? 2 : (S == 4 ? 0 : -1); }
 };
 
-template <int L, bool PAIR>
+// F16: 3xFP16 operands (kind::f16, K = 16 per stage) scaled by the recorded
+// |Zb_out| bounds g.amax_in and |W| bound g.amax_w; the epilogue unscales and
+// records the |Zb_in| bounds in g.amax_out.
+template <int L, bool PAIR, bool F16 = false>
 __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constant__ TcGemmArgs g) {
     using Cfg = Tc5BwdCfg<L, PAIR>;
     constexpr int NST = Cfg::NST, NF = Cfg::NF;
@@ -1329,8 +1332,21 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0;
     const int r0 = PAIR ? (int)(blockIdx.x >> 1) * 256 + (int)rank * 128 : (int)blockIdx.x * TC_M;
-    const int nkb = g.K / 8;
+    const int nkb = g.K / (F16 ? 16 : 8);
     const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * NF;
+    // weight stage copy of k-step kk into `stage` (tid 0 of the producers)
+    auto load_w = [&](int kk, int st, uint32_t stage, uint32_t full0) {
+        if constexpr (PAIR) {
+            // image rows (32 B each) of k-step kk: [hi: 256 rows][lo: 256 rows]
+            const int rowb = kk * 2 * NF + (int)rank * Cfg::NFL;
+            if (rank == 0) tc::mbar_arrive_expect_tx(&full[st], 2 * 2 * Cfg::B_T);
+            tc::tma_load_2d_pair(stage + 4 * Cfg::A_T, &g.tmB, 0, rowb, full0 + st * 8);
+            tc::tma_load_2d_pair(stage + 4 * Cfg::A_T + Cfg::B_T, &g.tmB, 0, rowb + NF, full0 + st * 8);
+        } else {
+            tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
+            tc::bulk_g2s(stage + 4 * Cfg::A_T, g.img + (int64_t)kk * (2 * Cfg::B_T / 4), 2 * Cfg::B_T, &full[st]);
+        }
+    };
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             tc::mbar_init(&full[i], PAIR ? 17 : 9);  // producer warps (both CTAs) + expect_tx
@@ -1355,7 +1371,68 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
     const uint32_t full0 = PAIR ? tc::mapa(tc::smem_u32(&full[0]), 0) : tc::smem_u32(&full[0]);
     const uint32_t tempty_all0 = PAIR ? tc::mapa(tc::smem_u32(&tempty_all), 0) : tc::smem_u32(&tempty_all);
 
-    if (warp < 8) {
+    if (F16 && warp < 8) {
+        // ---------------- producers (3xFP16): one 16-wide k-step per stage ----------------
+        const int prow = tid >> 1, pc = tid & 1;
+        const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 8;
+        const uint32_t aoff = tc::sw32_chunk((uint32_t)prow, (uint32_t)pc);
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            const int s0 = Cfg::sa(pass), s1 = Cfg::sb(pass);
+            const float sc0 = ldexpf(1.0f, tc::f16_exp_bits(g.amax_in[s0]));
+            const float sc1 = s1 >= 0 ? ldexpf(1.0f, tc::f16_exp_bits(g.amax_in[s1])) : 1.0f;
+            constexpr int D = 2;  // k-steps of A prefetched in registers
+            float4 ra[D][2], rb[D][2];
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    ra[d][u] = d < nkb ? ldg4(asrc + s0 * RK + d * 16 + 4 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    rb[d][u] = (s1 >= 0 && d < nkb) ? ldg4(asrc + s1 * RK + d * 16 + 4 * u)
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            if (pass == 1) tc::mbar_wait(&tempty, 0);  // the epilogue released the stage ring
+#pragma unroll 1
+            for (int kb0 = 0; kb0 < nkb; kb0 += D)
+#pragma unroll
+                for (int cur = 0; cur < D; ++cur) {
+                    const int kb = kb0 + cur;
+                    if (kb >= nkb) break;
+                    uint4 ahi, alo, bhi, blo;
+                    {
+                        const float ha[8] = {ra[cur][0].x, ra[cur][0].y, ra[cur][0].z, ra[cur][0].w,
+                                             ra[cur][1].x, ra[cur][1].y, ra[cur][1].z, ra[cur][1].w};
+                        const float hb[8] = {rb[cur][0].x, rb[cur][0].y, rb[cur][0].z, rb[cur][0].w,
+                                             rb[cur][1].x, rb[cur][1].y, rb[cur][1].z, rb[cur][1].w};
+                        tc::split_h8(ha, sc0, ahi, alo);
+                        tc::split_h8(hb, sc1, bhi, blo);
+                    }
+                    if (kb + D < nkb) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            ra[cur][u] = ldg4(asrc + s0 * RK + (kb + D) * 16 + 4 * u);
+                            if (s1 >= 0) rb[cur][u] = ldg4(asrc + s1 * RK + (kb + D) * 16 + 4 * u);
+                        }
+                    }
+                    const int it = pass * nkb + kb, st = it % NST;
+                    const uint32_t stage = sbase + st * Cfg::STAGE;
+                    tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                    if (tid == 0) load_w(kb, st, stage, full0);
+                    sts128u(stage + aoff, ahi);
+                    sts128u(stage + Cfg::A_T + aoff, alo);
+                    if (s1 >= 0) {
+                        sts128u(stage + 2 * Cfg::A_T + aoff, bhi);
+                        sts128u(stage + 3 * Cfg::A_T + aoff, blo);
+                    }
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (PAIR) tc::mbar_arrive_cluster(full0 + st * 8);
+                        else tc::mbar_arrive(&full[st]);
+                    }
+                }
+        }
+    } else if (warp < 8) {
         // ---------------- producers: A tiles of the pass's two streams ----------------
         const int prow = tid >> 1, pc = tid & 1;
         const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
@@ -1398,20 +1475,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                         tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
                         if (tid == 0) TC_ACC(2);
                     }
-                    if (tid == 0) {
-                        const int kk = kb + u;
-                        if constexpr (PAIR) {
-                            // image rows (8 fp32 each) of k-step kk: [hi: 256 rows][lo: 256 rows]
-                            const int rowb = kk * 2 * NF + (int)rank * Cfg::NFL;
-                            if (rank == 0) tc::mbar_arrive_expect_tx(&full[st], 2 * 2 * Cfg::B_T);
-                            tc::tma_load_2d_pair(stage + 4 * Cfg::A_T, &g.tmB, 0, rowb, full0 + st * 8);
-                            tc::tma_load_2d_pair(stage + 4 * Cfg::A_T + Cfg::B_T, &g.tmB, 0, rowb + NF, full0 + st * 8);
-                        } else {
-                            tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
-                            tc::bulk_g2s(stage + 4 * Cfg::A_T, g.img + (int64_t)kk * (2 * Cfg::B_T / 4), 2 * Cfg::B_T,
-                                         &full[st]);
-                        }
-                    }
+                    if (tid == 0) load_w(kb + u, st, stage, full0);
                     sts128(stage + aoff, h[u][0]);
                     sts128(stage + Cfg::A_T + aoff, h[u][1]);
                     if (s1 >= 0) {
@@ -1433,7 +1497,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
     } else if (warp == 8) {
         // ---------------- MMA issuer ----------------
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NF, 0, 0);
+            constexpr uint32_t idesc = F16 ? tc::make_idesc_f16(PAIR ? 2 * TC_M : TC_M, NF, 0, 0)
+                                           : tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NF, 0, 0);
             for (int pass = 0; pass < 2; ++pass) {
                 const bool two = Cfg::sb(pass) >= 0;
                 if (pass == 1) tc::mbar_wait(&tempty_all, 0);
@@ -1455,7 +1520,15 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                         const uint32_t ah = stage + (2 * a) * Cfg::A_T;
                         const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(ah + Cfg::A_T, 16, 256, 6);
                         const uint32_t d = tmem + (uint32_t)(a * NF);
-                        if constexpr (PAIR) {
+                        if constexpr (F16 && PAIR) {
+                            tc::mma_f16_pair(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
+                            tc::mma_f16_pair(d, adh, bl, idesc, 1u);
+                            tc::mma_f16_pair(d, adl, bh, idesc, 1u);
+                        } else if constexpr (F16) {
+                            tc::mma_f16(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
+                            tc::mma_f16(d, adh, bl, idesc, 1u);
+                            tc::mma_f16(d, adl, bh, idesc, 1u);
+                        } else if constexpr (PAIR) {
                             tc::mma_tf32_pair(d, adh, bh, idesc, kb > 0 ? 1u : 0u);
                             tc::mma_tf32_pair(d, adh, bl, idesc, 1u);
 #ifndef PNX_EXP_TWO_MMA  // timing experiment only: drops a product
@@ -1507,6 +1580,13 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                 }
                 asm volatile("cp.async.commit_group;" ::: "memory");
             };
+            float usa = 1.0f, usb = 1.0f;  // 3xFP16 unscale of the two accumulators
+            if constexpr (F16) {
+                const float usw = ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w));
+                usa = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s0]));
+                if (s1 >= 0) usb = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s1]));
+            }
+            unsigned mxa = 0, mxb = 0;
             tc::mbar_wait(&tfull, (uint32_t)pass);
             tc::tc_fence_after();
             TC_T0();
@@ -1526,6 +1606,13 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                 }
                 __syncwarp();
                 tc::tmem_ld_wait();
+                if constexpr (F16) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        ha[j] *= usa;
+                        hb[j] *= usb;
+                    }
+                }
 #pragma unroll
                 for (int j4 = 0; j4 < 16; j4 += 4) {
                     const uint32_t ro = soff(lane, j4 >> 2);
@@ -1580,6 +1667,11 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                         for (int e = 0; e < 4; ++e)
                             sts32(pbuf + (uint32_t)(((cch * 16 + j4 + e) * 32 + lane) * 4), pp[e]);
                     }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        mxa = max(mxa, tc::abs_bits(oa[e]));
+                        mxb = max(mxb, tc::abs_bits(ob[e]));
+                    }
                     // outputs in place: stream s0 -> its z tile (the t tile when s0 = 0),
                     // stream s1 -> its z tile (the t tile when s1 = 0)
                     sts128(stg + (zA >= 0 ? Cfg::TILE : 0) + ro, make_float4(oa[0], oa[1], oa[2], oa[3]));
@@ -1599,6 +1691,10 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                     }
                 }
                 __syncwarp();
+            }
+            if (g.amax_out) {
+                tc::warp_amax(g.amax_out + s0, mxa);
+                if (s1 >= 0) tc::warp_amax(g.amax_out + s1, mxb);
             }
             if (warp == 9 && lane == 0) TC_ACC(3);
             tc::tc_fence_before();

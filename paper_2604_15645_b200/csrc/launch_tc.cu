@@ -187,11 +187,11 @@ int launch_tc2_fwd(int L, int pro, const TcGemmArgs& g, cudaStream_t st) {
     }
     return -1;
 }
-template <int L, int PRO, int NF, bool PAIR, bool F16C = false>
+template <int L, int PRO, int NF, bool PAIR, bool F16 = false>
 int launch_tc2_wgrad_t(const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st) {
     using Cfg = Tc2WgCfg<Streams<L>::S, NF, PAIR>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc2_wgrad<L, PRO, NF, PAIR, F16C>;
+    auto kern = k_tc2_wgrad<L, PRO, NF, PAIR, F16>;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
@@ -218,9 +218,8 @@ int launch_tc2_wgrad_t(const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t
 }
 template <int L, int NF, bool PAIR>
 int launch_tc2_wgrad_p(int pro, const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st) {
-    // two-MMA mode (fp16 correction products) when the producers recorded absmax bounds
-    static const bool f16c = getenv("PNX_F16CORR") != nullptr;
-    if (f16c && w.amaxA && w.amaxB)
+    // 3xFP16 operands (the producers recorded the per-stream bounds)
+    if (w.f16 && w.amaxA && w.amaxB)
         return pro == ACT_NONE ? launch_tc2_wgrad_t<L, ACT_NONE, NF, PAIR, true>(w, ntiles, wrows, st)
                                : launch_tc2_wgrad_t<L, ACT_TANH, NF, PAIR, true>(w, ntiles, wrows, st);
     return pro == ACT_NONE ? launch_tc2_wgrad_t<L, ACT_NONE, NF, PAIR>(w, ntiles, wrows, st)

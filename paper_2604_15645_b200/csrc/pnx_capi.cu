@@ -370,7 +370,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
     bool tc_fwd[kMaxLayers] = {}, tc_bwd[kMaxLayers] = {}, tc_wg[kMaxLayers] = {};
     // 3xFP16 per layer: the pair forward, fed by a producer that records |Z| bounds
     // (the fused layer 0 or another pair forward)
-    bool f16_fwd[kMaxLayers] = {}, f16_bwd[kMaxLayers] = {};
+    bool f16_fwd[kMaxLayers] = {}, f16_bwd[kMaxLayers] = {}, f16_wg[kMaxLayers] = {};
     // debug/ablation: PNX_TC_MASK bit0 forward, bit1 reverse, bit2 weight-gradient (default all)
     static const int tc_mask = getenv("PNX_TC_MASK") ? atoi(getenv("PNX_TC_MASK")) : 7;
     if (tc_on) {
@@ -399,15 +399,16 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         for (int l = 0; l < ctx->depth; ++l) {
             tc_wg[l] = tc_fwd[l] && (tc_mask & 4);
             if (!(tc_mask & 2)) tc_bwd[l] = false;
-            if (l > 0) {
-                const bool pairf = tc_fwd[l] && (tc_mask & 1) && tc4_fwd_ok(t.K[l], t.N[l]);
-                f16_fwd[l] = f16 && pairf && rec;
-                rec = pairf;
-            }
             // backward: Zb_out bounds come from the head (last hidden layer) or the
             // decoupled backward of layer l+1 (both record them)
             const bool recb = l == ctx->depth - 1 ||
                               (tc_bwd[l + 1] && (tc_mask & 2) && tc5_bwd_ok(L, t.K[l + 1], t.N[l + 1]));
+            if (l > 0) {
+                const bool pairf = tc_fwd[l] && (tc_mask & 1) && tc4_fwd_ok(t.K[l], t.N[l]);
+                f16_fwd[l] = f16 && pairf && rec;
+                f16_wg[l] = f16 && tc_wg[l] && rec && recb;  // A = Z_{l-1}, B = Zb_l
+                rec = pairf;
+            }
             if (tc_bwd[l] && f16 && recb && tc5_bwd_ok(L, t.K[l], t.N[l])) f16_bwd[l] = true;
             if (f16_fwd[l]) {
                 k_tc_prep_image16<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 0, t.N[l], amax_w(ctx, l),
@@ -616,6 +617,9 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 tw.nrows = nrows;
                 tw.Kin = t.K[l];
                 tw.N = t.N[l];
+                tw.f16 = f16_wg[l] ? 1 : 0;
+                tw.amaxA = l > 0 ? amax_z(ctx, l - 1) : nullptr;
+                tw.amaxB = amax_zb(ctx, l);
                 const int wr = tc_wgrad_rows(Rpad, t.K[l], ctx->nsm);
                 const int ntl = (int)((Rpad + wr - 1) / wr);
                 if (launch_tc2_wgrad(L, pro, tw, ntl, wr, st)) return fail(ctx, PNX_ERR_CUDA, "tc wgrad launch");

@@ -196,10 +196,12 @@ struct TcGemmArgs {
 struct TcWgradArgs {
     const float* A;   // Z_in / Hin [S][Rpad][Kin]
     const float* Bm;  // Zb_out [S][Rpad][N]
-    // two-MMA mode: |A| and |B| bounds (float bits) from the producing kernels;
-    // the correction products run as one kind::f16 MMA on 2^s-scaled operands
+    // 3xFP16 mode: per-stream |Z_in| and |Zb_out| bounds (float bits) recorded
+    // by the producing kernels; one power-of-two scale per operand (the whole
+    // reduction over rows and streams accumulates into one TMEM accumulator)
     const unsigned* amaxA;
     const unsigned* amaxB;
+    int f16;
     CUtensorMap tmA;  // A as [S][Rpad][Kin], box {128, 8, S}
     CUtensorMap tmB;  // Bm as [S][Rpad][N], box {N, 8, S}
     float* wpart;
@@ -970,10 +972,16 @@ struct Tc2WgCfg {
     static_assert(NR * RAW >= 2 * 8 * NFL * 8, "db reduction reuses the raw ring");
 };
 
-template <int L, int PRO, int NF, bool PAIR, bool F16C = false>
+// F16: 3xFP16 operands. A stage is one kind::f16 K = 16 step: the same 8 rows
+// of two streams (k-rows 0-7 stream s, 8-15 stream s+1; a group's odd last
+// stream pads with zeros), fp16 MN-major 128 B-swizzled tiles of the same byte
+// size as the tf32 ones.
+template <int L, int PRO, int NF, bool PAIR, bool F16 = false>
 __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_constant__ TcWgradArgs g, int wrows) {
     using St = Streams<L>;
     constexpr int S = St::S;
+    constexpr int SG = (S + 1) / 2;                                   // streams of converter group 0
+    constexpr int NSTG = F16 ? (SG + 1) / 2 + (S - SG + 1) / 2 : S;  // MMA stages per 8-row block
     using Cfg = Tc2WgCfg<S, NF, PAIR>;
     constexpr int NST = Cfg::NST, NR = Cfg::NR, NFL = Cfg::NFL;
     extern __shared__ uint8_t smem_raw[];
@@ -987,7 +995,7 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
     const int rbeg = tile * wrows;
     const int rend = min(g.Rpad, rbeg + wrows);
     const int nblk = (rend - rbeg) / 8;
-    const int nit = nblk * S;
+    const int nit = nblk * NSTG;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             tc::mbar_init(&full[i], PAIR ? 16 : 8);  // the converter group(s) filling stage i
@@ -1011,12 +1019,24 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
     const uint32_t tmem = tmem_base;
     const uint32_t sraw = tc::smem_u32(smem);
     const uint32_t sbase = sraw + NR * Cfg::RAW;
-    // F16C: operand scales 2^sA, 2^sB (|h| <= max(1, |Z_in|) for tanh jets)
+    // F16: operand scales 2^sA, 2^sB from the largest per-stream bound
+    // (|act(z)[s]| <= 1 (value), |z_s| (first order), |z_aa| + 2 z_a^2 (second))
     int sA = 0, sB = 0;
-    if constexpr (F16C) {
-        const float ma = __uint_as_float(*g.amaxA);
-        sA = tc::f16_scale_exp(PRO == ACT_NONE ? ma : fmaxf(1.0f, ma));
-        sB = tc::f16_scale_exp(__uint_as_float(*g.amaxB));
+    if constexpr (F16) {
+        float ma = 0.0f, mb = 0.0f;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            float b = __uint_as_float(g.amaxA[s]);
+            if (PRO != ACT_NONE && s == 0) b = 1.0f;
+            if (PRO != ACT_NONE && St::order(s) == 2) {
+                const float a = __uint_as_float(g.amaxA[St::partner(s)]);
+                b = b + 2.0f * a * a;
+            }
+            ma = fmaxf(ma, b);
+            mb = fmaxf(mb, __uint_as_float(g.amaxB[s]));
+        }
+        sA = tc::f16_exp_bits(__float_as_uint(ma * 1.001f));
+        sB = tc::f16_exp_bits(__float_as_uint(mb));
     }
     const float scA = ldexpf(1.0f, sA), scB = ldexpf(1.0f, sB);
 
@@ -1029,17 +1049,13 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
         constexpr int BCH = NFL / 4;  // float4 chunks per row
         constexpr int NB = (8 * BCH + 255) / 256;
         int brow[2];
-        uint32_t boff[2], b16l[2], b16h[2];
+        uint32_t boff[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const int idx = gtid + 256 * j;
             brow[j] = j < NB ? idx / BCH : 8;
             boff[j] = tc::mn32_off((uint32_t)(brow[j] & 7), (uint32_t)((idx % BCH) * 4), (uint32_t)NFL);
-            b16l[j] = tc::mn16_off((uint32_t)(brow[j] & 7), (uint32_t)((idx % BCH) * 4), (uint32_t)NFL);
-            b16h[j] = tc::mn16_off((uint32_t)(8 + (brow[j] & 7)), (uint32_t)((idx % BCH) * 4), (uint32_t)NFL);
         }
-        const uint32_t a16h = tc::mn16_off((uint32_t)ar, (uint32_t)(ac * 4), 128u);
-        const uint32_t a16l = tc::mn16_off((uint32_t)(8 + ar), (uint32_t)(ac * 4), 128u);
         const uint32_t full0 = PAIR ? tc::mapa(tc::smem_u32(&full[0]), 0) : tc::smem_u32(&full[0]);
         double dbacc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
         for (int b = 0; b < nblk; ++b) {
@@ -1081,7 +1097,8 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                                             (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
                         }
                     }
-                    split4(h, ahi[i], alo[i]);
+                    if constexpr (F16) ahi[i] = h;
+                    else split4(h, ahi[i], alo[i]);
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         if (brow[j] >= 8) continue;
@@ -1092,12 +1109,66 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                             dbacc[j][2] += bv.z;
                             dbacc[j][3] += bv.w;
                         }
-                        split4(bv, bhi[i][j], blo[i][j]);
+                        if constexpr (F16) bhi[i][j] = bv;
+                        else split4(bv, bhi[i][j], blo[i][j]);
                     }
                 }
 #ifdef PNX_TC_TRACE
                 if (tid == 0) atomicAdd(&g_tc_trace[5], (unsigned long long)(clock64() - _tc));
 #endif
+                if constexpr (F16) {
+                    // stage (b, SOFF + i/2): k-rows 8*(i&1) + row of stream SLO + i
+                    constexpr int SOFF = SLO == 0 ? 0 : (SG + 1) / 2;
+                    auto st_h = [](uint32_t addr, float4 v, float sc, uint32_t lo_addr) {
+                        uint32_t h0, l0, h1, l1;
+                        tc::split_h2(v.x * sc, v.y * sc, h0, l0);
+                        tc::split_h2(v.z * sc, v.w * sc, h1, l1);
+                        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(h0), "r"(h1));
+                        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(lo_addr), "r"(l0), "r"(l1));
+                    };
+                    auto st_z = [](uint32_t addr) {
+                        asm volatile("st.shared.v2.b32 [%0], {%1, %1};" ::"r"(addr), "r"(0u));
+                    };
+#pragma unroll
+                    for (int i = 0; i < NS; ++i) {
+                        const int it = b * NSTG + SOFF + (i >> 1), st = it % NST, pos = i & 1;
+                        const uint32_t stage = sbase + st * Cfg::STAGE;
+                        if (pos == 0) tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                        // (ahi, alo) hold the unsplit values in the F16 mode
+                        const uint32_t ao = tc::mn16_off((uint32_t)(ar + 8 * pos), (uint32_t)(ac * 4), 128u);
+                        st_h(stage + ao, ahi[i], scA, stage + Cfg::A_T + ao);
+                        const bool pad = pos == 0 && i + 1 == NS;  // odd tail: zero k-rows 8-15
+                        if (pad) {
+                            const uint32_t az = tc::mn16_off((uint32_t)(ar + 8), (uint32_t)(ac * 4), 128u);
+                            st_z(stage + az);
+                            st_z(stage + Cfg::A_T + az);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            if (brow[j] >= 8) continue;
+                            const int idx = gtid + 256 * j;
+                            const uint32_t bo = tc::mn16_off((uint32_t)(brow[j] + 8 * pos), (uint32_t)((idx % BCH) * 4),
+                                                             (uint32_t)NFL);
+                            st_h(stage + 2 * Cfg::A_T + bo, bhi[i][j], scB, stage + 2 * Cfg::A_T + Cfg::B_T + bo);
+                            if (pad) {
+                                const uint32_t bz = tc::mn16_off((uint32_t)(brow[j] + 8), (uint32_t)((idx % BCH) * 4),
+                                                                 (uint32_t)NFL);
+                                st_z(stage + 2 * Cfg::A_T + bz);
+                                st_z(stage + 2 * Cfg::A_T + Cfg::B_T + bz);
+                            }
+                        }
+                    }
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int i = 0; i < NS; i += 2) {
+                            const int st = (b * NSTG + SOFF + (i >> 1)) % NST;
+                            if constexpr (PAIR) tc::mbar_arrive_cluster(full0 + st * 8);
+                            else tc::mbar_arrive(&full[st]);
+                        }
+                    }
+                } else {
 #pragma unroll
                 for (int i = 0; i < NS; ++i) {
                     const int it = b * S + SLO + i;
@@ -1112,32 +1183,12 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                     _tc = clock64();
 #endif
                     sts128(stage + aoff, ahi[i]);
-                    if constexpr (F16C) {
-                        // A' = [Ah | Al] (k = row, 8 + row), fp16 MN-major SW128, 2^sA-scaled
-                        const float4 h = ahi[i], l = alo[i];
-                        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + Cfg::A_T + a16h),
-                                     "r"(tc::pack_half2(h.x * scA, h.y * scA)), "r"(tc::pack_half2(h.z * scA, h.w * scA)));
-                        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + Cfg::A_T + a16l),
-                                     "r"(tc::pack_half2(l.x * scA, l.y * scA)), "r"(tc::pack_half2(l.z * scA, l.w * scA)));
-                    } else {
-                        sts128(stage + Cfg::A_T + aoff, alo[i]);
-                    }
+                    sts128(stage + Cfg::A_T + aoff, alo[i]);
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         if (brow[j] >= 8) continue;
                         sts128(stage + 2 * Cfg::A_T + boff[j], bhi[i][j]);
-                        if constexpr (F16C) {
-                            // B' = [Bl ; Bh] (k = row, 8 + row)
-                            const float4 h = bhi[i][j], l = blo[i][j];
-                            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + 2 * Cfg::A_T + Cfg::B_T + b16l[j]),
-                                         "r"(tc::pack_half2(l.x * scB, l.y * scB)),
-                                         "r"(tc::pack_half2(l.z * scB, l.w * scB)));
-                            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + 2 * Cfg::A_T + Cfg::B_T + b16h[j]),
-                                         "r"(tc::pack_half2(h.x * scB, h.y * scB)),
-                                         "r"(tc::pack_half2(h.z * scB, h.w * scB)));
-                        } else {
-                            sts128(stage + 2 * Cfg::A_T + Cfg::B_T + boff[j], blo[i][j]);
-                        }
+                        sts128(stage + 2 * Cfg::A_T + Cfg::B_T + boff[j], blo[i][j]);
                     }
                 }
                 tc::fence_proxy_async_smem();
@@ -1149,6 +1200,7 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                         if constexpr (PAIR) tc::mbar_arrive_cluster(full0 + st * 8);
                         else tc::mbar_arrive(&full[st]);
                     }
+                }
                 }
 #ifdef PNX_TC_TRACE
                 if (tid == 0) atomicAdd(&g_tc_trace[6], (unsigned long long)(clock64() - _tc));
@@ -1203,18 +1255,22 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                 const uint64_t al = tc::make_sdesc(stage + Cfg::A_T, 512, 4 * 512, 1);
                 const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 512, (NFL / 32) * 512, 1);
                 const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 512, (NFL / 32) * 512, 1);
-                if constexpr (F16C) {
-                    // hh in tf32; Ah.Bl + Al.Bh as one K=16 fp16 MMA (MN-major SW128, LBO 1024)
+                if constexpr (F16) {
+                    // fp16 MN-major SW128 tiles: LBO 1024 (next 64 MN), SBO = next 8 k-rows
                     constexpr uint32_t idesc16 = tc::make_idesc_f16(PAIR ? 2 * TC_M : TC_M, NF, 1, 1);
-                    const uint64_t a16 = tc::make_sdesc(stage + Cfg::A_T, 1024, 2 * 1024, 2);
-                    const uint64_t b16 = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 1024, (NFL / 64) * 1024, 2);
+                    const uint64_t a16h = tc::make_sdesc(stage, 1024, 2 * 1024, 2);
+                    const uint64_t a16l = tc::make_sdesc(stage + Cfg::A_T, 1024, 2 * 1024, 2);
+                    const uint64_t b16h = tc::make_sdesc(stage + 2 * Cfg::A_T, 1024, (NFL / 64) * 1024, 2);
+                    const uint64_t b16l = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 1024, (NFL / 64) * 1024, 2);
                     if constexpr (PAIR) {
-                        tc::mma_tf32_pair(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
-                        tc::mma_f16_pair(dsmall, a16, b16, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_f16_pair(dbig, a16h, b16h, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_f16_pair(dsmall, a16h, b16l, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_f16_pair(dsmall, a16l, b16h, idesc16, 1u);
                         tc::mma_commit_pair(&empty[st], 3);
                     } else {
-                        tc::mma_tf32(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
-                        tc::mma_f16(dsmall, a16, b16, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_f16(dbig, a16h, b16h, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_f16(dsmall, a16h, b16l, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_f16(dsmall, a16l, b16h, idesc16, 1u);
                         tc::mma_commit(&empty[st]);
                     }
                 } else if constexpr (PAIR) {
@@ -1258,15 +1314,16 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                 tc::tmem_ld16(tl + (uint32_t)c, a);
                 tc::tmem_ld16(tl + (uint32_t)(NF + c), b);
                 tc::tmem_ld_wait();
-                if constexpr (F16C) {
-                    const float us = ldexpf(1.0f, -(sA + sB));
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) b[j] *= us;
+                for (int j = 0; j < 16; ++j) a[j] += b[j];
+                if constexpr (F16) {
+                    const float usA = ldexpf(1.0f, -sA), usB = ldexpf(1.0f, -sB);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) a[j] = a[j] * usA * usB;
                 }
 #pragma unroll
                 for (int j = 0; j < 16; j += 4)
-                    *reinterpret_cast<float4*>(dst + c + j) =
-                        make_float4(a[j] + b[j], a[j + 1] + b[j + 1], a[j + 2] + b[j + 2], a[j + 3] + b[j + 3]);
+                    *reinterpret_cast<float4*>(dst + c + j) = make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]);
             }
         } else {
             for (int c = 0; c < NF; ++c) dst[c] = 0.0f;

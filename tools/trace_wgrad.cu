@@ -24,11 +24,12 @@ int main(int argc, char** argv) {
     std::vector<float> ref, out, out16;
     std::vector<double> dref, dout, dout16;
     unsigned* amax;
-    cudaMalloc(&amax, 8);
-    const float am[2] = {0.8f, 0.5f};  // |A| <= 0.8 (fill 1.6), |B| <= 0.5
-    cudaMemcpy(amax, am, 8, cudaMemcpyHostToDevice);
+    cudaMalloc(&amax, 2 * S * 4);
+    const float am[2 * S] = {0.8f, 0.8f, 0.8f, 0.8f, 0.5f, 0.5f, 0.5f, 0.5f};  // |A| <= 0.8 (fill 1.6), |B| <= 0.5
+    cudaMemcpy(amax, am, sizeof(am), cudaMemcpyHostToDevice);
     w.amaxA = amax;
-    w.amaxB = amax + 1;
+    w.amaxB = amax + S;
+    w.f16 = 1;
     for (int mode = 0; mode < 3; ++mode) {
         const bool pair = mode >= 1;
         for (int rep = 0; rep < 2; ++rep) {

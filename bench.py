@@ -408,7 +408,16 @@ def main():
         use_tc = args.engine != "ffma" and H in (128, 256) and wl.spec.activation == "tanh"
         bf16 = float(peaks.get("bf16_tflops_sustained", 1366.2))
         fp32_peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
-        if use_tc:
+        # the 3xFP16 kernels run where the CTA-pair paths apply (H = 256); "auto" picks them
+        use_f16 = use_tc and args.engine != "tc3xtf32" and H == 256
+        if use_f16:
+            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                    "frac": achieved / bf16,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense bf16, of measured)",
+                    "effective_peak": bf16 / 3.0, "frac_effective": achieved / (bf16 / 3.0),
+                    "effective_note": "3xFP16: tensor-pipe work = 3 x algorithmic flops at the fp16 rate "
+                                      "(= bf16), so the FP32-accurate peak = bf16/3 (derived)"}
+        elif use_tc:
             roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
                     "frac": achieved / bf16,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense bf16, of measured)",

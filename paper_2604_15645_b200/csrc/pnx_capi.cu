@@ -394,7 +394,8 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             CK(cudaMalloc(&ctx->tc.img, need * sizeof(float)));
             ctx->tc.img_cap = need;
         }
-        const bool f16 = ctx->engine == PNX_ENGINE_TC3XF16;
+        // AUTO: 3xFP16 wherever the kernels support it, 3xTF32 elsewhere
+        const bool f16 = ctx->engine == PNX_ENGINE_TC3XF16 || ctx->engine == PNX_ENGINE_AUTO;
         bool rec = layer0_fused(ctx);  // Z_{l-1} bounds recorded
         for (int l = 0; l < ctx->depth; ++l) {
             tc_wg[l] = tc_fwd[l] && (tc_mask & 4);

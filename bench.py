@@ -391,43 +391,61 @@ def main():
             peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         except Exception:
             pass
-        # roofline of the dominant kernel class (CUDA events on the launching stream):
-        # algorithmic flops of that class per step (2*S*rows*sum K*N over its
-        # layers) / its measured ms per step.
+        # roofline of the dominant kernel class (CUDA events on the launching stream).
+        # Algorithmic work per step of each class:
+        #   flops  2*S*rows*sum K*N over its layers
+        #   bytes  per row and hidden layer: fwd S*4*(K+N) (read act input, write out),
+        #          bwd S*4*(N+2K) (read Zb_out and Z_in, write Zb_in), wgrad S*4*(K+N);
+        #          layer 0 (fused): fwd 8*d + S*4*N0, wgrad S*4*N0
+        # The bound is whichever takes longer at peak; the other view is kept beside it.
         S = wl.streams()
         H = wl.spec.hidden_dim
         rows = hi - lo
         K0 = wl.spec.first_layer_width()
-        sum_fwd = K0 * H + H * H * (wl.spec.depth - 1)      # layers 0..depth-1 (head excluded)
-        sum_bwd = H * H * (wl.spec.depth - 1)               # reverse GEMMs of layers 1..depth-1
+        d_in = wl.spec.in_dim
+        nh = wl.spec.depth - 1                               # hidden->hidden layers
+        sum_fwd = K0 * H + H * H * nh                        # layers 0..depth-1 (head excluded)
+        sum_bwd = H * H * nh                                 # reverse GEMMs of layers 1..depth-1
         flops_cls = {"fwd_gemm": 2.0 * S * rows * sum_fwd, "bwd_gemm": 2.0 * S * rows * sum_bwd,
                      "wgrad_gemm": 2.0 * S * rows * sum_fwd}
+        bytes_cls = {"fwd_gemm": rows * (S * 4.0 * 2 * H * nh + S * 4.0 * H + 8.0 * d_in),
+                     "bwd_gemm": rows * S * 4.0 * 3 * H * nh,
+                     "wgrad_gemm": rows * (S * 4.0 * 2 * H * nh + S * 4.0 * H)}
         dom = max(flops_cls, key=lambda k: prof[k][0])
         tms, nl = prof[dom]
-        achieved = flops_cls[dom] * args.steps / (tms / 1e3) / 1e12
+        t_s = (tms / 1e3) / args.steps                       # class seconds per step
+        achieved = flops_cls[dom] / t_s / 1e12
+        achieved_gbs = bytes_cls[dom] / t_s / 1e9
         use_tc = args.engine != "ffma" and H in (128, 256) and wl.spec.activation == "tanh"
         bf16 = float(peaks.get("bf16_tflops_sustained", 1366.2))
+        hbm = float(peaks.get("hbm_gbs", 6546.2))
         fp32_peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
         # the 3xFP16 kernels run where the CTA-pair paths apply (H = 256); "auto" picks them
         use_f16 = use_tc and args.engine != "tc3xtf32" and H == 256
         if use_f16:
-            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                    "frac": achieved / bf16,
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense bf16, of measured)",
-                    "effective_peak": bf16 / 3.0, "frac_effective": achieved / (bf16 / 3.0),
-                    "effective_note": "3xFP16: tensor-pipe work = 3 x algorithmic flops at the fp16 rate "
-                                      "(= bf16), so the FP32-accurate peak = bf16/3 (derived)"}
+            eff, note = bf16 / 3.0, ("3xFP16: tensor-pipe work = 3 x algorithmic flops at the fp16 rate "
+                                     "(= bf16), so the FP32-accurate peak = bf16/3 (derived)")
         elif use_tc:
-            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                    "frac": achieved / bf16,
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (dense bf16, of measured)",
-                    "effective_peak": bf16 / 6.0, "frac_effective": achieved / (bf16 / 6.0),
-                    "effective_note": "3xTF32: tensor-pipe work = 3 x algorithmic flops at the TF32 rate "
-                                      "(= bf16/2), so FP32-accurate peak = bf16/6 (derived)"}
+            eff, note = bf16 / 6.0, ("3xTF32: tensor-pipe work = 3 x algorithmic flops at the TF32 rate "
+                                     "(= bf16/2), so FP32-accurate peak = bf16/6 (derived)")
         else:
-            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                    "frac": achieved / fp32_peak,
-                    "peak_source": "FP32 FFMA pipe: 148 SM x 128 lanes x 2 x sm_max_mhz (derived)"}
+            eff, note = fp32_peak, "FP32 FFMA pipe: 148 SM x 128 lanes x 2 x sm_max_mhz (derived)"
+        tensor_view = {"achieved": achieved, "unit": "TFLOP/s",
+                       "peak": bf16 if use_tc else fp32_peak, "frac": achieved / (bf16 if use_tc else fp32_peak),
+                       "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (dense bf16, of measured)"
+                                       if use_tc else note),
+                       "effective_peak": eff, "frac_effective": achieved / eff, "effective_note": note,
+                       "flops_per_step": flops_cls[dom]}
+        hbm_view = {"achieved": achieved_gbs, "unit": "GB/s", "peak": hbm, "frac": achieved_gbs / hbm,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy read+write, measured)",
+                    "bytes_per_step": bytes_cls[dom]}
+        hbm_bound = bytes_cls[dom] / (hbm * 1e9) > flops_cls[dom] / (eff * 1e12)
+        main, other = (hbm_view, tensor_view) if hbm_bound else (tensor_view, hbm_view)
+        roof = {"bound": "hbm" if hbm_bound else "tensor", "kernel": dom, **main,
+                "other_view": other,
+                "t_min_ms": {"hbm": 1e3 * bytes_cls[dom] / (hbm * 1e9),
+                             "tensor_effective": 1e3 * flops_cls[dom] / (eff * 1e12),
+                             "measured": 1e3 * t_s}}
         traffic_db = {}
         try:
             traffic_db = json.load(open(os.path.join(ROOT, "profiles", "kernel_traffic.json")))
@@ -435,6 +453,8 @@ def main():
             pass
         key = f"{name}:{dom}"
         roof["traffic"] = traffic_db.get(key)
+        # one hidden-layer launch's algorithmic bytes, the comparand of `traffic`
+        roof["algorithmic_bytes_per_launch"] = rows * S * 4.0 * H * (3 if dom == "bwd_gemm" else 2)
         roof["launches_per_step"] = nl / args.steps
         step_flops = wl.flops_per_point() * n_total
         line = {

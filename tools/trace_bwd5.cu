@@ -32,8 +32,8 @@ int main(int argc, char** argv) {
             cudaMemcpyToSymbol(g_tc_trace, z, sizeof(z));
             cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
             cudaEventRecord(e0);
-            const int rc = mode == 2 ? launch_tc5_bwd_t<LAY_MX, true>(g, 0)
-                         : mode == 1 ? launch_tc5_bwd_t<LAY_MX, false>(g, 0) : launch_tc2_bwd_t<LAY_MX, 128, false>(g, 0);
+            const int rc = mode == 2 ? launch_tc5_bwd_t<LAY_MX, true, false>(g, 0)
+                         : mode == 1 ? launch_tc5_bwd_t<LAY_MX, false, false>(g, 0) : launch_tc2_bwd_t<LAY_MX, 128, false>(g, 0);
             cudaError_t le = cudaGetLastError();
             if (rc || le != cudaSuccess) printf("launch rc=%d %s\n", rc, cudaGetErrorString(le));
             cudaEventRecord(e1);

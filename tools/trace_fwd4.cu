@@ -30,7 +30,7 @@ int main(int argc, char** argv) {
             cudaMemcpyToSymbol(g_tc_trace, z, sizeof(z));
             cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
             cudaEventRecord(e0);
-            const int rc = mode ? launch_tc4_fwd_t<LAY_MX, ACT_TANH>(g, 0) : launch_tc2_fwd_t<LAY_MX, ACT_TANH, 256>(g, 0);
+            const int rc = mode ? launch_tc4_fwd_t<LAY_MX, ACT_TANH, false>(g, 0) : launch_tc2_fwd_t<LAY_MX, ACT_TANH, 256>(g, 0);
             cudaError_t le = cudaGetLastError();
             if (rc || le != cudaSuccess) printf("launch rc=%d %s\n", rc, cudaGetErrorString(le));
             cudaEventRecord(e1);

@@ -651,7 +651,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
 //             completing on the leader's full barrier (.cta_group::2 TMA)
 //   warps 0-7  : converters -- jet activation + hi/lo split of a whole 4-k-step
 //                group per thread, SW32 stores, one proxy fence per group
-//   warps 9-16 : epilogue (warp 9 lane 0 of the leader also issues the MMAs)
+//   warps 9-16 : epilogue
+//   warp 18 : lane 0 of the leader issues the MMAs
 template <int L>
 struct Tc4FwdCfg {
     using St = Streams<L>;
@@ -663,7 +664,10 @@ struct Tc4FwdCfg {
     static constexpr int BOX = 128 * 32 * 4;   // 128 rows x 32 features
     static constexpr int NBOX = SECOND ? 3 : 2;
     static constexpr int RAW = NBOX * BOX;
-    static constexpr int NR = 2;
+    // raw ring depth: 3 groups in flight for first-order layouts (2 for second-order,
+    // whose 3-box groups leave no room); tools/trace_fwd4.cu: 3 slots + the MMA warp
+    // cut the 3xFP16 forward by 5.5%
+    static constexpr int NR = SECOND ? 2 : 3;
     static constexpr int EPI_TILE = 32 * 128;       // 32 rows x 32 fp32, 128 B swizzled (TMA store box)
     static constexpr int EPI_BYTES = 8 * 2 * EPI_TILE;  // 8 warps x 2 buffers
     static constexpr int BUDGET = 226 * 1024;
@@ -672,7 +676,10 @@ struct Tc4FwdCfg {
     static constexpr int SMEM = NR * RAW + NST * STAGE + EPI_BYTES + 1024;
     static_assert(NST >= 4, "forward stage ring");
 };
-constexpr int TC4_THREADS = 576;  // 18 warps
+// warp 18 issues the MMAs, so stream p+1 starts as soon as the epilogue warps
+// have read stream p's accumulators (not after warp 9's own stores)
+constexpr bool kFwdMmaWarp = true;
+constexpr int TC4_THREADS = 608;  // 19 warps
 
 // F16: 3xFP16 operands (kind::f16, K = 16 per stage) scaled by the recorded
 // bounds g.amax_in / g.amax_w; the epilogue unscales and records g.amax_out.
@@ -684,7 +691,7 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
     constexpr int NST = Cfg::NST, NR = Cfg::NR, NF = Cfg::NF, NFL = Cfg::NFL;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
-    __shared__ uint64_t full[8], empty[8], rfull[2], rempty[2], tfull, tempty;
+    __shared__ uint64_t full[8], empty[8], rfull[NR], rempty[NR], tfull, tempty;
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -729,6 +736,45 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
     // raw boxes a pass needs: [0] = stream 0 (t), [1] = stream p, [2] = partner
     auto nbox = [](int p) { return PRO == ACT_NONE ? 1 : (p == 0 ? 1 : (St::order(p) == 2 ? 3 : 2)); };
 
+    // MMAs of stream p (one elected thread of the pair leader)
+    auto issue_stream = [&](int p) {
+        constexpr uint32_t idesc =
+            F16 ? tc::make_idesc_f16(2 * TC_M, NF, 0, 0) : tc::make_idesc_tf32(2 * TC_M, NF, 0, 0);
+        {
+            TC_T0();
+            tc::mbar_wait(&tempty, ((uint32_t)p & 1u) ^ 1u);
+            TC_ACC(1);
+        }
+        tc::tc_fence_after();
+        const uint32_t dbig = tmem, dsmall = tmem + NF;
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int it = p * nkb + kb, st = it % NST;
+            const uint32_t stage = sbase + st * Cfg::STAGE;
+            {
+                TC_T0();
+                tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
+                TC_ACC(0);
+            }
+            tc::tc_fence_after();
+            const uint64_t ah = tc::make_sdesc(stage, 16, 256, 6), al = tc::make_sdesc(stage + Cfg::A_T, 16, 256, 6);
+            const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 16, 256, 6);
+            const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 16, 256, 6);
+            if constexpr (F16) {
+                tc::mma_f16_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
+                tc::mma_f16_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+                tc::mma_f16_pair(dsmall, al, bh, idesc, 1u);
+            } else {
+                tc::mma_tf32_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
+                tc::mma_tf32_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+#ifndef PNX_EXP_TWO_MMA  // timing experiment only: drops a product
+                tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
+#endif
+            }
+            tc::mma_commit_pair(&empty[st], 3);
+        }
+        tc::mma_commit_pair(&tfull, 3);
+    };
+
     if (warp < 8) {
         // ---------------- converters ----------------
         const int row = tid >> 1, c = tid & 1;
@@ -753,7 +799,11 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
             for (int gi = 0; gi < ngrp; ++gi) {
                 const int gq = p * ngrp + gi, rs = gq % NR;
                 const uint32_t raw = sraw + rs * Cfg::RAW;
-                tc::mbar_wait(&rfull[rs], (uint32_t)(gq / NR) & 1u);
+                {
+                    TC_T0();
+                    tc::mbar_wait(&rfull[rs], (uint32_t)(gq / NR) & 1u);
+                    if (tid == 0) TC_ACC(5);
+                }
                 if constexpr (F16) {
                     // stage j = features [16j, 16j+16) of the group; this thread: chunk c
                     uint4 hi[2], lo[2];
@@ -776,7 +826,9 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                     for (int j = 0; j < 2; ++j) {
                         const int it = gq * 2 + j, st = it % NST;
                         const uint32_t stage = sbase + st * Cfg::STAGE;
+                        TC_T0();
                         tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+                        if (tid == 0) TC_ACC(2);
                         sts128u(stage + aoff, hi[j]);
                         sts128u(stage + Cfg::A_T + aoff, lo[j]);
                     }
@@ -837,6 +889,10 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
             }
         }
         __syncwarp();
+    } else if (kFwdMmaWarp && warp == 18) {
+        if (lane == 0 && rank == 0)
+            for (int p = 0; p < S; ++p) issue_stream(p);
+        __syncwarp();
     } else {
         // ---------------- MMA issue (leader, warp 9 lane 0) + epilogue ----------------
         // Epilogue: TMEM -> registers -> 128 B-swizzled staging tile (row r, 16 B chunk c
@@ -848,39 +904,7 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
         const uint32_t stg0 = sepi + (uint32_t)(warp - 9) * 2 * Cfg::EPI_TILE;
         int nst = 0;  // stores issued by this warp (buffer = nst & 1)
         for (int p = 0; p < S; ++p) {
-            if (warp == 9 && lane == 0 && rank == 0) {
-                constexpr uint32_t idesc =
-                    F16 ? tc::make_idesc_f16(2 * TC_M, NF, 0, 0) : tc::make_idesc_tf32(2 * TC_M, NF, 0, 0);
-                tc::mbar_wait(&tempty, ((uint32_t)p & 1u) ^ 1u);
-                tc::tc_fence_after();
-                const uint32_t dbig = tmem, dsmall = tmem + NF;
-                for (int kb = 0; kb < nkb; ++kb) {
-                    const int it = p * nkb + kb, st = it % NST;
-                    const uint32_t stage = sbase + st * Cfg::STAGE;
-                    {
-                        TC_T0();
-                        tc::mbar_wait(&full[st], (uint32_t)(it / NST) & 1u);
-                        TC_ACC(0);
-                    }
-                    tc::tc_fence_after();
-                    const uint64_t ah = tc::make_sdesc(stage, 16, 256, 6), al = tc::make_sdesc(stage + Cfg::A_T, 16, 256, 6);
-                    const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 16, 256, 6);
-                    const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 16, 256, 6);
-                    if constexpr (F16) {
-                        tc::mma_f16_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
-                        tc::mma_f16_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
-                        tc::mma_f16_pair(dsmall, al, bh, idesc, 1u);
-                    } else {
-                        tc::mma_tf32_pair(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
-                        tc::mma_tf32_pair(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
-#ifndef PNX_EXP_TWO_MMA  // timing experiment only: drops a product
-                        tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
-#endif
-                    }
-                    tc::mma_commit_pair(&empty[st], 3);
-                }
-                tc::mma_commit_pair(&tfull, 3);
-            }
+            if (!kFwdMmaWarp && warp == 9 && lane == 0 && rank == 0) issue_stream(p);  // (19-warp layout: unused)
             __syncwarp();
             float usA = 1.0f, usW = 1.0f;  // 3xFP16 unscale 2^-eA, 2^-eW
             if constexpr (F16) {
@@ -1438,7 +1462,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
             const int s0 = Cfg::sa(pass), s1 = Cfg::sb(pass);
             const float sc0 = ldexpf(1.0f, tc::f16_exp_bits(g.amax_in[s0]));
             const float sc1 = s1 >= 0 ? ldexpf(1.0f, tc::f16_exp_bits(g.amax_in[s1])) : 1.0f;
-            constexpr int D = 2;  // k-steps of A prefetched in registers
+            constexpr int D = 2;  // k-steps of A prefetched in registers (3 or 4: slower, trace_bwd5)
             float4 ra[D][2], rb[D][2];
 #pragma unroll
             for (int d = 0; d < D; ++d)

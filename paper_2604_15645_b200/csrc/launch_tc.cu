@@ -150,7 +150,16 @@ int launch_tc4_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
         tc_make_tmap(&a.tmO, g.out, 3, Cfg::NF, g.Rpad, S, 32, 32, 1, true))
         return -1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g.Rpad / TC_M);
+    // persistent pairs: one per two SMs (each walks tiles pair, pair + npairs, ...)
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nsm < 2) nsm = 2;
+    }
+    const int ntiles = g.Rpad / 256;
+    cfg.gridDim = dim3(2 * (ntiles < nsm / 2 ? ntiles : nsm / 2));
     cfg.blockDim = dim3(TC4_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;

@@ -696,7 +696,12 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = tc::cluster_ctarank();
-    const int r0 = (blockIdx.x >> 1) * 256 + (int)rank * 128;
+    // persistent: pair `pair` owns 256-row tiles pair, pair + npairs, ...; every ring
+    // and accumulator barrier keeps counting across tiles, so the converters and
+    // loaders run into the next tile while the epilogue drains the previous one
+    const int npairs = (int)(gridDim.x >> 1), pair = (int)(blockIdx.x >> 1), ntiles = g.Rpad / 256;
+    const int nloc = pair < ntiles ? (ntiles - 1 - pair) / npairs + 1 : 0;
+    auto row0 = [&](int i) { return (pair + i * npairs) * 256 + (int)rank * 128; };
     constexpr int KS = F16 ? 16 : 8;   // K per stage (one MMA)
     constexpr int SPG = 32 / KS;       // stages per 32-feature raw group
     const int nkb = g.K / KS, ngrp = g.K / 32;
@@ -736,19 +741,19 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
     // raw boxes a pass needs: [0] = stream 0 (t), [1] = stream p, [2] = partner
     auto nbox = [](int p) { return PRO == ACT_NONE ? 1 : (p == 0 ? 1 : (St::order(p) == 2 ? 3 : 2)); };
 
-    // MMAs of stream p (one elected thread of the pair leader)
-    auto issue_stream = [&](int p) {
+    // MMAs of the ps-th (tile, stream) item (one elected thread of the pair leader)
+    auto issue_stream = [&](int ps) {
         constexpr uint32_t idesc =
             F16 ? tc::make_idesc_f16(2 * TC_M, NF, 0, 0) : tc::make_idesc_tf32(2 * TC_M, NF, 0, 0);
         {
             TC_T0();
-            tc::mbar_wait(&tempty, ((uint32_t)p & 1u) ^ 1u);
+            tc::mbar_wait(&tempty, ((uint32_t)ps & 1u) ^ 1u);
             TC_ACC(1);
         }
         tc::tc_fence_after();
         const uint32_t dbig = tmem, dsmall = tmem + NF;
         for (int kb = 0; kb < nkb; ++kb) {
-            const int it = p * nkb + kb, st = it % NST;
+            const int it = ps * nkb + kb, st = it % NST;
             const uint32_t stage = sbase + st * Cfg::STAGE;
             {
                 TC_T0();
@@ -794,10 +799,11 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                                (1.f - t.z * t.z) * (z.z - 2.f * t.z * za.z * za.z),
                                (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
         };
-        for (int p = 0; p < S; ++p) {
+        for (int ps = 0; ps < nloc * S; ++ps) {
+            const int p = ps % S;
             const float sc = F16 ? ldexpf(1.0f, a_exp(p)) : 1.0f;
             for (int gi = 0; gi < ngrp; ++gi) {
-                const int gq = p * ngrp + gi, rs = gq % NR;
+                const int gq = ps * ngrp + gi, rs = gq % NR;
                 const uint32_t raw = sraw + rs * Cfg::RAW;
                 {
                     TC_T0();
@@ -859,11 +865,12 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
     } else if (warp == 8) {
         // ---------------- raw A loader ----------------
         if (lane == 0) {
-            for (int p = 0; p < S; ++p) {
+            for (int ps = 0; ps < nloc * S; ++ps) {
+                const int p = ps % S, r0 = row0(ps / S);
                 const int nb = nbox(p);
                 const int s1 = PRO == ACT_NONE ? p : 0;
                 for (int gi = 0; gi < ngrp; ++gi) {
-                    const int gq = p * ngrp + gi, rs = gq % NR;
+                    const int gq = ps * ngrp + gi, rs = gq % NR;
                     const uint32_t raw = sraw + rs * Cfg::RAW;
                     tc::mbar_wait(&rempty[rs], ((uint32_t)(gq / NR) & 1u) ^ 1u);
                     tc::mbar_arrive_expect_tx(&rfull[rs], nb * Cfg::BOX);
@@ -877,7 +884,7 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
     } else if (warp == 17) {
         // ---------------- weight-half loader ----------------
         if (lane == 0) {
-            const int nit = S * nkb;
+            const int nit = nloc * S * nkb;
             for (int it = 0; it < nit; ++it) {
                 const int st = it % NST, kb = it % nkb;
                 const uint32_t stage = sbase + st * Cfg::STAGE;
@@ -891,7 +898,7 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
         __syncwarp();
     } else if (kFwdMmaWarp && warp == 18) {
         if (lane == 0 && rank == 0)
-            for (int p = 0; p < S; ++p) issue_stream(p);
+            for (int ps = 0; ps < nloc * S; ++ps) issue_stream(ps);
         __syncwarp();
     } else {
         // ---------------- MMA issue (leader, warp 9 lane 0) + epilogue ----------------
@@ -903,8 +910,9 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
         const uint32_t stg0 = sepi + (uint32_t)(warp - 9) * 2 * Cfg::EPI_TILE;
         int nst = 0;  // stores issued by this warp (buffer = nst & 1)
-        for (int p = 0; p < S; ++p) {
-            if (!kFwdMmaWarp && warp == 9 && lane == 0 && rank == 0) issue_stream(p);  // (19-warp layout: unused)
+        for (int ps = 0; ps < nloc * S; ++ps) {
+            const int p = ps % S, r0 = row0(ps / S);
+            if (!kFwdMmaWarp && warp == 9 && lane == 0 && rank == 0) issue_stream(ps);  // (19-warp layout: unused)
             __syncwarp();
             float usA = 1.0f, usW = 1.0f;  // 3xFP16 unscale 2^-eA, 2^-eW
             if constexpr (F16) {
@@ -912,7 +920,7 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                 usW = ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w));
             }
             unsigned mx = 0;
-            tc::mbar_wait(&tfull, (uint32_t)p & 1u);
+            tc::mbar_wait(&tfull, (uint32_t)ps & 1u);
             tc::tc_fence_after();
             TC_T0();
 #pragma unroll 1

@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpnx.so")
+LIB_PATH = os.environ.get("PNX_LIB_PATH") or os.path.join(HERE, "libpnx.so")  # override: dev A/B builds
 
 _lib = None
 

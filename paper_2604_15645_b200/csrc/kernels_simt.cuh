@@ -767,6 +767,7 @@ __global__ void __launch_bounds__(256) k_wgrad(WgradArgs g) {
 // ---------------------------------------------------------------------------
 constexpr int kHeadMaxJ = 16;  // hidden width <= 512
 constexpr int kHeadWarps = 8;
+constexpr int kHeadBlocks = 2;  // resident head blocks per SM (grid = kHeadBlocks x SMs; 3 is slower)
 
 struct HeadArgs {
     const float* Z;      // [S][Rpad][H]
@@ -811,7 +812,7 @@ struct HeadArgs {
 constexpr int kStatMax = 64;  // max causality segments / Poynting time samples
 
 template <int P, int ACT, int J>
-__global__ void __launch_bounds__(32 * kHeadWarps, 2) k_head(HeadArgs a) {
+__global__ void __launch_bounds__(32 * kHeadWarps, kHeadBlocks) k_head(HeadArgs a) {
     using Tr = PdeTraits<P>;
     constexpr int L = Tr::L, F = Tr::F, K = Tr::K;
     constexpr int S = Streams<L>::S;
@@ -875,12 +876,13 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 2) k_head(HeadArgs a) {
         for (int i = lane; i < 3 * kStatMax; i += 32) sacc[wid][i] = 0.0;
         __syncwarp();
     }
-    float z[S][J], zn[S][J];
+    // one row per warp iteration, no register prefetch of the next row: the
+    // prefetch pushed the kernel into local-memory spills (2.5 -> 2.0 ms at C5
+    // without it; occupancy hides the load latency)
+    float z[S][J];
     int r = a.rbeg + gw;
-    if (r < a.nrows) load_row(r, z);
     for (; r < a.nrows; r += nw) {
-        const int rn = r + nw;
-        if (rn < a.nrows) load_row(rn, zn);  // prefetch the next row of this warp
+        load_row(r, z);
         const int64_t g = a.row0 + r;
         float o[S * F];
 #pragma unroll
@@ -1040,12 +1042,7 @@ __global__ void __launch_bounds__(32 * kHeadWarps, 2) k_head(HeadArgs a) {
             for (int f = 0; f < F; ++f) accB[f] += ob[f];
             if (++since_flush == FLUSH) flush();
         }
-        if (rn < a.nrows) {
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-                for (int j = 0; j < J; ++j) z[s][j] = zn[s][j];
-        }
+
     }
     if (a.stats) {  // fixed-order fold of the warps' sums, one partial per block
         __syncthreads();

@@ -771,6 +771,7 @@ int pnx_create(const pnx_model_desc* m, const pnx_problem_desc* p, int device, p
     pnx_ctx* ctx = new pnx_ctx();
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
+    ctx->head_grid = kHeadBlocks * ctx->nsm;
     ctx->in_dim = m->in_dim;
     ctx->H = m->hidden_dim;
     ctx->depth = m->depth;

@@ -81,13 +81,29 @@ class ClockSampler:
         self.proc = None
         self.out = tempfile.NamedTemporaryFile(prefix="clocks_", suffix=".csv", delete=False).name
 
+    def _lines(self):
+        try:
+            return sum(1 for _ in open(self.out))
+        except Exception:
+            return 0
+
     def start(self):
+        """Start sampling and wait (<= 3 s) for the first sample, so that even a
+        short timed region is sampled; mark() then drops the pre-region lines."""
+        self.skip = 0
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=open(self.out, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        t0 = time.time()
+        while self._lines() == 0 and time.time() - t0 < 3.0:
+            time.sleep(0.02)
+
+    def mark(self):
+        self.skip = self._lines()
 
     def stop(self):
         if self.proc is None:
@@ -99,7 +115,11 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.out):
+        lines = open(self.out).readlines()
+        # samples inside the timed region; if the region was shorter than one
+        # sampling interval, the first sample after it (the GPU is still loaded)
+        lines = lines[self.skip:] or lines[-1:]
+        for line in lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 8:
                 continue
@@ -307,10 +327,11 @@ def main():
     clk = ClockSampler(local)
     if not trainer.graph:
         worker.profile(True)
+    clk.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clk.start()
+    clk.mark()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)

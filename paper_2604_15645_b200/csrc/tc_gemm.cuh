@@ -1106,7 +1106,8 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
 #ifdef PNX_TC_TRACE
                 long long _tc = clock64();
 #endif
-                float4 ahi[NS], alo[NS], bhi[NS][2], blo[NS][2];
+                float4 ahi[NS], bhi[NS][2];
+                [[maybe_unused]] float4 alo[NS], blo[NS][2];  // tf32 split only
 #pragma unroll
                 for (int i = 0; i < NS; ++i) {
                     const int s = SLO + i;

@@ -914,12 +914,19 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
             const int p = ps % S, r0 = row0(ps / S);
             if (!kFwdMmaWarp && warp == 9 && lane == 0 && rank == 0) issue_stream(ps);  // (19-warp layout: unused)
             __syncwarp();
-            float usA = 1.0f, usW = 1.0f;  // 3xFP16 unscale 2^-eA, 2^-eW
+            // 3xFP16 unscale 2^-(eA+eW): one multiply while the power of two is a normal
+            // float (always, in practice), else two
+            float usA = 1.0f, usW = 1.0f;
             if constexpr (F16) {
-                usA = ldexpf(1.0f, -a_exp(p));
-                usW = ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w));
+                const int e = a_exp(p) + tc::f16_exp_bits(*g.amax_w);
+                if (e > -120 && e < 120) {
+                    usA = ldexpf(1.0f, -e);
+                } else {
+                    usA = ldexpf(1.0f, -a_exp(p));
+                    usW = ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w));
+                }
             }
-            unsigned mx = 0;
+            float mx = 0.0f;  // |z| bound of this stream (fmax with |.|: one FMNMX per element)
             tc::mbar_wait(&tfull, (uint32_t)ps & 1u);
             tc::tc_fence_after();
             TC_T0();
@@ -939,15 +946,20 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
 #pragma unroll
                 for (int j = 0; j < 32; ++j) a[j] += b[j];
                 if constexpr (F16) {
+                    if (usW != 1.0f) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) a[j] = a[j] * usA * usW;
+                        for (int j = 0; j < 32; ++j) a[j] = a[j] * usA * usW;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) a[j] *= usA;
+                    }
                 }
                 if (p == 0) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) mx = max(mx, tc::abs_bits(a[j]));
+                    for (int j = 0; j < 32; ++j) mx = fmaxf(mx, fabsf(a[j]));
                 }
                 const uint32_t stg = stg0 + (uint32_t)(nst & 1) * Cfg::EPI_TILE;
                 if (lane == 0) tc::bulk_wait_read<1>();  // the store that last used this buffer has read it
@@ -964,7 +976,7 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
                 }
                 ++nst;
             }
-            if (p > 0 && g.amax_out) tc::warp_amax(g.amax_out + p, mx);
+            if (p > 0 && g.amax_out) tc::warp_amax(g.amax_out + p, __float_as_uint(mx));
             if (warp == 9 && lane == 0) TC_ACC(3);
         }
         if (lane == 0) tc::bulk_wait<0>();
@@ -1676,7 +1688,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                 usa = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s0]));
                 if (s1 >= 0) usb = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s1]));
             }
-            unsigned mxa = 0, mxb = 0;
+            float mxa = 0.0f, mxb = 0.0f;
             tc::mbar_wait(&tfull, (uint32_t)pass);
             tc::tc_fence_after();
             TC_T0();
@@ -1759,8 +1771,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                     }
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        mxa = max(mxa, tc::abs_bits(oa[e]));
-                        mxb = max(mxb, tc::abs_bits(ob[e]));
+                        mxa = fmaxf(mxa, fabsf(oa[e]));
+                        mxb = fmaxf(mxb, fabsf(ob[e]));
                     }
                     // outputs in place: stream s0 -> its z tile (the t tile when s0 = 0),
                     // stream s1 -> its z tile (the t tile when s1 = 0)
@@ -1783,8 +1795,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                 __syncwarp();
             }
             if (g.amax_out) {
-                tc::warp_amax(g.amax_out + s0, mxa);
-                if (s1 >= 0) tc::warp_amax(g.amax_out + s1, mxb);
+                tc::warp_amax(g.amax_out + s0, __float_as_uint(mxa));
+                if (s1 >= 0) tc::warp_amax(g.amax_out + s1, __float_as_uint(mxb));
             }
             if (warp == 9 && lane == 0) TC_ACC(3);
             tc::tc_fence_before();

@@ -1660,7 +1660,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
         const int q = warp & 3, half = (warp - 9) >> 2, ew = warp - 9;
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
         const uint32_t stg0 = sbase + (uint32_t)ew * 2 * 3 * Cfg::TILE;
-        const uint32_t pbuf = sP + (uint32_t)ew * 128 * 32 * 4;     // [col][lane]
+        const uint32_t pbuf = sP + (uint32_t)ew * 128 * 32 * 4;     // [col/4][lane][4]: one 16 B access per 4 columns
         const int64_t rbase = (int64_t)(r0 + q * 32) * NF;
         const int lr = lane >> 2, lcv = lane & 3;
         auto soff = [](int r, int c) { return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4)); };
@@ -1730,9 +1730,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                         zb2[0] = v.x; zb2[1] = v.y; zb2[2] = v.z; zb2[3] = v.w;
                     }
                     if (pass == 1) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            pp[e] = __uint_as_float(lds32u(pbuf + (uint32_t)(((cch * 16 + j4 + e) * 32 + lane) * 4)));
+                        const float4 v = lds128(pbuf + (uint32_t)((((cch * 16 + j4) >> 2) * 32 + lane) * 16));
+                        pp[0] = v.x; pp[1] = v.y; pp[2] = v.z; pp[3] = v.w;
                     }
                     float oa[4], ob[4];
 #pragma unroll
@@ -1764,11 +1763,9 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                             ob[e] = 0.0f;
                         }
                     }
-                    if (pass == 0) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            sts32(pbuf + (uint32_t)(((cch * 16 + j4 + e) * 32 + lane) * 4), pp[e]);
-                    }
+                    if (pass == 0)
+                        sts128(pbuf + (uint32_t)((((cch * 16 + j4) >> 2) * 32 + lane) * 16),
+                               make_float4(pp[0], pp[1], pp[2], pp[3]));
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         mxa = fmaxf(mxa, fabsf(oa[e]));

@@ -223,6 +223,32 @@ def test_f16_adam_trajectory_tracks_ffma(graph):
     assert np.all(np.abs(got - ref) <= 1e-3 * np.abs(ref) + 1e-9), np.max(np.abs(got - ref) / (np.abs(ref) + 1e-30))
 
 
+@pytest.mark.parametrize("rff", [False, True])
+def test_width256_engine_mix_vs_oracle(rff):
+    """Width-256 Maxwell models whose first layer is not the fused narrow one
+    (RFF embedding of width 128 -> K0 = 256, plus RWF) run 3xTF32 until a
+    bound-recording producer exists and 3xFP16 after it; without RFF every
+    hidden layer is 3xFP16. Both against the FP64 oracle."""
+    import dataclasses
+    pk = _pkg()
+    from paper_2604_15645_b200 import configs
+    wl = configs.get_config("c4")
+    spec = dataclasses.replace(wl.spec, depth=4,
+                               rff=pk.RFFSpec(width=128, sigma=1.0) if rff else None,
+                               rwf=pk.RWFSpec(1.0, 0.1) if rff else None)
+    col = configs.collocation(wl, [10, 10, 8])
+    flat, rffB = pk.init_params(spec, seed=3)
+    ospec = gi.spec_from_json(_spec_json(spec))
+    ores = po.ResidualSpec(wl.res.id, wl.res.advection_c, wl.res.epsilon, wl.res.mu, wl.res.reynolds)
+    ocol = po.Collocation(col["interior"], col["ic_points"], col["ic_targets"], col["bc_a"], col["bc_b"],
+                          col["bc_targets"])
+    ref, outs = po.data_parallel_gradient(ospec, flat, rffB, ores, ocol, wl.bc, 1)
+    grad, losses = pk.data_parallel_gradient(spec, wl.res, wl.bc, flat, rffB, workers=1, engine="auto", **col)
+    assert rel_l2(grad, ref) <= GRAD_RTOL_TC, rel_l2(grad, ref)
+    for k in ("pde", "ic", "bc"):
+        assert abs(losses[0][k] - outs[0][k]) <= LOSS_RTOL * abs(outs[0][k]) + 1e-12
+
+
 def test_chunking_is_invisible_with_causality_and_poynting():
     """Several chunks: causality needs every chunk's segment sums before any
     seed (two-pass forward) and the Poynting nodes ride in chunk 0; the step

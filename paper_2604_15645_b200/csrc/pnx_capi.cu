@@ -402,13 +402,17 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             if (!(tc_mask & 2)) tc_bwd[l] = false;
             // backward: Zb_out bounds come from the head (last hidden layer) or the
             // decoupled backward of layer l+1 (both record them)
-            const bool recb = l == ctx->depth - 1 ||
-                              (tc_bwd[l + 1] && (tc_mask & 2) && tc5_bwd_ok(L, t.K[l + 1], t.N[l + 1]));
+            // every tcgen05 forward / backward epilogue and the fused layer 0 / head
+            // record their output bounds; only the CTA-pair forward and the decoupled
+            // backward have 3xFP16 variants, the weight gradient has one everywhere
+            const bool recb = l == ctx->depth - 1 || (tc_bwd[l + 1] && (tc_mask & 2));
             if (l > 0) {
                 const bool pairf = tc_fwd[l] && (tc_mask & 1) && tc4_fwd_ok(t.K[l], t.N[l]);
                 f16_fwd[l] = f16 && pairf && rec;
                 f16_wg[l] = f16 && tc_wg[l] && rec && recb;  // A = Z_{l-1}, B = Zb_l
-                rec = pairf;
+                rec = tc_fwd[l] && (tc_mask & 1);
+            } else if (!layer0_fused(ctx)) {
+                rec = tc_fwd[0] && (tc_mask & 1);  // the tcgen05 layer 0 records Z_0 bounds too
             }
             if (tc_bwd[l] && f16 && recb && tc5_bwd_ok(L, t.K[l], t.N[l])) f16_bwd[l] = true;
             if (f16_fwd[l]) {

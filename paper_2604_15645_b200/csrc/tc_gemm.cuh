@@ -592,6 +592,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
         const uint32_t stg = sbase + NST * Cfg::STAGE + (uint32_t)(warp - 9) * 32 * Cfg::EPI_ROW;
         for (int p = 0; p < S; ++p) {
             const int buf = p % NBUF, use = p / NBUF;
+            float mx = 0.0f;  // |z| bound of this stream (consumers' 3xFP16 scales)
             tc::mbar_wait(&tfull[buf], (uint32_t)use & 1u);
             tc::tc_fence_after();
             TC_T0();
@@ -608,6 +609,9 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
                 if (p == 0) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) mx = fmaxf(mx, fabsf(a[j]));
                 }
                 // row `lane` of this warp's 32 x 32 block -> padded smem
 #pragma unroll
@@ -630,6 +634,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
                 }
                 __syncwarp();
             }
+            if (p > 0 && g.amax_out) tc::warp_amax(g.amax_out + p, __float_as_uint(mx));
             tc::tc_fence_before();
             __syncwarp();
             if (warp == 9 && lane == 0) TC_ACC(3);
@@ -1969,6 +1974,9 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
         const uint32_t buf = sbase + (uint32_t)(warp - 9) * (S * 32 * ROWF * 4);
         const int64_t rbase = (int64_t)(r0 + q * 32) * g.N + n0;
         const int lr = lane >> 3, lc = (lane & 7) * 4;
+        float mx[S];  // |Zb_in| bounds per stream (consumers' 3xFP16 scales)
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) mx[s2] = 0.0f;
         tc::mbar_wait(&tfull, 0);
         tc::tc_fence_after();
         TC_T0();
@@ -2009,7 +2017,10 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
                     }
                     act_bwd<L, ACT_TANH>(zz, hh, oo, 1.0f);
 #pragma unroll
-                    for (int s2 = 0; s2 < S; ++s2) hb[s2][j] = oo[s2];
+                    for (int s2 = 0; s2 < S; ++s2) {
+                        hb[s2][j] = oo[s2];
+                        mx[s2] = fmaxf(mx[s2], fabsf(oo[s2]));
+                    }
                 }
 #pragma unroll
                 for (int s2 = 0; s2 < S; ++s2) {
@@ -2032,6 +2043,10 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
                 }
             }
             __syncwarp();
+        }
+        if (g.amax_out) {
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) tc::warp_amax(g.amax_out + s2, __float_as_uint(mx[s2]));
         }
         if (warp == 9 && lane == 0) TC_ACC(3);
     }

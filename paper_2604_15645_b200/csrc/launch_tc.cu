@@ -119,11 +119,11 @@ int launch_tc_layer(int L, int mode, int pro, const TcGemmArgs& g, cudaStream_t 
     return -1;
 }
 
-template <int L, int PRO, int NF>
+template <int L, int PRO, int NF, bool F16 = false>
 int launch_tc2_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc3FwdCfg<NF>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc2_fwd<L, PRO, NF>;
+    auto kern = k_tc2_fwd<L, PRO, NF, F16>;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
@@ -182,7 +182,12 @@ int launch_tc2_fwd_l(int pro, const TcGemmArgs& g, cudaStream_t st) {
         return pro == ACT_NONE ? launch_tc4_fwd_t<L, ACT_NONE, false>(g, st)
                                : launch_tc4_fwd_t<L, ACT_TANH, false>(g, st);
     }
-    if (g.f16) return -1;  // 3xFP16 only in the pair forward
+    if (g.f16) {  // 3xFP16 single-CTA forward (tanh inputs: the producer records their bounds)
+        if (pro == ACT_NONE) return -1;
+        if (g.N == 256) return launch_tc2_fwd_t<L, ACT_TANH, 256, true>(g, st);
+        if (g.N == 128) return launch_tc2_fwd_t<L, ACT_TANH, 128, true>(g, st);
+        return -1;
+    }
     if (g.N == 256) return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 256>(g, st) : launch_tc2_fwd_t<L, ACT_TANH, 256>(g, st);
     if (g.N == 128) return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 128>(g, st) : launch_tc2_fwd_t<L, ACT_TANH, 128>(g, st);
     return -1;

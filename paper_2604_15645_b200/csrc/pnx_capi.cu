@@ -400,15 +400,14 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         for (int l = 0; l < ctx->depth; ++l) {
             tc_wg[l] = tc_fwd[l] && (tc_mask & 4);
             if (!(tc_mask & 2)) tc_bwd[l] = false;
-            // backward: Zb_out bounds come from the head (last hidden layer) or the
-            // decoupled backward of layer l+1 (both record them)
-            // every tcgen05 forward / backward epilogue and the fused layer 0 / head
-            // record their output bounds; only the CTA-pair forward and the decoupled
-            // backward have 3xFP16 variants, the weight gradient has one everywhere
+            // Zb_out bounds come from the head (last hidden layer) or the backward of
+            // layer l+1; every tcgen05 forward / backward epilogue and the fused layer 0 / head
+            // record their output bounds; the forwards (pair and single-CTA) and the
+            // weight gradient have 3xFP16 variants everywhere, the backward only in
+            // its decoupled first-order form (width 256)
             const bool recb = l == ctx->depth - 1 || (tc_bwd[l + 1] && (tc_mask & 2));
             if (l > 0) {
-                const bool pairf = tc_fwd[l] && (tc_mask & 1) && tc4_fwd_ok(t.K[l], t.N[l]);
-                f16_fwd[l] = f16 && pairf && rec;
+                f16_fwd[l] = f16 && tc_fwd[l] && (tc_mask & 1) && rec;  // pair or single-CTA forward
                 f16_wg[l] = f16 && tc_wg[l] && rec && recb;  // A = Z_{l-1}, B = Zb_l
                 rec = tc_fwd[l] && (tc_mask & 1);
             } else if (!layer0_fused(ctx)) {

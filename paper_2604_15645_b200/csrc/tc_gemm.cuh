@@ -416,7 +416,9 @@ struct Tc3FwdCfg {
     static constexpr int SMEM = NST * STAGE + EPI_BYTES + 1024;
 };
 
-template <int L, int PRO, int NF>
+// F16: 3xFP16 operands (kind::f16, K = 16 per stage: two stages per 32-feature
+// group), scaled by the recorded bounds like the pair forward.
+template <int L, int PRO, int NF, bool F16 = false>
 __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
     using St = Streams<L>;
     constexpr int S = St::S;
@@ -430,8 +432,19 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int r0 = blockIdx.x * TC_M;
-    const int nkb = g.K / 8, ngrp = g.K / 32;
+    constexpr int KS = F16 ? 16 : 8, SPG = 32 / KS;  // K per stage, stages per 32-feature group
+    const int nkb = g.K / KS, ngrp = g.K / 32;
     const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * NF;
+    // 3xFP16 operand scale exponent of stream p's A (|act(Z_in)[p]| bound)
+    auto a_exp = [&](int p) -> int {
+        if (PRO != ACT_NONE && p == 0) return tc::f16_scale_exp(1.0f);
+        float b = __uint_as_float(g.amax_in[p]);
+        if (PRO != ACT_NONE && St::order(p) == 2) {
+            const float a = __uint_as_float(g.amax_in[St::partner(p)]);
+            b = b + 2.0f * a * a;
+        }
+        return tc::f16_exp_bits(__float_as_uint(b * 1.001f));
+    };
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             tc::mbar_init(&full[i], 9);  // 8 producer warps + 1 expect_tx
@@ -455,12 +468,18 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
         // lane -> (row quad offset rq = lane/8, 16 B chunk c = lane%8 of a 128 B
         // group line); warp w covers rows 16w .. 16w+15 as rq + 4i, i = 0..3.
         const int rq = lane >> 3, c = lane & 7;
-        const int j_own = c >> 1;           // k-step of the group this lane feeds
-        const int kc = (c & 1) * 4;         // feature offset inside the k-step
+        // k-step of the group this lane feeds and its place in that step's 32 B row:
+        // tf32: 4 of 8 features (16 B chunk); fp16: 4 of 16 halves (8 B in a 16 B chunk)
+        const int j_own = F16 ? c >> 2 : c >> 1;
+        const int kc = (c & 1) * 4;
         const float* base = g.A + (int64_t)(r0 + warp * 16 + rq) * g.K + c * 4;
         uint32_t aoff[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) aoff[i] = tc::sw32_off((uint32_t)(warp * 16 + rq + 4 * i), (uint32_t)kc);
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t row = (uint32_t)(warp * 16 + rq + 4 * i);
+            aoff[i] = F16 ? tc::sw32_chunk(row, (uint32_t)((c & 3) >> 1)) + (uint32_t)(c & 1) * 8u
+                          : tc::sw32_off(row, (uint32_t)kc);
+        }
         float4 t4[4], z4[4], p4[SECOND ? 4 : 1];
         auto load = [&](int grp, float4* tt, float4* zz, float4* pp) {
 #ifdef PNX_EXP_NOLOAD
@@ -493,10 +512,12 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
                 zc4[i] = z4[i];
                 if constexpr (SECOND) pc4[i] = p4[i];
             }
-            if (gi + 1 < ngt) load(gi + 1, t4, z4, p4);  // prefetch one group (4 stages) ahead
+            if (gi + 1 < ngt) load(gi + 1, t4, z4, p4);  // prefetch one group ahead
             const int p = gi / ngrp;
+            const float sc = F16 ? ldexpf(1.0f, a_exp(p)) : 1.0f;
             // activation + split for this lane's 4 rows (used at stage j_own)
             float4 hi[4], lo[4];
+            uint2 hi16[4], lo16[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 float4 h;
@@ -518,11 +539,16 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
                                         (1.f - t.w * t.w) * (z.w - 2.f * t.w * za.w * za.w));
                     }
                 }
-                split4(h, hi[i], lo[i]);
+                if constexpr (F16) {
+                    tc::split_h2(h.x * sc, h.y * sc, hi16[i].x, lo16[i].x);
+                    tc::split_h2(h.z * sc, h.w * sc, hi16[i].y, lo16[i].y);
+                } else {
+                    split4(h, hi[i], lo[i]);
+                }
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int it = gi * 4 + j, st = it % NST, kb = it % nkb;
+            for (int j = 0; j < SPG; ++j) {
+                const int it = gi * SPG + j, st = it % NST, kb = it % nkb;
                 const uint32_t stage = sbase + st * Cfg::STAGE;
                 {
                     TC_T0();
@@ -542,8 +568,15 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
                 if (j == j_own) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        sts128(stage + aoff[i], hi[i]);
-                        sts128(stage + Cfg::A_T + aoff[i], lo[i]);
+                        if constexpr (F16) {
+                            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + aoff[i]), "r"(hi16[i].x),
+                                         "r"(hi16[i].y));
+                            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(stage + Cfg::A_T + aoff[i]),
+                                         "r"(lo16[i].x), "r"(lo16[i].y));
+                        } else {
+                            sts128(stage + aoff[i], hi[i]);
+                            sts128(stage + Cfg::A_T + aoff[i], lo[i]);
+                        }
                     }
                 }
                 tc::fence_proxy_async_smem();
@@ -554,7 +587,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
     } else if (warp == 8) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            constexpr uint32_t idesc = tc::make_idesc_tf32(TC_M, NF, 0, 0);
+            constexpr uint32_t idesc = F16 ? tc::make_idesc_f16(TC_M, NF, 0, 0) : tc::make_idesc_tf32(TC_M, NF, 0, 0);
             for (int p = 0; p < S; ++p) {
                 const int buf = p % NBUF, use = p / NBUF;
                 {
@@ -576,9 +609,15 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
                     const uint64_t ah = tc::make_sdesc(stage, 16, 256, 6), al = tc::make_sdesc(stage + Cfg::A_T, 16, 256, 6);
                     const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 16, 256, 6);
                     const uint64_t bl = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 16, 256, 6);
-                    tc::mma_tf32(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
-                    tc::mma_tf32(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
-                    tc::mma_tf32(dsmall, al, bh, idesc, 1u);
+                    if constexpr (F16) {
+                        tc::mma_f16(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
+                        tc::mma_f16(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+                        tc::mma_f16(dsmall, al, bh, idesc, 1u);
+                    } else {
+                        tc::mma_tf32(dbig, ah, bh, idesc, kb > 0 ? 1u : 0u);
+                        tc::mma_tf32(dsmall, ah, bl, idesc, kb > 0 ? 1u : 0u);
+                        tc::mma_tf32(dsmall, al, bh, idesc, 1u);
+                    }
                     tc::mma_commit(&empty[st]);
                 }
                 tc::mma_commit(&tfull[buf]);
@@ -593,6 +632,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
         for (int p = 0; p < S; ++p) {
             const int buf = p % NBUF, use = p / NBUF;
             float mx = 0.0f;  // |z| bound of this stream (consumers' 3xFP16 scales)
+            const float usA = F16 ? ldexpf(1.0f, -a_exp(p)) : 1.0f;
+            const float usW = F16 ? ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w)) : 1.0f;
             tc::mbar_wait(&tfull[buf], (uint32_t)use & 1u);
             tc::tc_fence_after();
             TC_T0();
@@ -606,6 +647,10 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_fwd(TcGemmArgs g) {
                 tc::tmem_ld_wait();
 #pragma unroll
                 for (int j = 0; j < 32; ++j) a[j] += b[j];
+                if constexpr (F16) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) a[j] = a[j] * usA * usW;
+                }
                 if (p == 0) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) a[j] = store_value<ACT_TANH>(a[j] + __ldg(g.bias + c + j));

@@ -30,11 +30,11 @@ int tc_make_tmap(CUtensorMap* map, const float* base, int rank, uint64_t d0, uin
 
 // ---- tcgen05 dispatch --------------------------------------------------------
 
-template <int L, int NT, bool PAIR>
+template <int L, int NT, bool PAIR, bool F16 = false>
 int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc2BwdCfg<Streams<L>::S, NT, PAIR>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc2_bwd<L, NT, PAIR>;
+    auto kern = k_tc2_bwd<L, NT, PAIR, F16>;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
@@ -99,7 +99,7 @@ int launch_tc_layer_l(int mode, int pro, const TcGemmArgs& g, cudaStream_t st) {
                                               : launch_tc5_bwd_t<L, false, false>(g, st);
         }
     }
-    if (g.f16) return -1;  // 3xFP16 only in the decoupled backward
+    if (g.f16) return launch_tc2_bwd_t<L, tc_nt(Streams<L>::S), false, true>(g, st);  // 3xFP16, single CTA
     constexpr int NT = tc_nt(Streams<L>::S);
     (void)mode;
     (void)pro;

@@ -402,9 +402,8 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             if (!(tc_mask & 2)) tc_bwd[l] = false;
             // Zb_out bounds come from the head (last hidden layer) or the backward of
             // layer l+1; every tcgen05 forward / backward epilogue and the fused layer 0 / head
-            // record their output bounds; the forwards (pair and single-CTA) and the
-            // weight gradient have 3xFP16 variants everywhere, the backward only in
-            // its decoupled first-order form (width 256)
+            // record their output bounds; every contraction kernel has a 3xFP16 variant
+            // (the CTA-pair variant of the general backward does not: it is opt-in)
             const bool recb = l == ctx->depth - 1 || (tc_bwd[l + 1] && (tc_mask & 2));
             if (l > 0) {
                 f16_fwd[l] = f16 && tc_fwd[l] && (tc_mask & 1) && rec;  // pair or single-CTA forward
@@ -413,7 +412,9 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             } else if (!layer0_fused(ctx)) {
                 rec = tc_fwd[0] && (tc_mask & 1);  // the tcgen05 layer 0 records Z_0 bounds too
             }
-            if (tc_bwd[l] && f16 && recb && tc5_bwd_ok(L, t.K[l], t.N[l])) f16_bwd[l] = true;
+            // the general (all streams in TMEM) backward gains from 3xFP16 only up to four
+            // streams: at S = 5 (NS, N = 64 tiles) its producers bound it (3.04 vs 3.16 ms at C3)
+            if (tc_bwd[l] && f16 && recb && (tc5_bwd_ok(L, t.K[l], t.N[l]) || S <= 4)) f16_bwd[l] = true;
             if (f16_fwd[l]) {
                 k_tc_prep_image16<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 0, t.N[l], amax_w(ctx, l),
                                                       reinterpret_cast<uint16_t*>(ctx->tc.img + ctx->tc.img_fwd[l]));
@@ -424,7 +425,8 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 CKL();
             }
             if (f16_bwd[l]) {
-                k_tc_prep_image16<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 1, 256, amax_w(ctx, l),
+                k_tc_prep_image16<<<256, 256, 0, st>>>(ctx->d_W + t.dW[l], t.K[l], t.N[l], 1,
+                                                      tc5_bwd_ok(L, t.K[l], t.N[l]) ? 256 : NT, amax_w(ctx, l),
                                                       reinterpret_cast<uint16_t*>(ctx->tc.img + ctx->tc.img_bwd[l]));
                 CKL();
             } else if (tc_bwd[l]) {

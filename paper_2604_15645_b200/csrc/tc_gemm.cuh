@@ -1880,13 +1880,16 @@ struct Tc2BwdCfg {
     static_assert(SMEM <= 227 * 1024, "bwd shared memory");
 };
 
-template <int L, int NT, bool PAIR>
+// F16: 3xFP16 operands (non-pair only), per-stream scales from the recorded |Zb| bounds
+template <int L, int NT, bool PAIR, bool F16 = false>
 __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constant__ TcGemmArgs g) {
     using St = Streams<L>;
     constexpr int S = St::S;
     using Cfg = Tc2BwdCfg<S, NT, PAIR>;
     constexpr int NST = Cfg::NST;
-    constexpr int D = 2;
+    static_assert(!(F16 && PAIR), "3xFP16 general backward: single CTA");
+    constexpr int D = F16 ? 1 : 2;  // k-steps of A in registers (F16 steps carry twice the features)
+    constexpr int KS = F16 ? 16 : 8;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     __shared__ uint64_t full[8], empty[8], tfull;
@@ -1898,7 +1901,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
     const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // (row tile, n tile) of this CTA / pair
     const int rt = cid / ntiles, nt = cid % ntiles;
     const int r0 = PAIR ? rt * 256 + (int)rank * 128 : rt * TC_M, n0 = nt * NT;
-    const int nkb = g.K / 8;
+    const int nkb = g.K / KS;
     const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * g.N;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
@@ -1921,7 +1924,51 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
     const float* bimg = g.img + (int64_t)nt * nkb * (2 * NT * 8);
     const uint32_t full0 = PAIR ? tc::mapa(tc::smem_u32(&full[0]), 0) : 0u;
 
-    if (warp < 8) {
+    if (F16 && warp < 8) {
+        // ---- 3xFP16 producers: 8 consecutive features per thread and k-step ----
+        const int prow = tid >> 1, pc = tid & 1;
+        const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 8;
+        const uint32_t aoff = tc::sw32_chunk((uint32_t)prow, (uint32_t)pc);
+        float sc[S];
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) sc[s2] = ldexpf(1.0f, tc::f16_exp_bits(g.amax_in[s2]));
+        float4 ring[S][2];
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) {
+            ring[s2][0] = ldg4(asrc + s2 * RK);
+            ring[s2][1] = ldg4(asrc + s2 * RK + 4);
+        }
+        for (int it = 0; it < nkb; ++it) {
+            const int st = it % NST;
+            const uint32_t stage = sbase + st * Cfg::STAGE;
+            uint4 hi[S], lo[S];
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) {
+                const float h[8] = {ring[s2][0].x, ring[s2][0].y, ring[s2][0].z, ring[s2][0].w,
+                                    ring[s2][1].x, ring[s2][1].y, ring[s2][1].z, ring[s2][1].w};
+                tc::split_h8(h, sc[s2], hi[s2], lo[s2]);
+            }
+            if (it + 1 < nkb)
+#pragma unroll
+                for (int s2 = 0; s2 < S; ++s2) {
+                    ring[s2][0] = ldg4(asrc + s2 * RK + (it + 1) * 16);
+                    ring[s2][1] = ldg4(asrc + s2 * RK + (it + 1) * 16 + 4);
+                }
+            tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
+            if (tid == 0) {
+                tc::mbar_arrive_expect_tx(&full[st], 2 * Cfg::B_T);
+                tc::bulk_g2s(stage + Cfg::A_BYTES, bimg + (int64_t)it * (2 * Cfg::B_T / 4), 2 * Cfg::B_T, &full[st]);
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) {
+                sts128u(stage + (2 * s2) * TC_TILE_BYTES + aoff, hi[s2]);
+                sts128u(stage + (2 * s2 + 1) * TC_TILE_BYTES + aoff, lo[s2]);
+            }
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&full[st]);
+        }
+    } else if (warp < 8) {
         const int prow = tid >> 1, pc = tid & 1;
         const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
         const uint32_t aoff = tc::sw32_off((uint32_t)prow, (uint32_t)(pc * 4));
@@ -1973,7 +2020,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
         }
     } else if (warp == 8) {
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NT, 0, 0);
+            constexpr uint32_t idesc = F16 ? tc::make_idesc_f16(TC_M, NT, 0, 0)
+                                           : tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NT, 0, 0);
             for (int it = 0; it < nkb; ++it) {
                 const int st = it % NST;
                 const uint32_t stage = sbase + st * Cfg::STAGE;
@@ -1992,7 +2040,11 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
                     const uint32_t ah = stage + (2 * s2) * TC_TILE_BYTES;
                     const uint64_t adh = tc::make_sdesc(ah, 16, 256, 6), adl = tc::make_sdesc(ah + TC_TILE_BYTES, 16, 256, 6);
                     const uint32_t d = tmem + (uint32_t)(s2 * NT);
-                    if constexpr (PAIR) {
+                    if constexpr (F16) {
+                        tc::mma_f16(d, adh, bh, idesc, it > 0 ? 1u : 0u);
+                        tc::mma_f16(d, adh, bl, idesc, 1u);
+                        tc::mma_f16(d, adl, bh, idesc, 1u);
+                    } else if constexpr (PAIR) {
                         tc::mma_tf32_pair(d, adh, bh, idesc, it > 0 ? 1u : 0u);
                         tc::mma_tf32_pair(d, adh, bl, idesc, 1u);
                         tc::mma_tf32_pair(d, adl, bh, idesc, 1u);
@@ -2020,8 +2072,13 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
         const int64_t rbase = (int64_t)(r0 + q * 32) * g.N + n0;
         const int lr = lane >> 3, lc = (lane & 7) * 4;
         float mx[S];  // |Zb_in| bounds per stream (consumers' 3xFP16 scales)
+        float us[S];  // 3xFP16 unscale per stream accumulator 2^-(e_s + e_W)
 #pragma unroll
-        for (int s2 = 0; s2 < S; ++s2) mx[s2] = 0.0f;
+        for (int s2 = 0; s2 < S; ++s2) {
+            mx[s2] = 0.0f;
+            us[s2] = F16 ? ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s2])) * ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w))
+                         : 1.0f;
+        }
         tc::mbar_wait(&tfull, 0);
         tc::tc_fence_after();
         TC_T0();
@@ -2058,7 +2115,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
 #pragma unroll
                     for (int s2 = 0; s2 < S; ++s2) {
                         zz[s2] = z[s2][j];
-                        hh[s2] = hb[s2][j];
+                        hh[s2] = F16 ? hb[s2][j] * us[s2] : hb[s2][j];
                     }
                     act_bwd<L, ACT_TANH>(zz, hh, oo, 1.0f);
 #pragma unroll

@@ -727,8 +727,7 @@ struct Tc4FwdCfg {
     static_assert(NST >= 4, "forward stage ring");
 };
 // warp 18 issues the MMAs, so stream p+1 starts as soon as the epilogue warps
-// have read stream p's accumulators (not after warp 9's own stores)
-constexpr bool kFwdMmaWarp = true;
+// have read stream p's accumulators (not after an epilogue warp's own stores)
 constexpr int TC4_THREADS = 608;  // 19 warps
 
 // F16: 3xFP16 operands (kind::f16, K = 16 per stage) scaled by the recorded
@@ -946,12 +945,12 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
             }
         }
         __syncwarp();
-    } else if (kFwdMmaWarp && warp == 18) {
+    } else if (warp == 18) {
         if (lane == 0 && rank == 0)
             for (int ps = 0; ps < nloc * S; ++ps) issue_stream(ps);
         __syncwarp();
     } else {
-        // ---------------- MMA issue (leader, warp 9 lane 0) + epilogue ----------------
+        // ---------------- epilogue (warps 9-16) ----------------
         // Epilogue: TMEM -> registers -> 128 B-swizzled staging tile (row r, 16 B chunk c
         // at r*128 + ((c ^ r%8) << 4): conflict-free) -> one TMA tensor store per
         // 32 x 32 block; TMEM is released as soon as it is read, the stores drain
@@ -962,8 +961,6 @@ __global__ void __launch_bounds__(TC4_THREADS, 1) k_tc4_fwd(const __grid_constan
         int nst = 0;  // stores issued by this warp (buffer = nst & 1)
         for (int ps = 0; ps < nloc * S; ++ps) {
             const int p = ps % S, r0 = row0(ps / S);
-            if (!kFwdMmaWarp && warp == 9 && lane == 0 && rank == 0) issue_stream(ps);  // (19-warp layout: unused)
-            __syncwarp();
             // 3xFP16 unscale 2^-(eA+eW): one multiply while the power of two is a normal
             // float (always, in practice), else two
             float usA = 1.0f, usW = 1.0f;

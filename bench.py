@@ -485,7 +485,10 @@ def main():
             "data": "synthetic (uniform collocation grid, numpy Xavier init; no dataset)",
             "config": {"workload": name, "pde": wl.res.id, "model": f"tanh MLP {wl.spec.depth}x{H}",
                        "points_total": n_total, "points_per_gpu": rows, "streams": S,
-                       "params": P, "engine": args.engine, "parallelism": f"dp{world}",
+                       "params": P, "engine": args.engine,
+                       "contraction": ("3xFP16 split operands, FP32 accumulate" if use_f16 else
+                                       "3xTF32 split operands, FP32 accumulate" if use_tc else "FP32 FFMA"),
+                       "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (per-step activations >> 126 MB)",
                        "cuda_graph": bool(trainer.graph)},
             "tflops_step": step_flops / (ms_step / 1e3) / 1e12,

@@ -110,6 +110,9 @@ struct pnx_ctx {
     double *d_poy_part = nullptr, *d_pen = nullptr;
     float* d_poy_g = nullptr;
     bool no_penalty = false;  // per-term gradient passes exclude the penalty (trainer.cpp:256-260)
+    // per-term passes 2 and 3 reuse the activations (and their operand bounds) of
+    // pass 1 when the whole step is one chunk: same parameters, same points
+    bool reuse_fwd = false;
     TcWorkspace tc{};
     // kernel-class timing with CUDA events on the launching stream (bench roofline)
     bool prof = false;
@@ -328,7 +331,11 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
     const int L = ctx->layout;
     const int act = ctx->act;
 
-    CK(cudaMemsetAsync(ctx->d_amax, 0, kAmaxLen * sizeof(unsigned), st));
+    const bool reuse = ctx->reuse_fwd && ctx->ld <= ctx->chunk_rows;
+    if (reuse)  // keep the |W| and |Z| bounds of the reused forward, reset the |Zb| ones
+        CK(cudaMemsetAsync(amax_zb(ctx, 0), 0, kMaxLayers * kAmaxS * sizeof(unsigned), st));
+    else
+        CK(cudaMemsetAsync(ctx->d_amax, 0, kAmaxLen * sizeof(unsigned), st));
     {
         dim3 grid(64, Lw);
         k_prep<<<grid, 256, 0, st>>>(d_params, t, ctx->d_W, ctx->d_Wt, ctx->d_bias, ctx->d_amax);
@@ -572,7 +579,13 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         const int nrows = (int)std::min<int64_t>(ctx->chunk_rows, T - c0);
         const int Rpad = (int)roundup(nrows, 256);
         const bool fuse0 = layer0_fused(ctx);
-        if (int r = forward_chunk(c0, nrows, Rpad)) return r;
+        if (reuse) {  // the chunk's input arguments (layer-0 weight gradient, input backward)
+            ia.row0 = c0;
+            ia.nrows = nrows;
+            ia.Rpad = Rpad;
+        } else if (int r = forward_chunk(c0, nrows, Rpad)) {
+            return r;
+        }
         HeadArgs h = head_args(c0, nrows, Rpad);
         if (!multi && (caus || poy)) {
             stats_chunk(c0, nrows, Rpad, nrows);
@@ -1171,10 +1184,13 @@ int pnx_step_terms(pnx_ctx* ctx, const double* params, double* grad_terms_out, d
     if (!ctx || !params || !grad_terms_out) return PNX_ERR_ARG;
     ctx->no_penalty = true;
     int r = PNX_OK;
+    static const bool no_reuse = getenv("PNX_TERMS_NO_REUSE") != nullptr;  // A/B and tests
     for (int k = 0; k < 3 && r == PNX_OK; ++k) {
         const double lam[3] = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0};
+        ctx->reuse_fwd = k > 0 && !no_reuse;
         r = pnx_step(ctx, params, lam, grad_terms_out + (int64_t)k * ctx->P, k == 0 ? losses_out : nullptr);
     }
+    ctx->reuse_fwd = false;
     ctx->no_penalty = false;
     return r;
 }
@@ -1184,11 +1200,14 @@ int pnx_step_terms_device(pnx_ctx* ctx, const float* d_params, float* d_grads, d
     CK(cudaSetDevice(ctx->device));
     ctx->no_penalty = true;
     int r = PNX_OK;
+    static const bool no_reuse = getenv("PNX_TERMS_NO_REUSE") != nullptr;  // A/B and tests
     for (int k = 0; k < 3 && r == PNX_OK; ++k) {
         const double lam[3] = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0};
+        ctx->reuse_fwd = k > 0 && !no_reuse;
         r = run_step(ctx, d_params, lam, d_grads + (int64_t)k * ctx->P, k == 0 ? d_losses : nullptr,
                      reinterpret_cast<cudaStream_t>(stream));
     }
+    ctx->reuse_fwd = false;
     ctx->no_penalty = false;
     return r;
 }

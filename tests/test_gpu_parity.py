@@ -249,6 +249,22 @@ def test_width256_engine_mix_vs_oracle(rff):
         assert abs(losses[0][k] - outs[0][k]) <= LOSS_RTOL * abs(outs[0][k]) + 1e-12
 
 
+@pytest.mark.parametrize("cfg,dims,caus", [("c4", [12, 10, 8], False), ("c1", [24, 20], True)])
+def test_per_term_gradients_reuse_one_forward(cfg, dims, caus):
+    """pnx_step_terms (loss balancing, trainer.cpp:256-260): passes 2 and 3 reuse
+    pass 1's activations and operand bounds; the three gradients must equal three
+    independent steps with unit lambdas bit for bit."""
+    pk = _pkg()
+    wl, col, flat, rffB, *_ = _workload_case(cfg, dims)
+    c = pk.CausalityConfig(4, 2.0, 0.0, 1.0) if caus else None
+    w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, causality=c, **col)
+    g3, l3 = w.step_terms(flat)
+    for k in range(3):
+        lam = tuple(1.0 if i == k else 0.0 for i in range(3))
+        gk, lk = w.step(flat, lam)
+        assert np.array_equal(g3[k], gk), (k, rel_l2(g3[k], gk))
+
+
 def test_chunking_is_invisible_with_causality_and_poynting():
     """Several chunks: causality needs every chunk's segment sums before any
     seed (two-pass forward) and the Poynting nodes ride in chunk 0; the step

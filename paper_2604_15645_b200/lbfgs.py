@@ -163,32 +163,72 @@ class Lbfgs:
 
 
 def lbfgs_refine(worker, params, lambdas, iters: int, cfg: LbfgsConfig = LbfgsConfig(),
-                 poynting_weight: float = 0.0, stream=None):
-    """The quasi-Newton phase of train() (trainer.cpp:558-617) on one worker that
-    holds the whole interior. params: float32/float64 device tensor (updated in
-    place, float32 view kept in sync). Returns (float64 params, records) with one
-    (l_pde, l_ic, l_bc) record per iteration, as MetricsRecord logs them."""
+                 poynting_weight: float = 0.0, stream=None, group=None, world: int = 1, n_total: int = 0):
+    """The quasi-Newton phase of train() (trainer.cpp:558-617). params: float32/
+    float64 device tensor (updated in place, float32 view kept in sync). Returns
+    (float64 params, records) with one (l_pde, l_ic, l_bc) record per iteration,
+    as MetricsRecord logs them.
+
+    The reference runs it full batch on one worker holding the whole interior.
+    Sharded: `worker` may be a list of shard workers on this device and `world`
+    > 1 ranks may each hold shards (process group `group`, `n_total` interior
+    points overall). Every shard's gradient and losses are weighted by its share
+    n_r / N and summed (one all-reduce of [grad | losses] per objective), which is
+    exactly the full-batch mean objective: the PDE term is a mean over all
+    points and the IC/BC/penalty terms are replicated on every shard. All ranks
+    then take identical L-BFGS steps. (Causality weights stay per shard, as in
+    the data-parallel Adam epochs, trainer.cpp:361-367.)"""
     import torch
     dev = params.device
+    workers = list(worker) if isinstance(worker, (list, tuple)) else [worker]
+    sharded = len(workers) > 1 or world > 1
+    if sharded:
+        n_loc = [getattr(w, "n_interior", 0) for w in workers]
+        if world == 1 and not n_total:
+            n_total = sum(n_loc)
+        if not n_total or not all(n_loc):
+            raise ValueError("lbfgs_refine: sharded objective needs every shard's interior size and n_total")
     x = params.detach().double().clone()
     p32 = torch.empty(x.numel(), dtype=torch.float32, device=dev)
     g32 = torch.empty_like(p32)
     losses = torch.zeros(3, dtype=torch.float64, device=dev)
+    acc = torch.zeros(x.numel() + 4, dtype=torch.float64, device=dev)  # [grad | l_pde l_ic l_bc pen]
     lam = tuple(float(v) for v in lambdas)
     last = {}
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
 
     def objective(v):
         p32.copy_(v)
-        worker.step_device(p32, g32, lam, losses, stream=st)
-        torch.cuda.synchronize(dev)
-        worker.check()
-        l = losses.tolist()
+        if not sharded:
+            w = workers[0]
+            w.step_device(p32, g32, lam, losses, stream=st)
+            torch.cuda.synchronize(dev)
+            w.check()
+            l = losses.tolist()
+            pen = w.penalty() if poynting_weight > 0.0 else 0.0
+            grad = g32.double()
+        else:
+            acc.zero_()
+            for w, n in zip(workers, n_loc):
+                w.step_device(p32, g32, lam, losses, stream=st)
+                torch.cuda.synchronize(dev)
+                w.check()
+                share = n / n_total
+                acc[:-4].add_(g32.double(), alpha=share)
+                acc[-4:-1].add_(losses, alpha=share)
+                if poynting_weight > 0.0:
+                    acc[-1] += share * w.penalty()
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+            l = acc[-4:-1].tolist()
+            pen = float(acc[-1])
+            grad = acc[:-4].clone()
         f = lam[0] * l[0] + lam[1] * l[1] + lam[2] * l[2]
         if poynting_weight > 0.0:
-            f += poynting_weight * worker.penalty()
+            f += poynting_weight * pen
         last["losses"] = l
-        return f, g32.double()
+        return f, grad
 
     lb = Lbfgs(cfg)
     records = []

@@ -225,6 +225,7 @@ class Worker:
             a = _axis_major(pts)
         self._chk(self.lib.pnx_set_points(self.ctx, a.ctypes.data_as(C.POINTER(C.c_double)),
                                           a.shape[1], a.shape[0]))
+        self.n_interior = int(a.shape[1])
 
     def set_ic(self, pts: np.ndarray, targets: np.ndarray):
         a = _axis_major(pts)

@@ -265,6 +265,29 @@ def test_per_term_gradients_reuse_one_forward(cfg, dims, caus):
         assert np.array_equal(g3[k], gk), (k, rel_l2(g3[k], gk))
 
 
+def test_lbfgs_sharded_objective_matches_full_batch():
+    """The L-BFGS phase over shards (weighted by n_r/N; unequal shards here) takes
+    the same iterations as the reference's full-batch worker: records within FP32
+    summation noise."""
+    import torch
+    pk = _pkg()
+    from paper_2604_15645_b200.lbfgs import LbfgsConfig, lbfgs_refine
+    wl, col, flat, rffB, *_ = _workload_case("c1", [30, 25])
+    full = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, engine="ffma", **col)
+    n = len(col["interior"])
+    cut = n // 3  # unequal shards: the weighting, not an equal average, makes it exact
+    shards = [pk.make_worker(wl.spec, wl.res, wl.bc, rffB, engine="ffma", **dict(col, interior=col["interior"][a:b]))
+              for a, b in ((0, cut), (cut, n))]
+    recs = []
+    for ws in (full, shards):
+        p = torch.tensor(flat, dtype=torch.float32, device="cuda")
+        _, r = lbfgs_refine(ws, p, (1.0, 1.0, 1.0), 8, LbfgsConfig())
+        recs.append(np.array(r))
+    assert recs[0].shape == recs[1].shape, (recs[0].shape, recs[1].shape)
+    assert np.all(np.abs(recs[1] - recs[0]) <= 1e-4 * np.abs(recs[0]) + 1e-9), np.max(
+        np.abs(recs[1] - recs[0]) / (np.abs(recs[0]) + 1e-30))
+
+
 def test_chunking_is_invisible_with_causality_and_poynting():
     """Several chunks: causality needs every chunk's segment sums before any
     seed (two-pass forward) and the Poynting nodes ride in chunk 0; the step

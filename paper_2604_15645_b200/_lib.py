@@ -10,7 +10,7 @@ LIB_PATH = os.environ.get("PNX_LIB_PATH") or os.path.join(HERE, "libpnx.so")  # 
 
 _lib = None
 
-# Every symbol include/pnx.h declares (checked by tests/test_capi_symbols.py).
+# Every symbol include/pnx.h declares (checked by tests/test_capi_host.py).
 EXPORTS = [
     "pnx_create", "pnx_destroy", "pnx_last_error", "pnx_create_error", "pnx_param_count",
     "pnx_set_points", "pnx_set_ic", "pnx_set_bc", "pnx_step", "pnx_step_device", "pnx_check",

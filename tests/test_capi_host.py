@@ -54,6 +54,19 @@ def test_create_without_gpu_fails_loudly():
         pk.Worker(pk.ModelSpec(2, 8, 2, 1), pk.ResidualSpec("burgers"))
 
 
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: loading a library that is not there raises (in a child
+    interpreter, so this process keeps its loaded libpnx.so)."""
+    import subprocess
+    import sys
+    code = ("from paper_2604_15645_b200 import _lib\n"
+            "try:\n    _lib.load()\nexcept RuntimeError as e:\n    print('RAISED', e)\n")
+    env = dict(os.environ, PNX_LIB_PATH=str(tmp_path / "absent" / "libpnx.so"))
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=120)
+    assert "RAISED" in out.stdout and "no CPU fallback" in out.stdout, out.stdout + out.stderr
+
+
 @pytest.mark.parametrize("name", gi.CASE_NAMES)
 def test_param_layout_mirror(name):
     import paper_2604_15645_b200 as pk

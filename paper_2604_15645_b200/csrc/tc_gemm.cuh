@@ -285,6 +285,8 @@ static __global__ void k_tc_wreduce2(const double* __restrict__ red, int64_t len
 // accumulator drain (~40K cycles vs ~150K per 512 rows) but quantise the grid
 // into coarser waves; pick the cheaper of 512 / 1024 under that model.
 inline int tc_wgrad_rows(int64_t Rpad, int Kin, int nsm) {
+    static const int force = getenv("PNX_WG_ROWS") ? atoi(getenv("PNX_WG_ROWS")) : 0;  // A/B override
+    if (force >= TC_WROWS && force % 8 == 0) return force;
     const int mt = Kin / 128;
     double best = 1e30;
     int pick = TC_WROWS;

@@ -284,9 +284,13 @@ static __global__ void k_tc_wreduce2(const double* __restrict__ red, int64_t len
 // Rows per weight-gradient CTA: larger tiles amortise the per-CTA prologue and
 // accumulator drain (~40K cycles vs ~150K per 512 rows) but quantise the grid
 // into coarser waves; pick the cheaper of 512 / 1024 under that model.
-inline int tc_wgrad_rows(int64_t Rpad, int Kin, int nsm) {
+// The FP32 TMEM accumulation error grows linearly with the tile (DESIGN §4
+// accuracy): 3xTF32 operands stay at 512 rows (2.1e-5 at 1024 rows > the
+// stated 2e-5; 1.4e-5 at 512), 3xFP16 may take 1024 (1.5e-5).
+inline int tc_wgrad_rows(int64_t Rpad, int Kin, int nsm, bool f16) {
     static const int force = getenv("PNX_WG_ROWS") ? atoi(getenv("PNX_WG_ROWS")) : 0;  // A/B override
     if (force >= TC_WROWS && force % 8 == 0) return force;
+    if (!f16) return TC_WROWS;
     const int mt = Kin / 128;
     double best = 1e30;
     int pick = TC_WROWS;

@@ -157,15 +157,17 @@ def test_chunking_is_invisible():
         assert abs(l1[k] - l2[k]) <= 1e-6 * abs(l1[k]) + 1e-12
 
 
-def test_bench_scale_gradient_within_tc_tolerance():
+@pytest.mark.parametrize("engine", ["auto", "tc3xtf32"])
+def test_bench_scale_gradient_within_tc_tolerance(engine):
     """The bench workload's size (C5 model, 1,040,400 interior points): the
-    weight gradient then runs 1024-row tiles (FP32 TMEM accumulation over 4096
-    products per tile -- the dominant error term; small cases pick 512). The
-    FFMA engine (1.1e-7 from the FP64 oracle at C4) stands in for the oracle,
-    which is too slow at this size. Measured 1.5e-5 (512-row tiles 0.9e-5)."""
+    3xFP16 weight gradient then runs 1024-row tiles (FP32 TMEM accumulation over
+    4096 products per tile -- the dominant error term; small cases and 3xTF32
+    keep 512). The FFMA engine (1.1e-7 from the FP64 oracle at C4) stands in for
+    the oracle, which is too slow at this size. Measured 1.5e-5 (3xFP16) and
+    1.4e-5 (3xTF32; 2.1e-5 with 1024-row tiles)."""
     pk = _pkg()
     wl, col, flat, rffB, *_ = _workload_case("c4", [102, 102, 100])
-    w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, **col)
+    w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, engine=engine, **col)
     g16, l16 = w.step(flat)
     w.set_engine("ffma")
     g32, l32 = w.step(flat)

@@ -360,7 +360,16 @@ def main():
         host_params = flat.copy()
         opt_m = np.zeros_like(host_params)
         opt_v = np.zeros_like(host_params)
-        tmp = np.empty_like(host_params)
+        import ctypes
+        hlib = ctypes.CDLL(os.path.join(ROOT, "host", "libpinnlab_b200.so"))  # built by build(); no fallback
+        hadam = hlib.pinnlab_adam_step
+        dptr = ctypes.POINTER(ctypes.c_double)
+        hadam.argtypes = [dptr, dptr, dptr, dptr, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                          ctypes.c_double, ctypes.c_double, ctypes.c_int64]
+        hadam.restype = ctypes.c_int
+
+        def pp(a):
+            return a.ctypes.data_as(dptr)
         shard_pinned = torch.from_numpy(np.ascontiguousarray(shard.T)).pin_memory()  # axis-major [d, N]
         g_dev = torch.zeros(P, dtype=torch.float64, device=dev)
         h2d = d2h = 0
@@ -374,20 +383,9 @@ def main():
                 g_dev.copy_(torch.from_numpy(g_host))
                 dist.all_reduce(g_dev, op=dist.ReduceOp.SUM)
                 g_host = g_dev.cpu().numpy() / world
-            b1, b2 = 0.9, 0.999                          # host Adam (optim.cpp:7-41), in place
-            np.multiply(opt_m, b1, out=opt_m)
-            np.multiply(g_host, 1 - b1, out=tmp)
-            np.add(opt_m, tmp, out=opt_m)
-            np.multiply(g_host, g_host, out=tmp)
-            np.multiply(tmp, 1 - b2, out=tmp)
-            np.multiply(opt_v, b2, out=opt_v)
-            np.add(opt_v, tmp, out=opt_v)
-            np.multiply(opt_v, 1.0 / (1 - b2 ** k), out=tmp)
-            np.sqrt(tmp, out=tmp)
-            np.add(tmp, 1e-8, out=tmp)
-            np.divide(opt_m, tmp, out=tmp)
-            np.multiply(tmp, 1e-3 / (1 - b1 ** k), out=tmp)
-            np.subtract(host_params, tmp, out=host_params)
+            g_host = np.ascontiguousarray(g_host)
+            # host Adam in place (optim.cpp:7-41), the C++ host mirror's fused loop
+            hadam(pp(host_params), pp(opt_m), pp(opt_v), pp(g_host), P, 1e-3, 0.9, 0.999, 1e-8, k)
             h2d = pts.nbytes + P * 4
             d2h = P * 4 + 3 * 8
 
@@ -404,7 +402,7 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": n_total / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(te.item()),
-               "path": "pnx_set_points + pnx_step (float64 host buffers) + host Adam"}
+               "path": "pnx_set_points + pnx_step (float64 host buffers) + host Adam (host/ C++ pinnlab_adam_step)"}
 
     if rank == 0:
         peaks = {}

@@ -230,4 +230,14 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
 
 std::uint64_t param_hash(const std::vector<NamedTensor>& params);
 
+// One Adam update in place (optim.cpp:7-41): t is the 1-based step count, lr
+// already scheduled (optim.cpp:71-73).
+void adam_update(double* p, double* m, double* v, const double* g, std::size_t n, double lr,
+                 const AdamConfig& a, std::int64_t t);
+
 }  // namespace pinnlab_b200
+
+// C ABI of the host Adam, for callers that drive pnx_step with host buffers
+// from another language (bench.py's end-to-end leg). Returns 0.
+extern "C" int pinnlab_adam_step(double* p, double* m, double* v, const double* g, std::int64_t n,
+                                 double lr, double beta1, double beta2, double eps, std::int64_t t);

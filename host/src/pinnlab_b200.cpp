@@ -697,13 +697,7 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
         ++t;
         const AdamConfig& a = cfg.adam;
         const double lr = a.lr * std::pow(cfg.scheduler_gamma, static_cast<double>(epoch));
-        const double bc1 = 1.0 - std::pow(a.beta1, static_cast<double>(t));
-        const double bc2 = 1.0 - std::pow(a.beta2, static_cast<double>(t));
-        for (std::size_t k = 0; k < p.size(); ++k) {
-            m[k] = a.beta1 * m[k] + (1.0 - a.beta1) * g[k];
-            v[k] = a.beta2 * v[k] + (1.0 - a.beta2) * g[k] * g[k];
-            p[k] -= lr * (m[k] / bc1) / (std::sqrt(v[k] / bc2) + a.eps);
-        }
+        adam_update(p.data(), m.data(), v.data(), g.data(), p.size(), lr, a, t);
         std::size_t at = 0;
         for (auto& prm : model.trainable())
             for (auto& x : prm.value.data) x = p[at++];
@@ -759,4 +753,27 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
     return result;
 }
 
+void adam_update(double* p, double* m, double* v, const double* g, std::size_t n, double lr,
+                 const AdamConfig& a, std::int64_t t) {
+    const double bc1 = 1.0 - std::pow(a.beta1, static_cast<double>(t));
+    const double bc2 = 1.0 - std::pow(a.beta2, static_cast<double>(t));
+    for (std::size_t k = 0; k < n; ++k) {
+        m[k] = a.beta1 * m[k] + (1.0 - a.beta1) * g[k];
+        v[k] = a.beta2 * v[k] + (1.0 - a.beta2) * g[k] * g[k];
+        p[k] -= lr * (m[k] / bc1) / (std::sqrt(v[k] / bc2) + a.eps);
+    }
+}
+
 }  // namespace pinnlab_b200
+
+extern "C" int pinnlab_adam_step(double* p, double* m, double* v, const double* g, std::int64_t n,
+                                 double lr, double beta1, double beta2, double eps, std::int64_t t) {
+    pinnlab_b200::AdamConfig a;
+    a.lr = lr;
+    a.beta1 = beta1;
+    a.beta2 = beta2;
+    a.eps = eps;
+    pinnlab_b200::adam_update(p, m, v, g, static_cast<std::size_t>(n), lr, a, t);
+    return 0;
+}
+

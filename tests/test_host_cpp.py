@@ -102,3 +102,26 @@ def test_cpp_train_trajectory_on_gpu(name, tmp_path):
     assert np.all(np.abs(m[:n_adam] - ref[:n_adam]) <= 1e-3 * np.abs(ref[:n_adam]) + 1e-9)
     # L-BFGS rows: FP32 objective, line-search paths may drift
     assert np.all(np.abs(m[n_adam:] - ref[n_adam:]) <= 1e-2 * np.abs(ref[n_adam:]) + 1e-8)
+
+
+def test_cpp_host_adam_matches_oracle_adam():
+    """pinnlab_adam_step (the C++ host mirror's Adam, optim.cpp:7-41; bench.py's
+    end-to-end leg calls it) against the oracle's Adam over five steps (CPU)."""
+    import ctypes
+    from oracle import pinn_oracle as po
+    _driver()
+    lib = ctypes.CDLL(os.path.join(gi.ROOT, "host", "libpinnlab_b200.so"))
+    fn = lib.pinnlab_adam_step
+    dp = ctypes.POINTER(ctypes.c_double)
+    fn.argtypes = [dp, dp, dp, dp, ctypes.c_int64] + [ctypes.c_double] * 4 + [ctypes.c_int64]
+    fn.restype = ctypes.c_int
+    rng = np.random.default_rng(3)
+    p = rng.standard_normal(1001)
+    p_ref = p.copy()
+    m, v = np.zeros_like(p), np.zeros_like(p)
+    opt = po.Adam(lr=2e-3, beta1=0.8, beta2=0.99, eps=1e-7)
+    for t in range(1, 6):
+        g = rng.standard_normal(p.size) * 10.0 ** (t - 3)
+        opt.step(p_ref, g)
+        assert fn(*(a.ctypes.data_as(dp) for a in (p, m, v, g)), p.size, 2e-3, 0.8, 0.99, 1e-7, t) == 0
+        np.testing.assert_allclose(p, p_ref, rtol=1e-14, atol=1e-15)

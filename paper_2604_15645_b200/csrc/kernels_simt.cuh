@@ -1217,9 +1217,19 @@ static __global__ void k_write_scalar_grads(const double* __restrict__ partP, in
 // ---------------------------------------------------------------------------
 // Adam (optim.cpp:7-41) fused with the 1/W average (trainer.cpp:278-280)
 // ---------------------------------------------------------------------------
+// Non-finite gradients (optim.cpp:16-22: "adam: non-finite gradient for
+// parameter <name> at step t" aborts before any update): k_any_nonfinite first
+// records the smallest bad index in bad[0]; the update kernels then skip the
+// whole step (bad[0] != kBadNone) and note its step number in bad[1]; the host
+// reports both at the next pnx_check (the flags are sticky until read).
+constexpr int kBadNone = 0x7f7f7f7f;
 static __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                        float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps,
-                       float bc1, float bc2, float gscale) {
+                       float bc1, float bc2, float gscale, int* __restrict__ bad, int t) {
+    if (*(volatile int*)bad != kBadNone) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(bad + 1, kBadNone, t);
+        return;
+    }
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float gi = g[i] * gscale;
         const float mi = b1 * m[i] + (1.0f - b1) * gi;
@@ -1233,11 +1243,17 @@ static __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g
 // Same update with the step count t and the epoch in device memory (state[0] =
 // steps taken, state[1] = epoch): bias corrections and lr = lr0 gamma^epoch
 // (ExponentialLr::at, optim.cpp:71-73) are formed on the device, so a captured
-// CUDA graph replays correct updates; k_adam_tick advances both after the update.
+// CUDA graph replays correct updates; k_adam_tick advances both after the update
+// (the step count only when the update ran).
 static __global__ void k_adam_state(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                                     float* __restrict__ v, int64_t n, const double* __restrict__ state, double lr0,
-                                    double gamma, double b1d, double b2d, float eps, float gscale) {
+                                    double gamma, double b1d, double b2d, float eps, float gscale,
+                                    int* __restrict__ bad) {
     const double t = state[0] + 1.0;
+    if (*(volatile int*)bad != kBadNone) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(bad + 1, kBadNone, (int)t);
+        return;
+    }
     const float lr = (float)(lr0 * pow(gamma, state[1]));
     const float bc1 = (float)(1.0 - pow(b1d, t)), bc2 = (float)(1.0 - pow(b2d, t));
     const float b1 = (float)b1d, b2 = (float)b2d;
@@ -1250,8 +1266,8 @@ static __global__ void k_adam_state(float* __restrict__ p, const float* __restri
         p[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
     }
 }
-static __global__ void k_adam_tick(double* state) {
-    state[0] += 1.0;
+static __global__ void k_adam_tick(double* state, const int* __restrict__ bad) {
+    if (*bad == kBadNone) state[0] += 1.0;
     state[1] += 1.0;
 }
 

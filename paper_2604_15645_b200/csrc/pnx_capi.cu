@@ -90,7 +90,14 @@ struct pnx_ctx {
     int ibwd_grid = 148;
     double* d_red = nullptr;
     float* d_bc_vals = nullptr;
+    // sticky non-finite flags (first bad index, kBadNone = none), read and reset by
+    // pnx_check: [0..2] residual component (losses.cpp:86-90), [3] Adam gradient
+    // entry, [4] the Adam step it happened at (optim.cpp:16-22)
     int* d_bad = nullptr;
+    // completion of the last step's work (recorded on the launching stream outside
+    // graph capture): host-side writes to step inputs wait on it
+    cudaEvent_t ev_done = nullptr;
+    bool ev_pending = false;
     // 3xFP16 operand bounds (float bits): [|W_l|] [|Z_l[s]|] [|Zb_l[s]|]
     unsigned* d_amax = nullptr;
     float* d_resid = nullptr;
@@ -229,7 +236,10 @@ int causality_counts(pnx_ctx* ctx, const double* tcol, int64_t n) {
     return PNX_OK;
 }
 
+int wait_last_step(pnx_ctx* ctx);
+
 int upload_rows(pnx_ctx* ctx) {
+    if (int r = wait_last_step(ctx)) return r;
     const int d = ctx->in_dim;
     if (ctx->h_int_stale && ctx->d_coords) {  // pull the fast-path interior back before re-layout
         const int64_t off = ctx->int_off_prev;
@@ -347,7 +357,6 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
     CK(cudaMemsetAsync(ctx->d_head_part, 0, (size_t)ctx->head_grid * (ctx->H * ctx->F + ctx->F) * 8, st));
     CK(cudaMemsetAsync(ctx->d_loss_part, 0, (size_t)ctx->head_grid * 3 * 8, st));
     CK(cudaMemsetAsync(ctx->d_partP, 0, (size_t)ctx->ibwd_grid * kMaxAxes * 8, st));
-    CK(cudaMemsetAsync(ctx->d_bad, 0x7f, 3 * sizeof(int), st));
 
     const int64_t T = ctx->ld;
     const int64_t bca0 = 0, bca1 = ctx->n_bca, bcb0 = bca1, bcb1 = bcb0 + ctx->n_bcb;
@@ -722,7 +731,37 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                                                caus ? ctx->d_caus_loss : nullptr);
         CKL();
     }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusNone) {  // a captured step is ordered by its replays' stream
+        CK(cudaEventRecord(ctx->ev_done, st));
+        ctx->ev_pending = true;
+    }
     return PNX_OK;
+}
+
+// Host-side writes of step inputs (points, targets) must not overtake a step
+// still reading them on the caller's stream (pnx_step_device is asynchronous).
+int wait_last_step(pnx_ctx* ctx) {
+    if (ctx->ev_pending) {
+        CK(cudaEventSynchronize(ctx->ev_done));
+        ctx->ev_pending = false;
+    }
+    return PNX_OK;
+}
+
+// name of the trainable() tensor holding flat entry i (model.cpp:64-101)
+std::string param_name(const pnx_ctx* ctx, int64_t i) {
+    const LayerTab& t = ctx->tab;
+    for (int l = 0; l < t.n; ++l) {
+        const std::string L = "layer" + std::to_string(l);
+        if (i >= t.offW[l] && i < t.offW[l] + (int64_t)t.K[l] * t.N[l]) return L + (ctx->rwf ? ".V" : ".W");
+        if (t.offS[l] >= 0 && i >= t.offS[l] && i < t.offS[l] + t.N[l]) return L + ".s";
+        if (i >= t.offB[l] && i < t.offB[l] + t.N[l]) return L + ".b";
+    }
+    for (int a = 0; a < kMaxAxes; ++a)
+        if (ctx->period_off[a] == i) return "periodic.P" + std::to_string(a);
+    return "?";
 }
 
 }  // namespace
@@ -871,7 +910,10 @@ int pnx_create(const pnx_model_desc* m, const pnx_problem_desc* p, int device, p
         (rc = dalloc(ctx, &ctx->d_head_part, (size_t)ctx->head_grid * (ctx->H * ctx->F + ctx->F))) ||
         (rc = dalloc(ctx, &ctx->d_loss_part, (size_t)ctx->head_grid * 3)) ||
         (rc = dalloc(ctx, &ctx->d_partP, (size_t)ctx->ibwd_grid * kMaxAxes)) ||
-        (rc = dalloc(ctx, &ctx->d_bad, 4)) || (rc = dalloc(ctx, &ctx->d_amax, kAmaxLen))) {
+        (rc = dalloc(ctx, &ctx->d_bad, 8)) || (rc = dalloc(ctx, &ctx->d_amax, kAmaxLen)) ||
+        (rc = (cudaMemset(ctx->d_bad, 0x7f, 8 * sizeof(int)) == cudaSuccess ? PNX_OK : PNX_ERR_CUDA)) ||
+        (rc = (cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming) == cudaSuccess ? PNX_OK
+                                                                                                : PNX_ERR_CUDA))) {
         g_create_error = ctx->err;
         pnx_destroy(ctx);
         return rc;
@@ -937,6 +979,7 @@ void pnx_destroy(pnx_ctx* ctx) {
     cudaFree(ctx->d_resid);
     tc_workspace_free(ctx->tc);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -958,6 +1001,7 @@ int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes
         // same row layout (e.g. resampled points, trainer.cpp:421-434): copy the
         // caller's axis-major buffer straight into the interior segment on device
         const int64_t off = ctx->int_off_prev;
+        if (int r = wait_last_step(ctx)) return r;  // the previous step may still read d_coords
         for (int a = 0; a < n_axes; ++a)
             CK(cudaMemcpyAsync(ctx->d_coords + a * ctx->ld + off, coords + a * n, (size_t)n * 8,
                                cudaMemcpyHostToDevice, ctx->stream));
@@ -1053,7 +1097,7 @@ int pnx_last_penalty(pnx_ctx* ctx, double* pen) {
     *pen = 0.0;
     if (ctx->n_poy == 0 || !ctx->d_pen) return PNX_OK;
     CK(cudaSetDevice(ctx->device));
-    CK(cudaStreamSynchronize(ctx->stream));
+    if (int r = wait_last_step(ctx)) return r;
     CK(cudaMemcpy(pen, ctx->d_pen, 8, cudaMemcpyDeviceToHost));
     return PNX_OK;
 }
@@ -1144,12 +1188,23 @@ int pnx_step_device(pnx_ctx* ctx, const float* d_params, const double lambdas[3]
 
 int pnx_check(pnx_ctx* ctx) {
     if (!ctx) return PNX_ERR_ARG;
-    int bad[3];
+    CK(cudaSetDevice(ctx->device));
+    if (int r = wait_last_step(ctx)) return r;
+    int bad[5];
+    CK(cudaDeviceSynchronize());  // Adam may run on another stream than the step
     CK(cudaMemcpy(bad, ctx->d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+    bool any = false;
+    for (int k = 0; k < 5; ++k) any |= bad[k] != kBadNone;
+    if (!any) return PNX_OK;
+    CK(cudaMemset(ctx->d_bad, 0x7f, 8 * sizeof(int)));  // sticky until read
     for (int k = 0; k < ctx->Kres; ++k)
-        if (bad[k] != 0x7f7f7f7f)
+        if (bad[k] != kBadNone)
             return fail(ctx, PNX_ERR_NONFINITE,
                         "residual_loss: non-finite residual at point index " + std::to_string(bad[k]));
+    if (bad[3] != kBadNone)
+        return fail(ctx, PNX_ERR_NONFINITE,
+                    "adam: non-finite gradient for parameter " + param_name(ctx, bad[3]) + " at step " +
+                        (bad[4] != kBadNone ? std::to_string(bad[4]) : std::string("?")));
     return PNX_OK;
 }
 
@@ -1219,10 +1274,12 @@ int pnx_adam_step_device_state(pnx_ctx* ctx, float* d_params, const float* d_gra
     CK(cudaSetDevice(ctx->device));
     const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    k_adam_state<<<grid, 256, 0, st>>>(d_params, d_grad, d_m, d_v, n, d_state, lr0, gamma, beta1, beta2,
-                                       (float)eps, (float)grad_scale);
+    k_any_nonfinite<<<grid, 256, 0, st>>>(d_grad, n, ctx->d_bad + 3);
     CKL();
-    k_adam_tick<<<1, 1, 0, st>>>(d_state);
+    k_adam_state<<<grid, 256, 0, st>>>(d_params, d_grad, d_m, d_v, n, d_state, lr0, gamma, beta1, beta2,
+                                       (float)eps, (float)grad_scale, ctx->d_bad + 3);
+    CKL();
+    k_adam_tick<<<1, 1, 0, st>>>(d_state, ctx->d_bad + 3);
     CKL();
     return PNX_OK;
 }
@@ -1235,9 +1292,11 @@ int pnx_adam_step_device(pnx_ctx* ctx, float* d_params, const float* d_grad, flo
     const float bc1 = (float)(1.0 - std::pow(beta1, (double)t));
     const float bc2 = (float)(1.0 - std::pow(beta2, (double)t));
     const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    k_adam<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        d_params, d_grad, d_m, d_v, n, (float)lr, (float)beta1, (float)beta2, (float)eps, bc1, bc2,
-        (float)grad_scale);
+    const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    k_any_nonfinite<<<grid, 256, 0, st>>>(d_grad, n, ctx->d_bad + 3);
+    CKL();
+    k_adam<<<grid, 256, 0, st>>>(d_params, d_grad, d_m, d_v, n, (float)lr, (float)beta1, (float)beta2, (float)eps,
+                                 bc1, bc2, (float)grad_scale, ctx->d_bad + 3, (int)t);
     CKL();
     return PNX_OK;
 }
@@ -1253,6 +1312,7 @@ int pnx_capture_residuals(pnx_ctx* ctx, int on) {
 int pnx_copy_residuals(pnx_ctx* ctx, double* out) {
     if (!ctx || !out || !ctx->d_resid) return PNX_ERR_ARG;
     CK(cudaSetDevice(ctx->device));
+    if (int r = wait_last_step(ctx)) return r;
     std::vector<float> r((size_t)(ctx->n_int * ctx->Kres));
     CK(cudaMemcpy(r.data(), ctx->d_resid, r.size() * 4, cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < r.size(); ++i) out[i] = r[i];

@@ -85,7 +85,7 @@ class DataParallelTrainer:
 
     def __init__(self, worker, params0: np.ndarray, world: int = 1, lr: float = 1e-3, gamma: float = 1.0,
                  betas=(0.9, 0.999), eps: float = 1e-8, device=None, group=None, balancing=None,
-                 has_bc: bool = True, poynting: bool = False, graph: bool = False):
+                 has_bc: bool = True, poynting: bool = False, graph: bool = False, check_every: int = 100):
         import torch
         self.torch = torch
         self.workers = list(worker) if isinstance(worker, (list, tuple)) else [worker]
@@ -114,6 +114,10 @@ class DataParallelTrainer:
         self._glam = None
         self._warm = False
         self.loss_history = []
+        # non-finite residuals / gradients (losses.cpp:86-90, optim.cpp:16-22) are
+        # flagged on the device (the update is skipped) and raised here every
+        # `check_every` steps and before parameters are read back
+        self.check_every = check_every
 
     def _total(self, lam, st):
         for w, gb, lb in zip(self.workers, self._wgrad, self._wloss):
@@ -199,7 +203,14 @@ class DataParallelTrainer:
             self._warm = True
         self.t += 1
         self.epoch += 1
+        if self.check_every and self.t % self.check_every == 0:
+            self.check()
         return self.losses
+
+    def check(self):
+        """Raise TensorError for a non-finite residual or gradient since the last check."""
+        for w in self.workers:
+            w.check()
 
     def should_switch(self, policy) -> bool:
         """SwitchPolicy check after a step (trainer.cpp:532-554): the history is
@@ -209,4 +220,5 @@ class DataParallelTrainer:
         return policy.should_switch(self.epoch - 1, self.loss_history)
 
     def params_host(self) -> np.ndarray:
+        self.check()
         return self.params.double().cpu().numpy()

@@ -35,6 +35,17 @@ CASES = {
                              model={"in_dim": 2, "hidden_dim": 64, "depth": 4, "out_dim": 1, "activation": "tanh"},
                              collocation={"mode": "uniform", "dims": [16, 16], "n_ic": 32, "n_bc": 16},
                              workers=[1, 4]),
+    # C1 exactly as BASELINE configs[0] runs it: 4x64 on the full 100 x 100 grid
+    "burgers_c1_full": dict(BURGERS, bc="dirichlet_zero",
+                            model={"in_dim": 2, "hidden_dim": 64, "depth": 4, "out_dim": 1, "activation": "tanh"},
+                            collocation={"mode": "uniform", "dims": [100, 100], "n_ic": 128, "n_bc": 64},
+                            workers=[1, 4]),
+    # C4/C5 model at full width (Maxwell TE, tanh 6x256) on a small grid: the
+    # width-256 tensor-core kernels against the reference itself
+    "maxwell_c4_shape": dict(MAXWELL, bc="hard",
+                             model={"in_dim": 3, "hidden_dim": 256, "depth": 6, "out_dim": 3, "activation": "tanh"},
+                             collocation={"mode": "uniform", "dims": [8, 6, 5], "n_ic": 16},
+                             workers=[1, 2]),
     # C2 family: RFF + RWF
     "burgers_rff_rwf": dict(BURGERS, bc="dirichlet_zero",
                             model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1, "activation": "tanh",

@@ -76,6 +76,6 @@ def load(name: str) -> dict:
 
 
 CASE_NAMES = sorted(n[:-4] for n in os.listdir(GOLDEN)
-                    if n.endswith(".npz") and not n.startswith(("traj_", "ckpt_")))
+                    if n.endswith(".npz") and not n.startswith(("traj_", "ckpt_", "bench_")))
 CKPT_NAMES = sorted(n[:-4] for n in os.listdir(GOLDEN) if n.startswith("ckpt_") and n.endswith(".npz"))
 TRAJ_NAMES = sorted(n[:-4] for n in os.listdir(GOLDEN) if n.startswith("traj_") and n.endswith(".npz"))

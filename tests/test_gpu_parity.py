@@ -3,10 +3,12 @@ reference's golden vectors and the FP64 oracle.
 
 Tolerances (FP32 device arithmetic vs FP64 reference):
   gradients  ||g - g_ref||_2 / ||g_ref||_2 <= GRAD_RTOL (north_star: ~1e-5)
-             FFMA engine 1e-5; tcgen05 engines ("auto": 3xFP16 on the
-             CTA-pair kernels at width 256, 3xTF32 elsewhere; "tc3xtf32")
-             2e-5 -- FP32 TMEM accumulation truncates ("3xTF32
-             accuracy"); measured 0.9e-5 (3xFP16) / 1.4e-5 (3xTF32) at C4
+             FFMA engine and the default engine ("auto": 3xFP16 tcgen05
+             kernels at width 256 and 128, 3xTF32 where no 3xFP16 variant
+             exists) 1e-5, also at the bench size against an FP64 fixture;
+             the opt-in "tc3xtf32" engine 2e-5 -- FP32 TMEM accumulation
+             truncates its correction products ("3xTF32 / 3xFP16
+             accuracy"; measured 1.4e-5 at C4)
   losses     |l - l_ref| <= LOSS_RTOL * |l_ref| + 1e-12
   residuals  max |r - r_ref| <= RES_ATOL * (1 + max |r_ref|)
 """
@@ -19,7 +21,8 @@ from oracle import pinn_oracle as po
 pytestmark = pytest.mark.gpu
 
 GRAD_RTOL = 1e-5
-GRAD_RTOL_TC = 2e-5
+GRAD_RTOL_TC = 1e-5     # "auto" (3xFP16 where it applies)
+GRAD_RTOL_TF32 = 2e-5   # opt-in "tc3xtf32"
 LOSS_RTOL = 1e-5
 RES_ATOL = 1e-5
 
@@ -57,6 +60,10 @@ def _objective(g):
     return c, p
 
 
+def _tol(engine):
+    return {"ffma": GRAD_RTOL, "auto": GRAD_RTOL_TC, "tc3xf16": GRAD_RTOL_TC}.get(engine, GRAD_RTOL_TF32)
+
+
 def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
@@ -73,7 +80,7 @@ def test_golden_gradients_and_losses(name, engine):
                                                  workers=w, engine=engine, causality=caus, poynting=poy,
                                                  **_col_args(g))
         ref = g[f"grad_w{w}"]
-        tol = GRAD_RTOL if engine == "ffma" else GRAD_RTOL_TC
+        tol = _tol(engine)
         assert rel_l2(grad, ref) <= tol, (name, w, rel_l2(grad, ref))
         for o, r in zip(losses, g["meta"]["worker_losses"][str(w)]):
             for k in ("pde", "ic", "bc"):
@@ -137,7 +144,7 @@ def test_config_shapes_vs_oracle(cfg, dims, workers, engine):
     ref, outs = po.data_parallel_gradient(ospec, flat, rffB, ores, ocol, wl.bc, workers)
     grad, losses = pk.data_parallel_gradient(wl.spec, wl.res, wl.bc, flat, rffB, workers=workers,
                                              engine=engine, **col)
-    tol = GRAD_RTOL if engine == "ffma" else GRAD_RTOL_TC
+    tol = _tol(engine)
     assert rel_l2(grad, ref) <= tol, rel_l2(grad, ref)
     for o, r in zip(losses, outs):
         for k in ("pde", "ic", "bc"):
@@ -157,23 +164,40 @@ def test_chunking_is_invisible():
         assert abs(l1[k] - l2[k]) <= 1e-6 * abs(l1[k]) + 1e-12
 
 
-@pytest.mark.parametrize("engine", ["auto", "tc3xtf32"])
-def test_bench_scale_gradient_within_tc_tolerance(engine):
-    """The bench workload's size (C5 model, 1,040,400 interior points): the
-    3xFP16 weight gradient then runs 1024-row tiles (FP32 TMEM accumulation over
-    4096 products per tile -- the dominant error term; small cases and 3xTF32
-    keep 512). The FFMA engine (1.1e-7 from the FP64 oracle at C4) stands in for
-    the oracle, which is too slow at this size. Measured 1.5e-5 (3xFP16) and
-    1.4e-5 (3xTF32; 2.1e-5 with 1024-row tiles)."""
+def _bench_fixture():
+    """tests/golden/bench_c4_1M_fp64.npz: the bench workload's FP64 step (made by
+    tests/golden/make_bench_fixture.py with the oracle); regenerate the same
+    inputs the bench builds and check they hash to what the fixture used."""
+    import hashlib
+    import os
     pk = _pkg()
-    wl, col, flat, rffB, *_ = _workload_case("c4", [102, 102, 100])
+    from paper_2604_15645_b200 import configs
+    z = np.load(os.path.join(gi.GOLDEN, "bench_c4_1M_fp64.npz"))
+    wl = configs.get_config("c4")
+    col = configs.collocation(wl, [int(d) for d in z["dims"]])
+    flat, rffB = pk.init_params(wl.spec, seed=int(z["seed"]))
+    h = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()  # noqa: E731
+    assert h(flat) == str(z["params_sha256"]) and h(col["interior"]) == str(z["interior_sha256"])
+    return wl, col, flat, rffB, z
+
+
+@pytest.mark.parametrize("engine", ["auto", "tc3xtf32"])
+def test_bench_scale_gradient_vs_fp64_fixture(engine):
+    """The headline bench step itself (C4/C5: Maxwell TE 6x256, 1,048,576
+    interior points, init seed 0) against its FP64 gradient and losses. At this
+    size the weight gradient sums 512-row tiles (FP32 TMEM accumulation over
+    2048 products per tile is the dominant error term); "auto" (3xFP16) must
+    meet the north_star 1e-5, the opt-in 3xTF32 engine its stated 2e-5."""
+    pk = _pkg()
+    wl, col, flat, rffB, z = _bench_fixture()
     w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, engine=engine, **col)
-    g16, l16 = w.step(flat)
-    w.set_engine("ffma")
-    g32, l32 = w.step(flat)
-    assert rel_l2(g16, g32) <= GRAD_RTOL_TC, rel_l2(g16, g32)
-    for k in l32:
-        assert abs(l16[k] - l32[k]) <= LOSS_RTOL * abs(l32[k]) + 1e-12, (k, l16[k], l32[k])
+    g, l = w.step(flat)
+    ref = z["grad"]
+    err = rel_l2(g, ref)
+    print(f"bench-size gradient rel-L2 ({engine}) vs FP64: {err:.3e}")
+    assert err <= _tol(engine), err
+    for k, r in zip(("pde", "ic", "bc"), z["losses"]):
+        assert abs(l[k] - r) <= LOSS_RTOL * abs(r) + 1e-12, (k, l[k], r)
 
 
 @pytest.mark.parametrize("factor", [0.05, 3.0])
@@ -215,11 +239,11 @@ def test_tensor_core_engines_with_causality_and_poynting(engine):
         if chunk:
             w.set_chunk_rows(chunk)
         g, l = w.step(flat)
-        assert rel_l2(g, ref) <= GRAD_RTOL_TC, (chunk, rel_l2(g, ref))
+        assert rel_l2(g, ref) <= _tol(engine), (chunk, rel_l2(g, ref))
         assert abs(l["pde"] - outs[0]["pde"]) <= LOSS_RTOL * abs(outs[0]["pde"])
         # the penalty (energy drift between time samples) amplifies the forward's
         # relative error: 3xTF32 measured 1.2e-5, 3xFP16 below 1e-5
-        pen_tol = LOSS_RTOL if engine == "auto" else GRAD_RTOL_TC
+        pen_tol = LOSS_RTOL if engine == "auto" else GRAD_RTOL_TF32
         assert abs(w.penalty() - outs[0]["pen"]) <= pen_tol * abs(outs[0]["pen"])
 
 
@@ -447,3 +471,31 @@ def test_adam_trajectory_on_device(name, graph):
             for k in range(3):
                 ref = metrics[ep + 1 + i, 1 + k]
                 assert abs(rec[k] - ref) <= 1e-2 * abs(ref) + 1e-8, (i, k, rec[k], ref)
+
+
+def test_device_adam_rejects_nonfinite_gradient():
+    """optim.cpp:16-22: a non-finite gradient aborts the step before any update
+    ("adam: non-finite gradient for parameter <name> at step t"). On the device
+    the update kernel skips the whole step and the sticky flag surfaces at the
+    next check; the parameters stay finite and unchanged."""
+    import torch
+    pk = _pkg()
+    wl, col, flat, rffB, *_ = _workload_case("c1", [12, 10])
+    w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, **col)
+    dev = torch.device("cuda:0")
+    p = torch.tensor(flat, dtype=torch.float32, device=dev)
+    g = torch.ones_like(p)
+    g[70] = float("nan")  # entry 70 of the flat vector: layer0.W is [2 x 64] (entries 0..127)
+    m, v = torch.zeros_like(p), torch.zeros_like(p)
+    p0 = p.clone()
+    w.adam_step_device(p, g, m, v, 5, 1e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(p, p0)
+    with pytest.raises(pk.TensorError, match=r"adam: non-finite gradient for parameter layer0\.W at step 5"):
+        w.check()
+    w.check()  # flags reset after being reported
+    g[70] = 0.5
+    w.adam_step_device(p, g, m, v, 6, 1e-3)
+    torch.cuda.synchronize()
+    w.check()
+    assert not torch.equal(p, p0)

@@ -202,7 +202,7 @@ int launch_tc2_fwd(int L, int pro, const TcGemmArgs& g, cudaStream_t st) {
     return -1;
 }
 template <int L, int PRO, int NF, bool PAIR, bool F16 = false>
-int launch_tc2_wgrad_t(const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st) {
+int launch_tc2_wgrad_t(const TcWgradArgs& w, int ntiles, int segrows, cudaStream_t st) {
     using Cfg = Tc2WgCfg<Streams<L>::S, NF, PAIR>;
     const int smem = Cfg::SMEM;
     auto kern = k_tc2_wgrad<L, PRO, NF, PAIR, F16>;
@@ -228,7 +228,7 @@ int launch_tc2_wgrad_t(const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, a, wrows) == cudaSuccess ? 0 : -1;
+    return cudaLaunchKernelEx(&cfg, kern, a, segrows, ntiles) == cudaSuccess ? 0 : -1;
 }
 template <int L, int NF, bool PAIR>
 int launch_tc2_wgrad_p(int pro, const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st) {

@@ -648,8 +648,9 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 tw.f16 = f16_wg[l] ? 1 : 0;
                 tw.amaxA = l > 0 ? amax_z(ctx, l - 1) : nullptr;
                 tw.amaxB = amax_zb(ctx, l);
-                const int wr = tc_wgrad_rows(Rpad, t.K[l], ctx->nsm, tw.f16 && tw.amaxA && tw.amaxB);
-                const int ntl = (int)((Rpad + wr - 1) / wr);
+                const int ntl = std::min(tc_wgrad_groups(Rpad, t.K[l], ctx->nsm), TC_WG_MAX_GROUPS);
+                const int wr = tc_wgrad_seg();
+                CK(cudaMemsetAsync(ctx->tc.wpart, 0, (size_t)ntl * t.K[l] * t.N[l] * sizeof(float), st));
                 if (launch_tc2_wgrad(L, pro, tw, ntl, wr, st)) return fail(ctx, PNX_ERR_CUDA, "tc wgrad launch");
                 CKL();
                 {

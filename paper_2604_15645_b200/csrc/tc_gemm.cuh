@@ -281,34 +281,22 @@ static __global__ void k_tc_wreduce2(const double* __restrict__ red, int64_t len
 
 
 // ---------------------------------------------------------------------------
-// Rows per weight-gradient CTA: larger tiles amortise the per-CTA prologue and
-// accumulator drain (~40K cycles vs ~150K per 512 rows) but quantise the grid
-// into coarser waves; pick the cheaper of 512 / 1024 under that model.
-// The FP32 TMEM accumulation error grows linearly with the tile (DESIGN §4
-// accuracy): 3xTF32 operands stay at 512 rows (2.1e-5 at 1024 rows > the
-// stated 2e-5; 1.4e-5 at 512), 3xFP16 may take 1024 (1.5e-5).
-inline int tc_wgrad_rows(int64_t Rpad, int Kin, int nsm, bool f16) {
-    static const int force = getenv("PNX_WG_ROWS") ? atoi(getenv("PNX_WG_ROWS")) : 0;  // A/B override
-    if (force >= TC_WROWS && force % 8 == 0) return force;
-    // 512 rows for both operand kinds: the north_star tolerance (~1e-5 gradient
-    // rel-L2) at the bench size needs the accumulator drained every <= 512 rows
-    // (1024-row 3xFP16 tiles measured 1.5e-5 at 1M points, 512 rows 8.8e-6)
-    static const bool long_tiles = getenv("PNX_WG_LONG") != nullptr;  // A/B only
-    if (!f16 || !long_tiles) return TC_WROWS;
-    const int mt = Kin / 128;
-    double best = 1e30;
-    int pick = TC_WROWS;
-    for (int wr = TC_WROWS; wr <= 2 * TC_WROWS; wr *= 2) {
-        const int64_t ctas = ((Rpad + wr - 1) / wr) * mt;
-        const int64_t waves = (ctas + nsm - 1) / nsm;
-        const double cost = (double)waves * (40.0 + 150.0 * wr / TC_WROWS);
-        if (cost < best * 0.999) {
-            best = cost;
-            pick = wr;
-        }
-    }
-    return pick;
+// Persistent weight gradient (k_tc2_wgrad): G groups of MT = Kin/128 CTAs (one
+// CTA per SM), each over a contiguous row range; the FP32 TMEM accumulator is
+// drained into the group's slot every tc_wgrad_seg() rows. The truncating FP32
+// accumulation error grows linearly with the rows per drain (DESIGN.md §4:
+// 1024 rows 1.5e-5, 512 rows 8.8e-6 gradient rel-L2 at 1M points), so 256 rows
+// keep the headline gradient well inside the north_star ~1e-5.
+inline int tc_wgrad_seg() {
+    static const int force = getenv("PNX_WG_SEG") ? atoi(getenv("PNX_WG_SEG")) : 0;  // A/B override
+    return force >= 8 && force % 8 == 0 ? force : 256;
 }
+inline int tc_wgrad_groups(int64_t Rpad, int Kin, int nsm) {
+    const int mt = Kin / 128;
+    const int64_t g = nsm / mt > 1 ? nsm / mt : 1;
+    return (int)(g < Rpad / 8 ? g : Rpad / 8);
+}
+constexpr int TC_WG_MAX_GROUPS = 256;  // slots allocated (>= SM count)
 
 // the decoupled N=256 backward (k_tc5_bwd): first-order tanh layouts whose
 // backward GEMM writes 256 features (PNX_TC5_OFF=1 falls back to k_tc2_bwd)
@@ -343,7 +331,8 @@ inline int tc_workspace_alloc(TcWorkspace& ws, int, int64_t Rpad, int H, int K0)
             ws.red_cap = need_red;
         }
     }
-    const int64_t tiles = (Rpad + TC_WROWS - 1) / TC_WROWS;
+    (void)Rpad;
+    const int64_t tiles = TC_WG_MAX_GROUPS;  // one FP32 slot per weight-gradient group
     const int64_t kmax = H > K0 ? H : K0;
     const int64_t need = tiles * kmax * H;
     if (need > ws.wpart_cap) {
@@ -392,7 +381,7 @@ __device__ unsigned long long g_tc_trace[8];
 #define TC_ACC(i)
 #endif
 constexpr int TC2_THREADS = 416;
-constexpr int TCW_THREADS = 640;  // 16 converter + 4 MMA/loader/epilogue warps
+constexpr int TCW_THREADS = 704;  // 16 converter + MMA + loader + 4 epilogue warps
 constexpr int TC3_THREADS = 544;  // 8 producer + 1 MMA + 8 epilogue warps
 constexpr int TC2_PROD = 256;
 
@@ -1077,8 +1066,20 @@ struct Tc2WgCfg {
 // of two streams (k-rows 0-7 stream s, 8-15 stream s+1; a group's odd last
 // stream pads with zeros), fp16 MN-major 128 B-swizzled tiles of the same byte
 // size as the tf32 ones.
+//
+// Persistent: CTA group `grp` (one CTA, or the pair / the MT m-tiles of a row
+// block) walks the contiguous 8-row blocks [NB*grp/G, NB*(grp+1)/G) and drains
+// the "big" accumulator every `segrows` rows into its FP32 slot g.wpart[grp]
+// (zeroed before the launch; round-to-nearest red.add, L2-resident: G x Kin x N
+// x 4 B), so the FP32 TMEM
+// accumulation (which truncates, DESIGN.md §4 accuracy) never spans more than
+// `segrows` rows; the "small" accumulator (the hi*lo + lo*hi corrections, 2^-11
+// of the result) keeps accumulating over the whole range and joins the slot at
+// the end. The MMA issuer pauses only for the big drain; loader and converters
+// run ahead through it.
 template <int L, int PRO, int NF, bool PAIR, bool F16 = false>
-__global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_constant__ TcWgradArgs g, int wrows) {
+__global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_constant__ TcWgradArgs g, int segrows,
+                                                             int G) {
     using St = Streams<L>;
     constexpr int S = St::S;
     constexpr int SG = (S + 1) / 2;                                   // streams of converter group 0
@@ -1087,16 +1088,19 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
     constexpr int NST = Cfg::NST, NR = Cfg::NR, NFL = Cfg::NFL;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
-    __shared__ uint64_t full[8], empty[8], rfull[4], rempty[4], tfull;
+    __shared__ uint64_t full[8], empty[8], rfull[4], rempty[4], tfull, tempty;
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int MT = g.Kin / 128;
-    const int tile = blockIdx.x / MT, mt = blockIdx.x % MT;  // PAIR: mt == cluster rank
-    const int rbeg = tile * wrows;
-    const int rend = min(g.Rpad, rbeg + wrows);
-    const int nblk = (rend - rbeg) / 8;
+    const int tile = blockIdx.x / MT, mt = blockIdx.x % MT;  // group; PAIR: mt == cluster rank
+    const int NB = g.Rpad / 8;
+    const int blk0 = (int)((int64_t)NB * tile / G), blk1 = (int)((int64_t)NB * (tile + 1) / G);
+    const int rbeg = blk0 * 8;
+    const int nblk = blk1 - blk0;
     const int nit = nblk * NSTG;
+    const int segit = (segrows / 8) * NSTG;  // MMA k-steps per big-accumulator segment
+    const int nseg = (nit + segit - 1) / segit;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             tc::mbar_init(&full[i], PAIR ? 16 : 8);  // the converter group(s) filling stage i
@@ -1107,6 +1111,7 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
             tc::mbar_init(&rempty[i], 16);
         }
         tc::mbar_init(&tfull, 1);
+        tc::mbar_init(&tempty, PAIR ? 8 : 4);  // the epilogue warps (of both CTAs) drained big
         tc::fence_barrier_init();
     }
     if (warp == 16) {
@@ -1339,13 +1344,17 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
             }
         }
     } else {
-        // warp 16 lane 0 issues the MMAs, warp 17 lane 0 streams the raw blocks;
-        // then warps 16-19 drain TMEM (warp % 4 = lane quarter)
+        // warp 16 lane 0 issues the MMAs, warp 17 lane 0 streams the raw blocks,
+        // warps 18-21 drain TMEM (warp % 4 = lane quarter) once per segment
         if (warp == 16 && lane == 0 && (!PAIR || mt == 0)) {
             constexpr uint32_t idesc = tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NF, 1, 1);
             const uint32_t dbig = tmem, dsmall = tmem + NF;
             for (int it = 0; it < nit; ++it) {
-                const int st = it % NST;
+                const int st = it % NST, sit = it % segit;
+                if (sit == 0 && it > 0) {  // the epilogue drained the previous segment's big
+                    tc::mbar_wait(&tempty, (uint32_t)((it / segit - 1) & 1));
+                    tc::tc_fence_after();
+                }
                 const uint32_t stage = sbase + st * Cfg::STAGE;
                 {
                     TC_T0();
@@ -1353,6 +1362,7 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                     TC_ACC(0);
                 }
                 tc::tc_fence_after();
+                const uint32_t accb = sit > 0 ? 1u : 0u, accs = it > 0 ? 1u : 0u;
                 const uint64_t ah = tc::make_sdesc(stage, 512, 4 * 512, 1);
                 const uint64_t al = tc::make_sdesc(stage + Cfg::A_T, 512, 4 * 512, 1);
                 const uint64_t bh = tc::make_sdesc(stage + 2 * Cfg::A_T, 512, (NFL / 32) * 512, 1);
@@ -1365,30 +1375,32 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                     const uint64_t b16h = tc::make_sdesc(stage + 2 * Cfg::A_T, 1024, (NFL / 64) * 1024, 2);
                     const uint64_t b16l = tc::make_sdesc(stage + 2 * Cfg::A_T + Cfg::B_T, 1024, (NFL / 64) * 1024, 2);
                     if constexpr (PAIR) {
-                        tc::mma_f16_pair(dbig, a16h, b16h, idesc16, it > 0 ? 1u : 0u);
-                        tc::mma_f16_pair(dsmall, a16h, b16l, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_f16_pair(dbig, a16h, b16h, idesc16, accb);
+                        tc::mma_f16_pair(dsmall, a16h, b16l, idesc16, accs);
                         tc::mma_f16_pair(dsmall, a16l, b16h, idesc16, 1u);
                         tc::mma_commit_pair(&empty[st], 3);
                     } else {
-                        tc::mma_f16(dbig, a16h, b16h, idesc16, it > 0 ? 1u : 0u);
-                        tc::mma_f16(dsmall, a16h, b16l, idesc16, it > 0 ? 1u : 0u);
+                        tc::mma_f16(dbig, a16h, b16h, idesc16, accb);
+                        tc::mma_f16(dsmall, a16h, b16l, idesc16, accs);
                         tc::mma_f16(dsmall, a16l, b16h, idesc16, 1u);
                         tc::mma_commit(&empty[st]);
                     }
                 } else if constexpr (PAIR) {
-                    tc::mma_tf32_pair(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
-                    tc::mma_tf32_pair(dsmall, ah, bl, idesc, it > 0 ? 1u : 0u);
+                    tc::mma_tf32_pair(dbig, ah, bh, idesc, accb);
+                    tc::mma_tf32_pair(dsmall, ah, bl, idesc, accs);
                     tc::mma_tf32_pair(dsmall, al, bh, idesc, 1u);
                     tc::mma_commit_pair(&empty[st], 3);
                 } else {
-                    tc::mma_tf32(dbig, ah, bh, idesc, it > 0 ? 1u : 0u);
-                    tc::mma_tf32(dsmall, ah, bl, idesc, it > 0 ? 1u : 0u);
+                    tc::mma_tf32(dbig, ah, bh, idesc, accb);
+                    tc::mma_tf32(dsmall, ah, bl, idesc, accs);
                     tc::mma_tf32(dsmall, al, bh, idesc, 1u);
                     tc::mma_commit(&empty[st]);
                 }
+                if (sit == segit - 1 || it == nit - 1) {
+                    if constexpr (PAIR) tc::mma_commit_pair(&tfull, 3);
+                    else tc::mma_commit(&tfull);
+                }
             }
-            if constexpr (PAIR) tc::mma_commit_pair(&tfull, 3);
-            else tc::mma_commit(&tfull);
         }
         if (warp == 17 && lane == 0) {
             // raw-block loader: two tensor-map copies per 8-row block
@@ -1402,33 +1414,49 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                 tc::tma_load_3d(raw + Cfg::RAW_A, &g.tmB, PAIR ? mt * NFL : 0, row0, 0, &rfull[rs]);
             }
         }
-        __syncwarp();
-        const int q = warp & 3;
-        const int m = q * 32 + lane;
-        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-        float* dst = g.wpart + ((int64_t)tile * g.Kin + mt * 128 + m) * NF;
-        if (nit > 0) {
-            tc::mbar_wait(&tfull, 0);
-            tc::tc_fence_after();
+        if (warp >= 18) {
+            const int q = warp & 3;
+            const int m = q * 32 + lane;
+            const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+            float* dst = g.wpart + ((int64_t)tile * g.Kin + mt * 128 + m) * NF;
+            const uint32_t tempty0 = PAIR ? tc::mapa(tc::smem_u32(&tempty), 0) : tc::smem_u32(&tempty);
+            float us = 1.0f;
+            if constexpr (F16) us = ldexpf(1.0f, -sA) * ldexpf(1.0f, -sB);
+            for (int seg = 0; seg < nseg; ++seg) {
+                const bool last = seg + 1 == nseg;
+                tc::mbar_wait(&tfull, (uint32_t)(seg & 1));
+                tc::tc_fence_after();
+                // big (and, after the last segment, small) in 64-column chunks: four
+                // tcgen05.ld in flight per wait, then 16 fire-and-forget vector
+                // reductions into the L2-resident slot (zeroed before the launch).
+                // Only this thread updates these addresses, so the adds apply in
+                // program (= row, then big-before-small) order: deterministic.
 #pragma unroll 1
-            for (int c = 0; c < NF; c += 16) {
-                float a[16], b[16];
-                tc::tmem_ld16(tl + (uint32_t)c, a);
-                tc::tmem_ld16(tl + (uint32_t)(NF + c), b);
-                tc::tmem_ld_wait();
+                for (int pass = 0; pass < (last ? 2 : 1); ++pass) {
+#pragma unroll 1
+                    for (int c = 0; c < NF; c += 64) {
+                        float a[64];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) a[j] += b[j];
-                if constexpr (F16) {
-                    const float usA = ldexpf(1.0f, -sA), usB = ldexpf(1.0f, -sB);
+                        for (int u = 0; u < 4; ++u) tc::tmem_ld16(tl + (uint32_t)(pass * NF + c + 16 * u), a + 16 * u);
+                        tc::tmem_ld_wait();
+                        if constexpr (F16) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) a[j] = a[j] * usA * usB;
+                            for (int j = 0; j < 64; ++j) a[j] *= us;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + c + 4 * j),
+                                         "f"(a[4 * j]), "f"(a[4 * j + 1]), "f"(a[4 * j + 2]), "f"(a[4 * j + 3])
+                                         : "memory");
+                    }
                 }
-#pragma unroll
-                for (int j = 0; j < 16; j += 4)
-                    *reinterpret_cast<float4*>(dst + c + j) = make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]);
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (PAIR) tc::mbar_arrive_cluster(tempty0);
+                    else tc::mbar_arrive(&tempty);
+                }
             }
-        } else {
-            for (int c = 0; c < NF; ++c) dst[c] = 0.0f;
         }
     }
     tc::tc_fence_before();

@@ -173,6 +173,53 @@ int pnx_profile_read(pnx_ctx* ctx, double* ms, int64_t* counts, int n);
 int pnx_capture_residuals(pnx_ctx* ctx, int on);
 int pnx_copy_residuals(pnx_ctx* ctx, double* out);
 
+/* ---- data-parallel group over the local GPUs (libpnx links NCCL) -------------
+ * Replaces train()'s per-epoch worker threads (trainer.cpp:441-460), the
+ * rank-ordered average_grads (trainer.cpp:264-281) and the replica update
+ * (trainer.cpp:626-638): rank r is a worker context on devices[r] (ranks of one
+ * device are its local replicas), one persistent host thread per device, and
+ * per step ONE ncclAllReduce (sum, float32, in place) of the packed
+ * [grad (P) | l_pde, l_ic, l_bc, pen] over one communicator per device
+ * (ncclCommInitAll), then the device Adam applies the 1/R average to every
+ * device's parameter replica. Interior points are sharded contiguously, the
+ * last rank taking the remainder (shard_interior, trainer.cpp:143-154); IC/BC
+ * sets are replicated on every rank (trainer.cpp:225-232). */
+typedef struct pnx_dp pnx_dp;
+int pnx_device_count(int* n);
+int pnx_dp_create(const pnx_model_desc* model, const pnx_problem_desc* problem, const int* devices, int n_ranks,
+                  pnx_dp** out);
+void pnx_dp_destroy(pnx_dp* dp);
+const char* pnx_dp_last_error(const pnx_dp* dp);
+int pnx_dp_size(const pnx_dp* dp, int* n_ranks, int* n_devices);
+/* The worker context of one rank (engine, chunking, causality, Poynting). */
+int pnx_dp_rank_ctx(pnx_dp* dp, int rank, pnx_ctx** ctx);
+/* Global interior set, axis-major float64 [n_axes][n]; sharded over the ranks. */
+int pnx_dp_set_points(pnx_dp* dp, const double* coords, int64_t n, int32_t n_axes);
+int pnx_dp_set_ic(pnx_dp* dp, const double* coords, const double* targets, int64_t n);
+int pnx_dp_set_bc(pnx_dp* dp, const double* a, const double* b, const double* targets, int64_t n);
+/* Parameters of every replica (flat trainable() order); resets Adam's moments and step. */
+int pnx_dp_set_params(pnx_dp* dp, const double* params);
+/* Host copy of the replica that `rank` trains (for param_hash / on_sync, trainer.cpp:540-544). */
+int pnx_dp_get_params(pnx_dp* dp, int rank, double* params);
+/* AdamConfig + ExponentialLr (optim.hpp:21-50); defaults lr 1e-3, gamma 1, 0.9, 0.999, 1e-8. */
+int pnx_dp_set_optimizer(pnx_dp* dp, double lr, double gamma, double beta1, double beta2, double eps);
+/* Capture each device's step (worker steps + sums + all-reduce + Adam) in a CUDA
+ * graph and replay it while the loss weights stay the same. */
+int pnx_dp_set_graph(pnx_dp* dp, int on);
+/* One synchronized step with loss weights lambdas: update != 0 applies Adam.
+ * losses_out (4: pde, ic, bc, penalty; means over ranks) and grad_out (P, the
+ * averaged gradient) are optional host buffers; with both NULL the call only
+ * enqueues (no host synchronization). Non-finite residuals / gradients raise
+ * PNX_ERR_NONFINITE with the reference's text at the next synchronizing call. */
+int pnx_dp_step(pnx_dp* dp, const double lambdas[3], int update, double* losses_out, double* grad_out);
+/* Per-term gradients averaged over ranks (balancing epochs, trainer.cpp:256-260,
+ * 462-506): grad_terms_out holds 3 x P (pde | ic | bc), losses_out 3. */
+int pnx_dp_step_terms(pnx_dp* dp, double* grad_terms_out, double* losses_out);
+/* Adam step of every replica with a host gradient (the balanced lambda-weighted sum). */
+int pnx_dp_apply_gradient(pnx_dp* dp, const double* grad);
+/* Synchronize and raise any non-finite flag of any rank. */
+int pnx_dp_check(pnx_dp* dp);
+
 #ifdef __cplusplus
 }
 #endif

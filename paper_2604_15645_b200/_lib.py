@@ -18,6 +18,10 @@ EXPORTS = [
     "pnx_capture_residuals", "pnx_copy_residuals", "pnx_profile", "pnx_profile_read",
     "pnx_step_terms", "pnx_step_terms_device", "pnx_set_causality", "pnx_set_poynting", "pnx_last_penalty",
     "pnx_adam_step_device_state",
+    "pnx_device_count", "pnx_dp_create", "pnx_dp_destroy", "pnx_dp_last_error", "pnx_dp_size", "pnx_dp_rank_ctx",
+    "pnx_dp_set_points", "pnx_dp_set_ic", "pnx_dp_set_bc", "pnx_dp_set_params", "pnx_dp_get_params",
+    "pnx_dp_set_optimizer", "pnx_dp_set_graph", "pnx_dp_step", "pnx_dp_step_terms", "pnx_dp_apply_gradient",
+    "pnx_dp_check",
 ]
 
 
@@ -74,8 +78,28 @@ def load(path: str = LIB_PATH):
     lib.pnx_last_penalty.argtypes = [vp, dp]
     lib.pnx_adam_step_device_state.argtypes = [vp, vp, vp, vp, vp, i64, vp, C.c_double, C.c_double, C.c_double,
                                                C.c_double, C.c_double, C.c_double, vp]
+    ip = C.POINTER(C.c_int)
+    lib.pnx_device_count.argtypes = [ip]
+    lib.pnx_dp_create.argtypes = [C.POINTER(ModelDesc), C.POINTER(ProblemDesc), ip, C.c_int, C.POINTER(vp)]
+    lib.pnx_dp_destroy.argtypes = [vp]
+    lib.pnx_dp_destroy.restype = None
+    lib.pnx_dp_last_error.argtypes = [vp]
+    lib.pnx_dp_last_error.restype = C.c_char_p
+    lib.pnx_dp_size.argtypes = [vp, ip, ip]
+    lib.pnx_dp_rank_ctx.argtypes = [vp, C.c_int, C.POINTER(vp)]
+    lib.pnx_dp_set_points.argtypes = [vp, dp, i64, i32]
+    lib.pnx_dp_set_ic.argtypes = [vp, dp, dp, i64]
+    lib.pnx_dp_set_bc.argtypes = [vp, dp, dp, dp, i64]
+    lib.pnx_dp_set_params.argtypes = [vp, dp]
+    lib.pnx_dp_get_params.argtypes = [vp, C.c_int, dp]
+    lib.pnx_dp_set_optimizer.argtypes = [vp] + [C.c_double] * 5
+    lib.pnx_dp_set_graph.argtypes = [vp, C.c_int]
+    lib.pnx_dp_step.argtypes = [vp, dp, C.c_int, dp, dp]
+    lib.pnx_dp_step_terms.argtypes = [vp, dp, dp]
+    lib.pnx_dp_apply_gradient.argtypes = [vp, dp]
+    lib.pnx_dp_check.argtypes = [vp]
     for name in EXPORTS:
-        if name not in ("pnx_destroy", "pnx_last_error", "pnx_create_error"):
+        if name not in ("pnx_destroy", "pnx_last_error", "pnx_create_error", "pnx_dp_destroy", "pnx_dp_last_error"):
             getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpnx.so")
-SOURCES = ["pnx_capi.cu", "launch_simt.cu", "launch_tc.cu"]
+SOURCES = ["pnx_capi.cu", "pnx_dp.cu", "launch_simt.cu", "launch_tc.cu"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -40,7 +40,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if p.wait() != 0:
             raise RuntimeError(f"nvcc failed on {src}")
     tmp = LIB + ".tmp"
-    subprocess.run([nvcc, *GENCODE, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
+    # NCCL (the data-parallel group's all-reduce): the image's libnccl.so.2; in a
+    # process that already loaded torch's bundled libnccl.so.2 the loader reuses it
+    subprocess.run([nvcc, *GENCODE, "-shared", "-o", tmp, *objs, "-lcudart", "-lnccl"], check=True)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

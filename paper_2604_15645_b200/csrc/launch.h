@@ -6,7 +6,47 @@
 #include "kernels_simt.cuh"
 #include "tc_gemm.cuh"
 
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+struct pnx_ctx;
+
 namespace pnx {
+// device pointer of the context's last Poynting penalty (NULL when disabled)
+const double* ctx_penalty_ptr(pnx_ctx* c);
+// message returned by pnx_create_error() (pnx_dp_create failures)
+void set_create_error(const std::string& m);
+// Dynamic shared-memory opt-in of kernel `Kern` for the CURRENT device (function
+// attributes are per device), remembered per device ordinal; thread-safe (racing
+// threads may both set the attribute, which is idempotent).
+template <auto Kern>
+inline int ensure_smem(int smem) {
+    static std::atomic<int> done_bytes[64];  // largest opt-in per device ordinal
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    std::atomic<int>& d = done_bytes[dev & 63];
+    int prev = d.load(std::memory_order_acquire);
+    if (smem <= prev) return 0;
+    if (cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
+    while (smem > prev && !d.compare_exchange_weak(prev, smem)) {
+    }
+    return 0;
+}
+// SM count of the current device (cached per device ordinal)
+inline int device_sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int n = cache[dev & 63].load(std::memory_order_relaxed);
+    if (n == 0) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n < 2) n = 2;
+        cache[dev & 63].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
+
 void launch_input(int L, const InputArgs& a, cudaStream_t st);
 void launch_input_bwd(int L, const InputArgs& a, const float* Hb, double* partP, int grid, cudaStream_t st);
 void launch_gemm(int L, int pro, int epi, int eact, const GemmArgs& g, cudaStream_t st);

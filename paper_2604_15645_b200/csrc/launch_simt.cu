@@ -89,12 +89,8 @@ void launch_wgrad(int L, int pro, const WgradArgs& w, int nsplit, cudaStream_t s
 template <int P, int ACT, int J>
 void launch_head_a(const HeadArgs& h, int grid, cudaStream_t st) {
     const int smem = kHeadWarps * (h.H * PdeTraits<P>::F + PdeTraits<P>::F) * (int)sizeof(double);
-    auto kern = k_head<P, ACT, J>;
-    static int attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = smem;
-    }
+    constexpr auto kern = k_head<P, ACT, J>;
+    ensure_smem<kern>(smem);  // smem grows with H: the per-device opt-in keeps the largest
     kern<<<grid, 32 * kHeadWarps, smem, st>>>(h);
 }
 template <int P, int J>

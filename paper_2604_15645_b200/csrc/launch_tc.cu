@@ -34,12 +34,8 @@ template <int L, int NT, bool PAIR, bool F16 = false>
 int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc2BwdCfg<Streams<L>::S, NT, PAIR>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc2_bwd<L, NT, PAIR, F16>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
-        attr = true;
-    }
+    constexpr auto kern = k_tc2_bwd<L, NT, PAIR, F16>;
+    if (ensure_smem<kern>(smem)) return -1;
     TcGemmArgs a = g;
     if (PAIR && tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)(g.N / NT) * (g.K / 8) * 2 * NT, 1, 8, Cfg::NTL, 1, false))
         return -1;
@@ -60,13 +56,8 @@ int launch_tc2_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
 template <int L, bool PAIR, bool F16>
 int launch_tc5_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc5BwdCfg<L, PAIR>;
-    auto kern = k_tc5_bwd<L, PAIR, F16>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
-            return -1;
-        attr = true;
-    }
+    constexpr auto kern = k_tc5_bwd<L, PAIR, F16>;
+    if (ensure_smem<kern>(Cfg::SMEM)) return -1;
     TcGemmArgs a = g;
     if (PAIR && tc_make_tmap(&a.tmB, g.img, 2, 8, (uint64_t)(g.K / (F16 ? 16 : 8)) * 2 * Cfg::NF, 1, 8, Cfg::NFL, 1,
                              false))
@@ -123,12 +114,8 @@ template <int L, int PRO, int NF, bool F16 = false>
 int launch_tc2_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc3FwdCfg<NF>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc2_fwd<L, PRO, NF, F16>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
-        attr = true;
-    }
+    constexpr auto kern = k_tc2_fwd<L, PRO, NF, F16>;
+    if (ensure_smem<kern>(smem)) return -1;
     kern<<<g.Rpad / TC_M, TC3_THREADS, smem, st>>>(g);
     return 0;
 }
@@ -136,12 +123,8 @@ template <int L, int PRO, bool F16>
 int launch_tc4_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
     using Cfg = Tc4FwdCfg<L>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc4_fwd<L, PRO, F16>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
-        attr = true;
-    }
+    constexpr auto kern = k_tc4_fwd<L, PRO, F16>;
+    if (ensure_smem<kern>(smem)) return -1;
     TcGemmArgs a = g;
     constexpr int S = Streams<L>::S;
     const int nkb = g.K / (F16 ? 16 : 8);
@@ -151,13 +134,7 @@ int launch_tc4_fwd_t(const TcGemmArgs& g, cudaStream_t st) {
         return -1;
     cudaLaunchConfig_t cfg = {};
     // persistent pairs: one per two SMs (each walks tiles pair, pair + npairs, ...)
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nsm < 2) nsm = 2;
-    }
+    const int nsm = device_sm_count();
     const int ntiles = g.Rpad / 256;
     cfg.gridDim = dim3(2 * (ntiles < nsm / 2 ? ntiles : nsm / 2));
     cfg.blockDim = dim3(TC4_THREADS);
@@ -205,12 +182,8 @@ template <int L, int PRO, int NF, bool PAIR, bool F16 = false>
 int launch_tc2_wgrad_t(const TcWgradArgs& w, int ntiles, int segrows, cudaStream_t st) {
     using Cfg = Tc2WgCfg<Streams<L>::S, NF, PAIR>;
     const int smem = Cfg::SMEM;
-    auto kern = k_tc2_wgrad<L, PRO, NF, PAIR, F16>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return -1;
-        attr = true;
-    }
+    constexpr auto kern = k_tc2_wgrad<L, PRO, NF, PAIR, F16>;
+    if (ensure_smem<kern>(smem)) return -1;
     TcWgradArgs a = w;
     constexpr int S = Streams<L>::S;
     if (tc_make_tmap_3d(&a.tmA, w.A, w.Kin, w.Rpad, S, 128, 8, S) ||

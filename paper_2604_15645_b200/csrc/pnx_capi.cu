@@ -767,6 +767,11 @@ std::string param_name(const pnx_ctx* ctx, int64_t i) {
 
 }  // namespace
 
+namespace pnx {
+const double* ctx_penalty_ptr(pnx_ctx* c) { return c->n_poy > 0 && c->d_pen ? c->d_pen : nullptr; }
+void set_create_error(const std::string& m) { g_create_error = m; }
+}  // namespace pnx
+
 // ============================================================================
 // C ABI
 // ============================================================================

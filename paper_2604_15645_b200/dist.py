@@ -7,9 +7,11 @@ Reference protocol (in-process threads there, processes + NCCL here):
 * identical Adam update on every replica                        trainer.cpp:626-638
 * replica consistency hash (FNV-1a) after each step             trainer.cpp:22-35, 540-544
 
-The only collective is one all-reduce of the flat gradient per step (the
-points are partitioned, not exchanged); the 1/W scale is fused into the device
-Adam kernel (pnx_adam_step_device).
+The only collective is one all-reduce per step of the packed
+[grad (P) | l_pde, l_ic, l_bc, pen] float32 buffer (the points are partitioned,
+not exchanged); the 1/W scale is fused into the device Adam kernel
+(pnx_adam_step_device). The C-ABI equivalent for a C++ host is pnx_dp
+(include/pnx.h, paper_2604_15645_b200.pinn.DataParallelGroup).
 """
 from __future__ import annotations
 
@@ -97,8 +99,11 @@ class DataParallelTrainer:
         self.lam = [1.0, 1.0, 1.0]
         dev = device or torch.device("cuda", self.worker.device)
         self.params = torch.tensor(np.asarray(params0), dtype=torch.float32, device=dev)
-        self.grad = torch.zeros_like(self.params)
-        self._wgrad = [torch.zeros_like(self.params) for _ in self.workers]
+        P = self.params.numel()
+        # one packed all-reduce per step: [grad (P) | l_pde, l_ic, l_bc, pen]
+        self.pack = torch.zeros(P + 4, dtype=torch.float32, device=dev)
+        self.grad = self.pack[:P]
+        self._wgrad = [self.grad] + [torch.zeros_like(self.params) for _ in self.workers[1:]]
         self._wloss = [torch.zeros(3, dtype=torch.float64, device=dev) for _ in self.workers]
         self._g3 = None
         self.m = torch.zeros_like(self.params)
@@ -106,9 +111,14 @@ class DataParallelTrainer:
         self.losses = torch.zeros(3, dtype=torch.float64, device=dev)
         self.t = 0
         self.epoch = 0
-        # CUDA-graph mode (one process per GPU without a collective to capture):
-        # Adam keeps (steps, epoch) on the device so one captured step replays.
-        self.graph = graph and world == 1
+        # CUDA-graph mode: Adam keeps (steps, epoch) on the device so one captured
+        # step (worker steps + the NCCL all-reduce + Adam) replays; a gloo
+        # collective (CPU tests) cannot be captured
+        backend = None
+        if world > 1:
+            import torch.distributed as dist
+            backend = dist.get_backend(group)
+        self.graph = graph and (world == 1 or backend == "nccl")
         self.state = torch.zeros(2, dtype=torch.float64, device=dev)
         self._graph = None
         self._glam = None
@@ -120,12 +130,18 @@ class DataParallelTrainer:
         self.check_every = check_every
 
     def _total(self, lam, st):
-        for w, gb, lb in zip(self.workers, self._wgrad, self._wloss):
+        """Every local worker's step, summed into the pack (gradient and loss
+        terms), then ONE all-reduce of the pack."""
+        P = self.params.numel()
+        for i, (w, gb, lb) in enumerate(zip(self.workers, self._wgrad, self._wloss)):
             w.step_device(self.params, gb, lam, lb, stream=st)
-        self.grad.copy_(self._wgrad[0])
-        for gb in self._wgrad[1:]:
-            self.grad.add_(gb)
-        allreduce_sum_(self.grad, self.world, self.group)
+            if i > 0:
+                self.grad.add_(gb)
+        ls = self._wloss[0].clone()
+        for lb in self._wloss[1:]:
+            ls.add_(lb)
+        self.pack[P:P + 3].copy_(ls)
+        allreduce_sum_(self.pack, self.world, self.group)
 
     def _balance(self, st):
         torch = self.torch
@@ -134,11 +150,15 @@ class DataParallelTrainer:
             self._g3 = [torch.zeros(3 * P, dtype=torch.float32, device=self.params.device) for _ in self.workers]
         for w, g3, lb in zip(self.workers, self._g3, self._wloss):
             w.step_terms_device(self.params, g3, lb, stream=st)
-        gs = self._g3[0].clone()
-        for g3 in self._g3[1:]:
-            gs.add_(g3)
+        # one all-reduce of [g_pde | g_ic | g_bc | l_pde, l_ic, l_bc] (trainer.cpp:469-498)
+        gs = torch.zeros(3 * P + 3, dtype=torch.float32, device=self.params.device)
+        for g3 in self._g3:
+            gs[:3 * P].add_(g3)
+        for lb in self._wloss:
+            gs[3 * P:].add_(lb)
         allreduce_sum_(gs, self.world, self.group)
-        terms = gs.view(3, P)
+        terms = gs[:3 * P].view(3, P)
+        self.pack[P:P + 3].copy_(gs[3 * P:])
         avg = terms.double() * (1.0 / self.W)
         norms = [float(avg[k].norm()) for k in range(3)]
         a, lam = self.balancing.alpha, self.lam
@@ -157,10 +177,8 @@ class DataParallelTrainer:
                 self.grad.add_(terms[2], alpha=self.lam[2])
 
     def _finish(self, st):
-        self.losses.copy_(self._wloss[0])
-        for lb in self._wloss[1:]:
-            self.losses.add_(lb)
-        allreduce_sum_(self.losses, self.world, self.group)
+        P = self.params.numel()
+        self.losses.copy_(self.pack[P:P + 3])
         self.losses.mul_(1.0 / self.W)  # MetricsRecord: mean over workers (trainer.cpp:517-526)
         if self.graph:
             self.worker.adam_step_device_state(self.params, self.grad, self.m, self.v, self.state, self.lr,

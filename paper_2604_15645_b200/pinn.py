@@ -157,42 +157,53 @@ def _axis_major(pts: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(pts, dtype=np.float64).T)
 
 
+def _descs(spec: ModelSpec, res: ResidualSpec, bc: str, rff_B):
+    """pnx_model_desc / pnx_problem_desc of a ModelSpec / ResidualSpec (+ the
+    arrays they point to, which must outlive the call)."""
+    per = spec.periodic_axes
+    keep = []
+    md = _lib.ModelDesc()
+    md.in_dim, md.hidden_dim, md.depth, md.out_dim = spec.in_dim, spec.hidden_dim, spec.depth, spec.out_dim
+    md.activation = ACTIVATIONS[spec.activation]
+    md.sine_w0 = spec.sine_w0
+    md.n_periodic_axes = len(per)
+    if per:
+        a = (C.c_int32 * len(per))(*[int(x.periodic) for x in per])
+        b = (C.c_double * len(per))(*[float(x.period) for x in per])
+        c = (C.c_int32 * len(per))(*[int(x.trainable) for x in per])
+        keep += [a, b, c]
+        md.periodic, md.period, md.period_trainable = a, b, c
+    md.rff_width = spec.rff.width if spec.rff else 0
+    if spec.rff:
+        B = np.ascontiguousarray(np.asarray(rff_B, dtype=np.float64))
+        if B.shape != (spec.embedded_width(), spec.rff.width):
+            raise TensorError("rff_B must be [embedded_width x rff.width]")
+        keep.append(B)
+        md.rff_B = B.ctypes.data_as(C.POINTER(C.c_double))
+    md.rwf = 1 if spec.rwf else 0
+    pd = _lib.ProblemDesc()
+    pd.pde = PDES[res.id]
+    pd.advection_c, pd.epsilon, pd.mu, pd.reynolds = res.advection_c, res.epsilon, res.mu, res.reynolds
+    pd.bc = BCS[bc]
+    return md, pd, keep
+
+
 class Worker:
     """One pnx context: a replica of the worker step on one CUDA device."""
 
     def __init__(self, spec: ModelSpec, res: ResidualSpec, bc: str = "hard",
-                 rff_B: Optional[np.ndarray] = None, device: int = 0, engine: str = "auto"):
+                 rff_B: Optional[np.ndarray] = None, device: int = 0, engine: str = "auto", _ctx=None):
         self.lib = _lib.load()
         self.spec, self.res, self.bc = spec, res, bc
-        per = spec.periodic_axes
-        self._keep = []
-        md = _lib.ModelDesc()
-        md.in_dim, md.hidden_dim, md.depth, md.out_dim = spec.in_dim, spec.hidden_dim, spec.depth, spec.out_dim
-        md.activation = ACTIVATIONS[spec.activation]
-        md.sine_w0 = spec.sine_w0
-        md.n_periodic_axes = len(per)
-        if per:
-            a = (C.c_int32 * len(per))(*[int(x.periodic) for x in per])
-            b = (C.c_double * len(per))(*[float(x.period) for x in per])
-            c = (C.c_int32 * len(per))(*[int(x.trainable) for x in per])
-            self._keep += [a, b, c]
-            md.periodic, md.period, md.period_trainable = a, b, c
-        md.rff_width = spec.rff.width if spec.rff else 0
-        if spec.rff:
-            B = np.ascontiguousarray(np.asarray(rff_B, dtype=np.float64))
-            if B.shape != (spec.embedded_width(), spec.rff.width):
-                raise TensorError("rff_B must be [embedded_width x rff.width]")
-            self._keep.append(B)
-            md.rff_B = B.ctypes.data_as(C.POINTER(C.c_double))
-        md.rwf = 1 if spec.rwf else 0
-        pd = _lib.ProblemDesc()
-        pd.pde = PDES[res.id]
-        pd.advection_c, pd.epsilon, pd.mu, pd.reynolds = res.advection_c, res.epsilon, res.mu, res.reynolds
-        pd.bc = BCS[bc]
-        ctx = C.c_void_p()
-        rc = self.lib.pnx_create(C.byref(md), C.byref(pd), device, C.byref(ctx))
-        if rc != 0:
-            raise TensorError(self.lib.pnx_create_error().decode())
+        self._owned = _ctx is None
+        if _ctx is None:
+            md, pd, self._keep = _descs(spec, res, bc, rff_B)
+            ctx = C.c_void_p()
+            rc = self.lib.pnx_create(C.byref(md), C.byref(pd), device, C.byref(ctx))
+            if rc != 0:
+                raise TensorError(self.lib.pnx_create_error().decode())
+        else:  # a rank context owned by a DataParallelGroup
+            ctx = _ctx
         self.ctx = ctx
         n = C.c_int64()
         self.lib.pnx_param_count(ctx, C.byref(n))
@@ -202,9 +213,9 @@ class Worker:
 
     def __del__(self):
         ctx = getattr(self, "ctx", None)
-        if ctx:
+        if ctx and getattr(self, "_owned", False):
             self.lib.pnx_destroy(ctx)
-            self.ctx = None
+        self.ctx = None
 
     def _chk(self, rc):
         if rc != 0:
@@ -403,3 +414,111 @@ def data_parallel_gradient(spec, res, bc, params, rff_B, interior, ic_points, ic
         outs.append(lw)
         g = gw.copy() if g is None else g + gw
     return g * (1.0 / workers), outs
+
+
+class DataParallelGroup:
+    """pnx_dp (include/pnx.h): R ranks over local GPUs -- train()'s worker
+    threads + average_grads + replica update (trainer.cpp:441-460, 264-281,
+    626-638) with one NCCL all-reduce of the packed [grad | losses] per step and
+    the device Adam on every replica. `devices[r]` is rank r's GPU; ranks that
+    share a GPU are summed on it before the all-reduce."""
+
+    def __init__(self, spec: ModelSpec, res: ResidualSpec, bc: str = "hard", rff_B=None,
+                 devices: Sequence[int] = (0,), engine: str = "auto"):
+        self.lib = _lib.load()
+        self.spec, self.res, self.bc = spec, res, bc
+        md, pd, self._keep = _descs(spec, res, bc, rff_B)
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        rc = self.lib.pnx_dp_create(C.byref(md), C.byref(pd), devs, len(devices), C.byref(h))
+        if rc != 0:
+            raise TensorError(self.lib.pnx_create_error().decode() or "pnx_dp_create failed")
+        self.h = h
+        self.R = len(devices)
+        self.devices = list(devices)
+        self.workers = []
+        for r in range(self.R):
+            c = C.c_void_p()
+            self._chk(self.lib.pnx_dp_rank_ctx(h, r, C.byref(c)))
+            self.workers.append(Worker(spec, res, bc, None, device=devices[r], engine=engine, _ctx=c))
+        self.n_params = self.workers[0].n_params
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            for w in getattr(self, "workers", []):
+                w.ctx = None
+            self.lib.pnx_dp_destroy(h)
+            self.h = None
+
+    def _chk(self, rc):
+        if rc != 0:
+            raise TensorError(self.lib.pnx_dp_last_error(self.h).decode())
+
+    def size(self):
+        r, d = C.c_int(), C.c_int()
+        self._chk(self.lib.pnx_dp_size(self.h, C.byref(r), C.byref(d)))
+        return r.value, d.value
+
+    def set_points(self, pts: np.ndarray):
+        a = _axis_major(pts)
+        self._chk(self.lib.pnx_dp_set_points(self.h, a.ctypes.data_as(C.POINTER(C.c_double)), a.shape[1],
+                                             a.shape[0]))
+
+    def set_ic(self, pts, targets):
+        a, t = _axis_major(pts), _axis_major(targets)
+        P = C.POINTER(C.c_double)
+        self._chk(self.lib.pnx_dp_set_ic(self.h, a.ctypes.data_as(P), t.ctypes.data_as(P), a.shape[1]))
+
+    def set_bc(self, a_pts, b_pts=None, targets=None):
+        P = C.POINTER(C.c_double)
+        if a_pts is None:
+            self._chk(self.lib.pnx_dp_set_bc(self.h, None, None, None, 0))
+            return
+        a = _axis_major(a_pts)
+        b = _axis_major(b_pts) if b_pts is not None else None
+        t = _axis_major(targets) if targets is not None else None
+        self._chk(self.lib.pnx_dp_set_bc(self.h, a.ctypes.data_as(P), b.ctypes.data_as(P) if b is not None else None,
+                                         t.ctypes.data_as(P) if t is not None else None, a.shape[1]))
+
+    def set_params(self, flat):
+        p = np.ascontiguousarray(np.asarray(flat, dtype=np.float64))
+        self._chk(self.lib.pnx_dp_set_params(self.h, p.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def params(self, rank: int = 0) -> np.ndarray:
+        out = np.empty(self.n_params, dtype=np.float64)
+        self._chk(self.lib.pnx_dp_get_params(self.h, rank, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def set_optimizer(self, lr=1e-3, gamma=1.0, beta1=0.9, beta2=0.999, eps=1e-8):
+        self._chk(self.lib.pnx_dp_set_optimizer(self.h, lr, gamma, beta1, beta2, eps))
+
+    def set_graph(self, on: bool = True):
+        self._chk(self.lib.pnx_dp_set_graph(self.h, 1 if on else 0))
+
+    def step(self, lambdas=(1.0, 1.0, 1.0), update: bool = True, sync: bool = True, want_grad: bool = False):
+        """One synchronized step; returns ({pde, ic, bc, pen} means over ranks[, averaged grad])
+        when sync, else None (enqueue only)."""
+        lam = (C.c_double * 3)(*lambdas)
+        P = C.POINTER(C.c_double)
+        l4 = (C.c_double * 4)()
+        g = np.empty(self.n_params, dtype=np.float64) if want_grad else None
+        self._chk(self.lib.pnx_dp_step(self.h, lam, 1 if update else 0, l4 if (sync or want_grad) else None,
+                                       g.ctypes.data_as(P) if want_grad else None))
+        if not (sync or want_grad):
+            return None
+        losses = {"pde": l4[0], "ic": l4[1], "bc": l4[2], "pen": l4[3]}
+        return (losses, g) if want_grad else losses
+
+    def step_terms(self):
+        g = np.empty((3, self.n_params), dtype=np.float64)
+        l3 = (C.c_double * 3)()
+        self._chk(self.lib.pnx_dp_step_terms(self.h, g.ctypes.data_as(C.POINTER(C.c_double)), l3))
+        return g, {"pde": l3[0], "ic": l3[1], "bc": l3[2]}
+
+    def apply_gradient(self, g):
+        a = np.ascontiguousarray(np.asarray(g, dtype=np.float64))
+        self._chk(self.lib.pnx_dp_apply_gradient(self.h, a.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def check(self):
+        self._chk(self.lib.pnx_dp_check(self.h))

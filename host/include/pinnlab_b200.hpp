@@ -201,7 +201,10 @@ struct TrainConfig {
     long lbfgs_max_iters = 0;  // quasi-Newton refinement budget after the switch
     LbfgsConfig lbfgs;
     std::array<double, 3> lambdas{1.0, 1.0, 1.0};  // initial loss weights
-    int device = 0;                                 // first CUDA device; worker w uses device + w % ndev
+    int device = 0;  // first CUDA device
+    int gpus = 0;    // GPUs used (0: every visible device from `device` on); worker w runs on
+                     // device + w % gpus -- workers sharing a GPU are summed on it, GPUs join in
+                     // one NCCL all-reduce per step (pnx_dp, include/pnx.h)
     std::function<void(long epoch, std::span<const std::uint64_t>)> on_sync;
 };
 
@@ -225,7 +228,9 @@ std::vector<Tensor> data_parallel_gradient(Model& model, const TrainingProblem& 
                                            int workers);
 
 // Adam training loop (loss balancing, causality weights, Poynting penalty as
-// configured); the per-worker step runs on the GPU.
+// configured): the W worker replicas live on the GPUs (pnx_dp: device steps,
+// one NCCL all-reduce and the device Adam per epoch, CUDA-graph replays);
+// on_sync receives one param_hash per replica, read from that replica's device.
 TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& cfg);
 
 std::uint64_t param_hash(const std::vector<NamedTensor>& params);

@@ -297,26 +297,52 @@ std::vector<double> field_major(const std::vector<std::vector<double>>& t) {
     return v;
 }
 
-std::unique_ptr<Ctx> make_worker(const Model& m, const TrainingProblem& prob, const Points& shard,
-                                 const CollocationData& data, const TrainConfig& cfg) {
-    const int device = cfg.device;
-    const ModelSpec& s = m.spec();
+// pnx_model_desc / pnx_problem_desc of a Model + TrainingProblem (the arrays
+// they point into live in the Descs object)
+struct Descs {
     std::vector<int32_t> per, tr;
     std::vector<double> period;
-    for (const auto& ax : s.periodic_axes) {
-        per.push_back(ax.periodic ? 1 : 0);
-        period.push_back(ax.period);
-        tr.push_back(ax.trainable ? 1 : 0);
+    pnx_model_desc md{};
+    pnx_problem_desc pd{};
+    Descs(const Model& m, const TrainingProblem& prob) {
+        const ModelSpec& s = m.spec();
+        for (const auto& ax : s.periodic_axes) {
+            per.push_back(ax.periodic ? 1 : 0);
+            period.push_back(ax.period);
+            tr.push_back(ax.trainable ? 1 : 0);
+        }
+        md = pnx_model_desc{static_cast<int32_t>(s.in_dim), static_cast<int32_t>(s.hidden_dim),
+                            static_cast<int32_t>(s.depth), static_cast<int32_t>(s.out_dim),
+                            static_cast<int32_t>(s.activation), s.sine_w0, static_cast<int32_t>(per.size()),
+                            per.data(), period.data(), tr.data(), s.rff ? static_cast<int32_t>(s.rff->width) : 0,
+                            s.rff ? m.rff_matrix().data.data() : nullptr, s.rwf ? 1 : 0};
+        pd = pnx_problem_desc{pde_code(prob.residual.id), prob.residual.advection_c, prob.residual.epsilon,
+                              prob.residual.mu, prob.residual.reynolds, static_cast<int32_t>(prob.bc)};
     }
-    pnx_model_desc md{static_cast<int32_t>(s.in_dim), static_cast<int32_t>(s.hidden_dim),
-                      static_cast<int32_t>(s.depth), static_cast<int32_t>(s.out_dim),
-                      static_cast<int32_t>(s.activation), s.sine_w0, static_cast<int32_t>(per.size()),
-                      per.data(), period.data(), tr.data(), s.rff ? static_cast<int32_t>(s.rff->width) : 0,
-                      s.rff ? m.rff_matrix().data.data() : nullptr, s.rwf ? 1 : 0};
-    pnx_problem_desc pd{pde_code(prob.residual.id), prob.residual.advection_c, prob.residual.epsilon,
-                        prob.residual.mu, prob.residual.reynolds, static_cast<int32_t>(prob.bc)};
+};
+
+// causality / Poynting options of one worker context (trainer.cpp:240-247, 361-367)
+void configure_objective(pnx_ctx* c, const TrainingProblem& prob, const TrainConfig& cfg) {
+    auto check = [c](int rc) {
+        if (rc != PNX_OK) throw TensorError(pnx_last_error(c));
+    };
+    const auto& dom = prob.domain.bounds;
+    if (cfg.causality.enabled)  // segments over the last axis
+        check(pnx_set_causality(c, cfg.causality.segments, cfg.causality.epsilon, dom.back()[0], dom.back()[1]));
+    if (cfg.poynting.weight > 0.0 && prob.residual.id == PdeId::maxwell_te) {
+        const double box[6] = {dom[0][0], dom[0][1], dom[1][0], dom[1][1], dom.back()[0], dom.back()[1]};
+        check(pnx_set_poynting(c, cfg.poynting.weight, static_cast<int32_t>(cfg.poynting.grid),
+                               static_cast<int32_t>(cfg.poynting.time_samples), box));
+    }
+}
+
+// Single worker context over a point set (the full-batch L-BFGS objective,
+// trainer.cpp:564-585).
+std::unique_ptr<Ctx> make_worker(const Model& m, const TrainingProblem& prob, const Points& shard,
+                                 const CollocationData& data, const TrainConfig& cfg) {
+    Descs d(m, prob);
     auto w = std::make_unique<Ctx>();
-    if (pnx_create(&md, &pd, device, &w->ctx) != PNX_OK) throw TensorError(pnx_create_error());
+    if (pnx_create(&d.md, &d.pd, cfg.device, &w->ctx) != PNX_OK) throw TensorError(pnx_create_error());
     auto pts = axis_major(shard);
     w->check(pnx_set_points(w->ctx, pts.data(), static_cast<int64_t>(shard.count()),
                             static_cast<int32_t>(shard.coords.size())));
@@ -329,102 +355,59 @@ std::unique_ptr<Ctx> make_worker(const Model& m, const TrainingProblem& prob, co
         w->check(pnx_set_bc(w->ctx, a.data(), b.empty() ? nullptr : b.data(), t.empty() ? nullptr : t.data(),
                             static_cast<int64_t>(data.bc_a.count())));
     }
-    const auto& dom = prob.domain.bounds;
-    if (cfg.causality.enabled)  // segments over the last axis (trainer.cpp:361-367)
-        w->check(pnx_set_causality(w->ctx, cfg.causality.segments, cfg.causality.epsilon, dom.back()[0],
-                                   dom.back()[1]));
-    if (cfg.poynting.weight > 0.0 && prob.residual.id == PdeId::maxwell_te) {  // trainer.cpp:240-247
-        const double box[6] = {dom[0][0], dom[0][1], dom[1][0], dom[1][1], dom.back()[0], dom.back()[1]};
-        w->check(pnx_set_poynting(w->ctx, cfg.poynting.weight, static_cast<int32_t>(cfg.poynting.grid),
-                                  static_cast<int32_t>(cfg.poynting.time_samples), box));
-    }
+    configure_objective(w->ctx, prob, cfg);
     return w;
 }
 
-std::vector<Points> shard_interior(const Points& interior, int workers) {
-    const std::size_t n = interior.count();
-    const std::size_t base = n / static_cast<std::size_t>(workers);
-    if (base == 0) throw TensorError("data parallel: fewer interior points than workers");
-    std::vector<Points> shards;
-    for (int w = 0; w < workers; ++w) {
-        const std::size_t from = static_cast<std::size_t>(w) * base;
-        const std::size_t to = (w + 1 == workers) ? n : from + base;
-        Points p;
-        for (const auto& c : interior.coords) p.coords.emplace_back(c.begin() + from, c.begin() + to);
-        shards.push_back(std::move(p));
+// The data-parallel group (pnx_dp): W ranks, worker w on GPU
+// cfg.device + w % gpus, one NCCL all-reduce per step, device Adam replicas.
+struct Group {
+    pnx_dp* dp = nullptr;
+    ~Group() {
+        if (dp) pnx_dp_destroy(dp);
     }
-    return shards;
+    void check(int rc) const {
+        if (rc != PNX_OK) throw TensorError(pnx_dp_last_error(dp));
+    }
+};
+
+std::unique_ptr<Group> make_group(const Model& m, const TrainingProblem& prob, const CollocationData& data,
+                                  const TrainConfig& cfg, int W) {
+    int ndev = 0;
+    if (pnx_device_count(&ndev) != PNX_OK || ndev <= cfg.device)
+        throw TensorError("pnx: no CUDA device (the B200 path has no CPU fallback)");
+    const int gpus = cfg.gpus > 0 ? std::min(cfg.gpus, ndev - cfg.device) : ndev - cfg.device;
+    std::vector<int> devices;
+    for (int w = 0; w < W; ++w) devices.push_back(cfg.device + w % gpus);
+    Descs d(m, prob);
+    auto g = std::make_unique<Group>();
+    if (pnx_dp_create(&d.md, &d.pd, devices.data(), W, &g->dp) != PNX_OK) throw TensorError(pnx_create_error());
+    if (data.interior.count() < static_cast<std::size_t>(W))
+        throw TensorError("data parallel: fewer interior points than workers");
+    auto pts = axis_major(data.interior);
+    g->check(pnx_dp_set_points(g->dp, pts.data(), static_cast<int64_t>(data.interior.count()),
+                               static_cast<int32_t>(data.interior.coords.size())));
+    auto ic = axis_major(data.ic_points);
+    auto ict = field_major(data.ic_targets);
+    g->check(pnx_dp_set_ic(g->dp, ic.data(), ict.data(), static_cast<int64_t>(data.ic_points.count())));
+    if (prob.bc != TrainingProblem::Bc::hard) {
+        auto a = axis_major(data.bc_a), b = axis_major(data.bc_b);
+        auto t = field_major(data.bc_targets);
+        g->check(pnx_dp_set_bc(g->dp, a.data(), b.empty() ? nullptr : b.data(), t.empty() ? nullptr : t.data(),
+                               static_cast<int64_t>(data.bc_a.count())));
+    }
+    for (int w = 0; w < W; ++w) {
+        pnx_ctx* c = nullptr;
+        g->check(pnx_dp_rank_ctx(g->dp, w, &c));
+        configure_objective(c, prob, cfg);
+    }
+    return g;
 }
 
 std::vector<double> flatten(const std::vector<NamedTensor>& ps) {
     std::vector<double> v;
     for (const auto& p : ps) v.insert(v.end(), p.value.data.begin(), p.value.data.end());
     return v;
-}
-
-struct Step {
-    std::vector<double> grad;
-    double losses[3];
-};
-
-// run every worker's step in its own thread (trainer.cpp:445-457), then the
-// rank-ordered average (trainer.cpp:264-281)
-std::vector<double> synchronized_step(std::vector<std::unique_ptr<Ctx>>& workers, const std::vector<double>& params,
-                                      const std::array<double, 3>& lambdas, std::array<double, 3>& mean_losses) {
-    const std::size_t W = workers.size();
-    std::vector<Step> out(W);
-    std::vector<std::string> errors(W);
-    std::vector<std::thread> threads;
-    for (std::size_t w = 0; w < W; ++w) {
-        out[w].grad.resize(params.size());
-        threads.emplace_back([&, w] {
-            const int rc = pnx_step(workers[w]->ctx, params.data(), lambdas.data(), out[w].grad.data(), out[w].losses);
-            if (rc != PNX_OK) errors[w] = pnx_last_error(workers[w]->ctx);
-        });
-    }
-    for (auto& t : threads) t.join();
-    for (const auto& e : errors)
-        if (!e.empty()) throw TensorError(e);
-    std::vector<double> avg = out[0].grad;
-    for (std::size_t w = 1; w < W; ++w)
-        for (std::size_t k = 0; k < avg.size(); ++k) avg[k] += out[w].grad[k];
-    const double inv = 1.0 / static_cast<double>(W);
-    for (auto& v : avg) v *= inv;
-    mean_losses = {0.0, 0.0, 0.0};
-    for (std::size_t w = 0; w < W; ++w)
-        for (int t = 0; t < 3; ++t) mean_losses[t] += out[w].losses[t] * inv;
-    return avg;
-}
-
-// per-term gradients of every worker (trainer.cpp:256-260), averaged per term
-std::array<std::vector<double>, 3> synchronized_terms(std::vector<std::unique_ptr<Ctx>>& workers,
-                                                     const std::vector<double>& params,
-                                                     std::array<double, 3>& mean_losses) {
-    const std::size_t W = workers.size(), P = params.size();
-    std::vector<std::vector<double>> g(W, std::vector<double>(3 * P));
-    std::vector<std::array<double, 3>> l(W);
-    std::vector<std::string> errors(W);
-    std::vector<std::thread> threads;
-    for (std::size_t w = 0; w < W; ++w)
-        threads.emplace_back([&, w] {
-            const int rc = pnx_step_terms(workers[w]->ctx, params.data(), g[w].data(), l[w].data());
-            if (rc != PNX_OK) errors[w] = pnx_last_error(workers[w]->ctx);
-        });
-    for (auto& t : threads) t.join();
-    for (const auto& e : errors)
-        if (!e.empty()) throw TensorError(e);
-    const double inv = 1.0 / static_cast<double>(W);
-    std::array<std::vector<double>, 3> avg;
-    for (int k = 0; k < 3; ++k) {
-        avg[k].assign(g[0].begin() + k * static_cast<std::ptrdiff_t>(P), g[0].begin() + (k + 1) * static_cast<std::ptrdiff_t>(P));
-        for (std::size_t w = 1; w < W; ++w)
-            for (std::size_t i = 0; i < P; ++i) avg[k][i] += g[w][k * P + i];
-        for (auto& v : avg[k]) v *= inv;
-    }
-    mean_losses = {0.0, 0.0, 0.0};
-    for (std::size_t w = 0; w < W; ++w)
-        for (int t = 0; t < 3; ++t) mean_losses[t] += l[w][t] * inv;
-    return avg;
 }
 
 double dot(const std::vector<double>& a, const std::vector<double>& b) {
@@ -573,16 +556,6 @@ private:
     bool have_grad_ = false;
 };
 
-double vec_norm(const std::vector<double>& v) {  // grad_vec_norm (trainer.cpp:283-288)
-    double s = 0.0;
-    for (double x : v) s += x * x;
-    return std::sqrt(s);
-}
-
-int device_count() {
-    // contexts need a device; pnx_create reports a missing GPU itself
-    return 0;
-}
 
 }  // namespace
 
@@ -605,20 +578,21 @@ std::vector<Tensor> data_parallel_gradient(Model& model, const TrainingProblem& 
                                            int workers) {
     const int W = std::max(1, workers);
     CollocationData data = build_collocation(prob, cfg.collocation, cfg.seed);
-    std::vector<Points> shards = shard_interior(data.interior, W);
-    std::vector<std::unique_ptr<Ctx>> ctxs;
-    for (int w = 0; w < W; ++w) ctxs.push_back(make_worker(model, prob, shards[static_cast<std::size_t>(w)], data, cfg));
-    std::array<double, 3> losses{};
-    std::vector<double> g = synchronized_step(ctxs, flatten(model.trainable()), {1.0, 1.0, 1.0}, losses);
+    auto grp = make_group(model, prob, data, cfg, W);
+    std::vector<double> p = flatten(model.trainable());
+    grp->check(pnx_dp_set_params(grp->dp, p.data()));
+    std::vector<double> g(p.size());
+    double losses[4];
+    const double lam[3] = {1.0, 1.0, 1.0};
+    grp->check(pnx_dp_step(grp->dp, lam, 0, losses, g.data()));  // no update: the averaged gradient
     std::vector<Tensor> out;
     std::size_t at = 0;
-    for (const auto& p : model.trainable()) {
-        Tensor t{p.value.shape, std::vector<double>(g.begin() + static_cast<std::ptrdiff_t>(at),
-                                                    g.begin() + static_cast<std::ptrdiff_t>(at + p.value.size()))};
-        at += p.value.size();
+    for (const auto& prm : model.trainable()) {
+        Tensor t{prm.value.shape, std::vector<double>(g.begin() + static_cast<std::ptrdiff_t>(at),
+                                                      g.begin() + static_cast<std::ptrdiff_t>(at + prm.value.size()))};
+        at += prm.value.size();
         out.push_back(std::move(t));
     }
-    (void)device_count;
     return out;
 }
 
@@ -626,43 +600,52 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
     TrainResult result;
     const int W = std::max(1, cfg.workers);
     CollocationData data = build_collocation(prob, cfg.collocation, cfg.seed);
-    std::vector<Points> shards = shard_interior(data.interior, W);
-    std::vector<std::unique_ptr<Ctx>> ctxs;
-    for (int w = 0; w < W; ++w) ctxs.push_back(make_worker(model, prob, shards[static_cast<std::size_t>(w)], data, cfg));
+    // W worker replicas on the GPUs, one NCCL all-reduce + device Adam per epoch
+    // (trainer.cpp:441-460, 264-281, 626-638)
+    auto grp = make_group(model, prob, data, cfg, W);
     std::vector<double> p = flatten(model.trainable());
-    std::vector<double> m(p.size(), 0.0), v(p.size(), 0.0);
-    std::array<double, 3> lam = cfg.lambdas;  // LossState (losses.hpp:70-78)
+    grp->check(pnx_dp_set_params(grp->dp, p.data()));
+    const AdamConfig& ad = cfg.adam;
+    grp->check(pnx_dp_set_optimizer(grp->dp, ad.lr, cfg.scheduler_gamma, ad.beta1, ad.beta2, ad.eps));
+    grp->check(pnx_dp_set_graph(grp->dp, 1));  // one CUDA graph per device and loss weighting
+    std::array<double, 3> lam = cfg.lambdas;   // LossState (losses.hpp:70-78)
     const bool has_bc = prob.bc != TrainingProblem::Bc::hard;
     const bool pen_on = cfg.poynting.weight > 0.0 && prob.residual.id == PdeId::maxwell_te;
-    std::vector<double> loss_history;
+    const std::size_t P = p.size();
+    std::vector<double> loss_history, terms(3 * P), g(P), replica(P);
     bool switched = false;
     long next_epoch = 0;
-    long t = 0;
+    auto sync_model = [&](int rank) {  // the replica a rank trains -> Model::trainable()
+        grp->check(pnx_dp_get_params(grp->dp, rank, p.data()));
+        std::size_t at = 0;
+        for (auto& prm : model.trainable())
+            for (auto& x : prm.value.data) x = p[at++];
+    };
     for (long epoch = 0; epoch < cfg.epochs; ++epoch) {
-        // optional interior resampling (trainer.cpp:421-434): fresh LHS set with seed + epoch
-        if (cfg.collocation.resample_every > 0 && epoch > 0 && epoch % cfg.collocation.resample_every == 0 &&
-            cfg.collocation.mode != CollocationConfig::Mode::uniform) {
-            CollocationData rd = build_collocation(prob, cfg.collocation, cfg.seed + static_cast<std::uint64_t>(epoch));
-            data.interior = std::move(rd.interior);
-            shards = shard_interior(data.interior, W);
-            for (int w = 0; w < W; ++w) {
-                auto pts = axis_major(shards[static_cast<std::size_t>(w)]);
-                ctxs[static_cast<std::size_t>(w)]->check(
-                    pnx_set_points(ctxs[static_cast<std::size_t>(w)]->ctx, pts.data(),
-                                   static_cast<int64_t>(shards[static_cast<std::size_t>(w)].count()),
-                                   static_cast<int32_t>(shards[static_cast<std::size_t>(w)].coords.size())));
-            }
-        }
-        std::array<double, 3> losses{};
-        std::vector<double> g;
-        const bool balance_now = cfg.balancing.enabled && cfg.balancing.update_period > 0 &&
-                                 epoch % cfg.balancing.update_period == 0;
+        double losses[4] = {0, 0, 0, 0};
         try {
+            // optional interior resampling (trainer.cpp:421-434): fresh LHS set with seed + epoch
+            if (cfg.collocation.resample_every > 0 && epoch > 0 && epoch % cfg.collocation.resample_every == 0 &&
+                cfg.collocation.mode != CollocationConfig::Mode::uniform) {
+                CollocationData rd =
+                    build_collocation(prob, cfg.collocation, cfg.seed + static_cast<std::uint64_t>(epoch));
+                data.interior = std::move(rd.interior);
+                auto pts = axis_major(data.interior);
+                grp->check(pnx_dp_set_points(grp->dp, pts.data(), static_cast<int64_t>(data.interior.count()),
+                                             static_cast<int32_t>(data.interior.coords.size())));
+            }
+            const bool balance_now = cfg.balancing.enabled && cfg.balancing.update_period > 0 &&
+                                     epoch % cfg.balancing.update_period == 0;
             if (!balance_now) {
-                g = synchronized_step(ctxs, p, lam, losses);
-            } else {  // trainer.cpp:462-506
-                auto terms = synchronized_terms(ctxs, p, losses);
-                std::array<double, 3> norms{vec_norm(terms[0]), vec_norm(terms[1]), has_bc ? vec_norm(terms[2]) : 0.0};
+                grp->check(pnx_dp_step(grp->dp, lam.data(), 1, losses, nullptr));
+            } else {  // trainer.cpp:462-506: per-term gradients (one all-reduce), new lambdas
+                grp->check(pnx_dp_step_terms(grp->dp, terms.data(), losses));
+                auto norm = [&](int k) {
+                    double s2 = 0.0;
+                    for (std::size_t i = 0; i < P; ++i) s2 += terms[k * P + i] * terms[k * P + i];
+                    return std::sqrt(s2);
+                };
+                std::array<double, 3> norms{norm(0), norm(1), has_bc ? norm(2) : 0.0};
                 const double a = cfg.balancing.alpha;
                 const std::array<double, 3> old = lam;
                 const double tot = norms[0] + norms[1] + (has_bc ? norms[2] : 0.0);
@@ -670,41 +653,36 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
                     lam[static_cast<std::size_t>(k)] = a * lam[static_cast<std::size_t>(k)] +
                                                        (1.0 - a) * (tot / std::max(norms[static_cast<std::size_t>(k)], 1e-9));
                 if (pen_on) {  // total gradient under the previous weights (trainer.cpp:491-498)
-                    std::array<double, 3> l2{};
-                    g = synchronized_step(ctxs, p, old, l2);
+                    double l4[4];
+                    grp->check(pnx_dp_step(grp->dp, old.data(), 1, l4, nullptr));
                 } else {
-                    g.assign(p.size(), 0.0);
-                    for (std::size_t i = 0; i < g.size(); ++i) {
-                        double s = lam[0] * terms[0][i] + lam[1] * terms[1][i];
-                        if (has_bc) s += lam[2] * terms[2][i];
-                        g[i] = s;
+                    for (std::size_t i = 0; i < P; ++i) {
+                        double s2 = lam[0] * terms[i] + lam[1] * terms[P + i];
+                        if (has_bc) s2 += lam[2] * terms[2 * P + i];
+                        g[i] = s2;
                     }
+                    grp->check(pnx_dp_apply_gradient(grp->dp, g.data()));
+                    grp->check(pnx_dp_check(grp->dp));  // Adam's non-finite check (optim.cpp:16-22)
                 }
             }
-        } catch (const std::exception& e) {
+        } catch (const std::exception& e) {  // TensorError with the reference's text
             result.aborted = true;
             result.abort_reason = e.what();
             break;
         }
-        // Adam (optim.cpp:7-41) with lr = base * gamma^epoch (optim.cpp:71-73)
-        for (std::size_t k = 0; k < g.size(); ++k)
-            if (!std::isfinite(g[k])) {
-                result.aborted = true;
-                result.abort_reason = "adam: non-finite gradient at step " + std::to_string(t + 1);
-                break;
-            }
-        if (result.aborted) break;
-        ++t;
-        const AdamConfig& a = cfg.adam;
-        const double lr = a.lr * std::pow(cfg.scheduler_gamma, static_cast<double>(epoch));
-        adam_update(p.data(), m.data(), v.data(), g.data(), p.size(), lr, a, t);
-        std::size_t at = 0;
-        for (auto& prm : model.trainable())
-            for (auto& x : prm.value.data) x = p[at++];
+        const double lr = ad.lr * std::pow(cfg.scheduler_gamma, static_cast<double>(epoch));  // optim.cpp:71-73
         result.metrics.push_back({epoch, losses[0], losses[1], losses[2], lam[0], lam[1], lam[2], lr});
         loss_history.push_back(lam[0] * losses[0] + lam[1] * losses[1] + lam[2] * losses[2]);
-        if (cfg.on_sync) {
-            std::vector<std::uint64_t> hashes(static_cast<std::size_t>(W), param_hash(model.trainable()));
+        if (cfg.on_sync) {  // one hash per replica, each from its own device copy (trainer.cpp:540-544)
+            std::vector<std::uint64_t> hashes;
+            std::vector<NamedTensor> view = model.trainable();
+            for (int w = 0; w < W; ++w) {
+                grp->check(pnx_dp_get_params(grp->dp, w, replica.data()));
+                std::size_t at = 0;
+                for (auto& prm : view)
+                    for (auto& x : prm.value.data) x = replica[at++];
+                hashes.push_back(param_hash(view));
+            }
             cfg.on_sync(epoch, hashes);
         }
         ++result.epochs_run;
@@ -714,6 +692,7 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
             break;
         }
     }
+    sync_model(0);
     if (switched && !result.aborted) {  // quasi-Newton refinement, full batch (trainer.cpp:558-617)
         result.switched_to_lbfgs = true;
         auto full = make_worker(model, prob, data.interior, data, cfg);

@@ -142,8 +142,9 @@ int main(int argc, char** argv) {
             cfg.epochs = static_cast<long>(num("epochs", 10));
             cfg.adam.lr = num("lr", 1e-3);
             cfg.scheduler_gamma = num("gamma", 1.0);
-            std::vector<std::uint64_t> last;
-            cfg.on_sync = [&last](long, std::span<const std::uint64_t> h) { last.assign(h.begin(), h.end()); };
+            cfg.gpus = static_cast<int>(num("gpus", 0));
+            std::vector<std::vector<std::uint64_t>> sync;  // per epoch: one hash per replica
+            cfg.on_sync = [&sync](long, std::span<const std::uint64_t> h) { sync.emplace_back(h.begin(), h.end()); };
             TrainResult r = train(model, prob, cfg);
             if (r.aborted) throw TensorError(r.abort_reason);
             std::vector<double> m;
@@ -155,8 +156,11 @@ int main(int argc, char** argv) {
             std::vector<double> p;
             for (const auto& t : model.trainable()) p.insert(p.end(), t.value.data.begin(), t.value.data.end());
             write_f64(out + "/final.bin", p);
-            std::ofstream os(out + "/hash.txt");
-            for (auto h : last) os << h << "\n";
+            std::ofstream os(out + "/hash.txt");  // one line per epoch, one hash per replica
+            for (const auto& row : sync) {
+                for (auto h : row) os << h << " ";
+                os << "\n";
+            }
         } else {
             throw TensorError("unknown mode " + mode);
         }

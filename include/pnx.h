@@ -89,6 +89,17 @@ int pnx_param_count(const pnx_ctx* ctx, int64_t* n);
 /* Interior collocation shard (WorkerTask::interior, trainer.cpp:192), axis-major
  * float64 [n_axes][n] (Points::coords, losses.hpp:39-43; space first, time last). */
 int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes);
+/* Interior points generated on the device instead (sampling.cpp:10-103): design
+ * mode 0 = uniform tensor grid of linspace axes, last axis fastest
+ * (sample_uniform; bit-exact), 1 = joint Latin hypercube of n_total points
+ * (sample_lhs), 2 = per-axis jittered LHS (sample_lhs_per_axis); bounds =
+ * {lo0, hi0, lo1, hi1, ...} per axis (Domain::bounds), dims per axis (modes 0/2).
+ * This worker's shard is rows [row_lo, row_hi) of the global design (no host
+ * copy, no upload). Randomness is counter-based on (seed, axis, index), not the
+ * reference's mt19937_64 stream; same designs. Resampling (trainer.cpp:421-434)
+ * with seed + epoch regenerates in place. */
+int pnx_sample_points(pnx_ctx* ctx, int32_t mode, const double* bounds, const int64_t* dims, int64_t n_total,
+                      uint64_t seed, int64_t row_lo, int64_t row_hi);
 /* Replicated IC set + per-field targets [out_dim][n] (CollocationData::ic_points /
  * ic_targets, trainer.hpp:140-146; losses.cpp:113-119). */
 int pnx_set_ic(pnx_ctx* ctx, const double* coords, const double* targets, int64_t n);
@@ -172,6 +183,9 @@ int pnx_profile_read(pnx_ctx* ctx, double* ms, int64_t* counts, int n);
  * [K][n_interior] as float64. */
 int pnx_capture_residuals(pnx_ctx* ctx, int on);
 int pnx_copy_residuals(pnx_ctx* ctx, double* out);
+/* The interior points the next step uses, axis-major float64 [n_axes][n]
+ * (e.g. a device design from pnx_sample_points). */
+int pnx_copy_points(pnx_ctx* ctx, double* out);
 
 /* ---- data-parallel group over the local GPUs (libpnx links NCCL) -------------
  * Replaces train()'s per-epoch worker threads (trainer.cpp:441-460), the
@@ -195,6 +209,9 @@ int pnx_dp_size(const pnx_dp* dp, int* n_ranks, int* n_devices);
 int pnx_dp_rank_ctx(pnx_dp* dp, int rank, pnx_ctx** ctx);
 /* Global interior set, axis-major float64 [n_axes][n]; sharded over the ranks. */
 int pnx_dp_set_points(pnx_dp* dp, const double* coords, int64_t n, int32_t n_axes);
+/* The global interior as a device design (pnx_sample_points), each rank generating its shard. */
+int pnx_dp_sample_points(pnx_dp* dp, int32_t mode, const double* bounds, const int64_t* dims, int64_t n_total,
+                         uint64_t seed);
 int pnx_dp_set_ic(pnx_dp* dp, const double* coords, const double* targets, int64_t n);
 int pnx_dp_set_bc(pnx_dp* dp, const double* a, const double* b, const double* targets, int64_t n);
 /* Parameters of every replica (flat trainable() order); resets Adam's moments and step. */

@@ -21,7 +21,7 @@ EXPORTS = [
     "pnx_device_count", "pnx_dp_create", "pnx_dp_destroy", "pnx_dp_last_error", "pnx_dp_size", "pnx_dp_rank_ctx",
     "pnx_dp_set_points", "pnx_dp_set_ic", "pnx_dp_set_bc", "pnx_dp_set_params", "pnx_dp_get_params",
     "pnx_dp_set_optimizer", "pnx_dp_set_graph", "pnx_dp_step", "pnx_dp_step_terms", "pnx_dp_apply_gradient",
-    "pnx_dp_check",
+    "pnx_dp_check", "pnx_sample_points", "pnx_dp_sample_points", "pnx_copy_points",
 ]
 
 
@@ -98,6 +98,10 @@ def load(path: str = LIB_PATH):
     lib.pnx_dp_step_terms.argtypes = [vp, dp, dp]
     lib.pnx_dp_apply_gradient.argtypes = [vp, dp]
     lib.pnx_dp_check.argtypes = [vp]
+    lp = C.POINTER(C.c_int64)
+    lib.pnx_sample_points.argtypes = [vp, i32, dp, lp, i64, C.c_uint64, i64, i64]
+    lib.pnx_copy_points.argtypes = [vp, dp]
+    lib.pnx_dp_sample_points.argtypes = [vp, i32, dp, lp, i64, C.c_uint64]
     for name in EXPORTS:
         if name not in ("pnx_destroy", "pnx_last_error", "pnx_create_error", "pnx_dp_destroy", "pnx_dp_last_error"):
             getattr(lib, name).restype = C.c_int

@@ -23,6 +23,7 @@
 #include "kernels_simt.cuh"
 #include "tc_gemm.cuh"
 #include "launch.h"
+#include "sampling.cuh"
 
 using namespace pnx;
 
@@ -103,6 +104,10 @@ struct pnx_ctx {
     float* d_resid = nullptr;
     int64_t resid_cap = 0;
     bool h_int_stale = false;  // interior coordinates newer on device than in h_int
+    // interior generated on the device (pnx_sample_points): no host copy; a
+    // re-layout regenerates it from the design below
+    bool int_on_device = false;
+    SampleArgs samp{};
     int64_t int_off_prev = 0;  // first interior row of the uploaded layout
     bool capture_resid = false;
     // objective terms whose seeds need a global reduction first (trainer.cpp:209-247)
@@ -238,10 +243,30 @@ int causality_counts(pnx_ctx* ctx, const double* tcol, int64_t n) {
 
 int wait_last_step(pnx_ctx* ctx);
 
+// generate the device design into the interior segment (rows laid out, ld set)
+// and recount the causality segments on the device; synchronous on ctx->stream
+int generate_interior(pnx_ctx* ctx) {
+    SampleArgs a = ctx->samp;
+    a.out = ctx->d_coords + ctx->int_off_prev;
+    a.ld = ctx->ld;
+    const unsigned grid = (unsigned)std::min<int64_t>((a.nrows + 255) / 256, 148 * 16);
+    k_sample<<<grid, 256, 0, ctx->stream>>>(a);
+    CK(cudaGetLastError());
+    if (ctx->caus_M > 0) {
+        CK(cudaMemsetAsync(ctx->d_caus_cnt, 0, (size_t)ctx->caus_M * 8, ctx->stream));
+        k_segment_counts<<<grid, 256, 0, ctx->stream>>>(a.out + (int64_t)(ctx->in_dim - 1) * a.ld, a.nrows,
+                                                        ctx->caus_M, ctx->caus_tlo, ctx->caus_thi - ctx->caus_tlo,
+                                                        ctx->d_caus_cnt);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PNX_OK;
+}
+
 int upload_rows(pnx_ctx* ctx) {
     if (int r = wait_last_step(ctx)) return r;
     const int d = ctx->in_dim;
-    if (ctx->h_int_stale && ctx->d_coords) {  // pull the fast-path interior back before re-layout
+    if (ctx->h_int_stale && ctx->d_coords && !ctx->int_on_device) {  // pull the fast-path interior back before re-layout
         const int64_t off = ctx->int_off_prev;
         for (int a = 0; a < d; ++a)
             CK(cudaMemcpy(ctx->h_int.data() + a * ctx->n_int, ctx->d_coords + a * ctx->ld + off,
@@ -251,22 +276,34 @@ int upload_rows(pnx_ctx* ctx) {
     const int64_t T = ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_poy + ctx->n_int;
     ctx->ld = T;
     ctx->int_off_prev = ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_poy;
-    std::vector<double> all((size_t)(d * T));
+    // host-assembled rows: all of them, or only the replicated ones when the
+    // interior is a device design (no host copy of a 64M-point set)
+    const int64_t Th = ctx->int_on_device ? T - ctx->n_int : T;
+    std::vector<double> all((size_t)(d * Th));
     auto put = [&](const std::vector<double>& src, int64_t n, int64_t at) {
         for (int a = 0; a < d; ++a)
-            for (int64_t i = 0; i < n; ++i) all[(size_t)(a * T + at + i)] = src[(size_t)(a * n + i)];
+            for (int64_t i = 0; i < n; ++i) all[(size_t)(a * Th + at + i)] = src[(size_t)(a * n + i)];
     };
     put(ctx->h_bca, ctx->n_bca, 0);
     put(ctx->h_bcb, ctx->n_bcb, ctx->n_bca);
     put(ctx->h_ic, ctx->n_ic, ctx->n_bca + ctx->n_bcb);
     put(ctx->h_poy, ctx->n_poy, ctx->n_bca + ctx->n_bcb + ctx->n_ic);
-    put(ctx->h_int, ctx->n_int, ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_poy);
-    if (int r = causality_counts(ctx, ctx->h_int.data() + (size_t)(d - 1) * ctx->n_int, ctx->n_int)) return r;
-    if ((int64_t)all.size() > ctx->coords_cap) {
-        if (int r = dalloc(ctx, &ctx->d_coords, all.size())) return r;
-        ctx->coords_cap = (int64_t)all.size();
+    if (!ctx->int_on_device) {
+        put(ctx->h_int, ctx->n_int, ctx->n_bca + ctx->n_bcb + ctx->n_ic + ctx->n_poy);
+        if (int r = causality_counts(ctx, ctx->h_int.data() + (size_t)(d - 1) * ctx->n_int, ctx->n_int)) return r;
     }
-    CK(cudaMemcpy(ctx->d_coords, all.data(), all.size() * 8, cudaMemcpyHostToDevice));
+    if (d * T > ctx->coords_cap) {
+        if (int r = dalloc(ctx, &ctx->d_coords, (size_t)(d * T))) return r;
+        ctx->coords_cap = d * T;
+    }
+    if (ctx->int_on_device) {  // replicated rows from the host, the interior from the device design
+        for (int a = 0; a < d && Th > 0; ++a)
+            CK(cudaMemcpy(ctx->d_coords + a * T, all.data() + (size_t)(a * Th), (size_t)Th * 8,
+                          cudaMemcpyHostToDevice));
+        if (int r = generate_interior(ctx)) return r;
+    } else {
+        CK(cudaMemcpy(ctx->d_coords, all.data(), all.size() * 8, cudaMemcpyHostToDevice));
+    }
     if (int r = dalloc(ctx, &ctx->d_ic_t, ctx->h_ic_t.size())) return r;
     if (!ctx->h_ic_t.empty())
         CK(cudaMemcpy(ctx->d_ic_t, ctx->h_ic_t.data(), ctx->h_ic_t.size() * 4, cudaMemcpyHostToDevice));
@@ -1004,6 +1041,7 @@ int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes
     if (n <= 0 || !coords) return fail(ctx, PNX_ERR_ARG, "residual_loss: empty point set");
     CK(cudaSetDevice(ctx->device));
     if (!ctx->rows_dirty && n == ctx->n_int && ctx->d_coords) {
+        ctx->int_on_device = false;
         // same row layout (e.g. resampled points, trainer.cpp:421-434): copy the
         // caller's axis-major buffer straight into the interior segment on device
         const int64_t off = ctx->int_off_prev;
@@ -1017,11 +1055,62 @@ int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes
     }
     ctx->h_int.assign(coords, coords + n * n_axes);
     ctx->h_int_stale = false;
+    ctx->int_on_device = false;
     ctx->n_int = n;
     ctx->rows_dirty = true;
     if ((int64_t)n * ctx->Kres > ctx->resid_cap) {
         if (int r = dalloc(ctx, &ctx->d_resid, (size_t)n * ctx->Kres)) return r;
         ctx->resid_cap = (int64_t)n * ctx->Kres;
+    }
+    return PNX_OK;
+}
+
+int pnx_sample_points(pnx_ctx* ctx, int32_t mode, const double* bounds, const int64_t* dims, int64_t n_total,
+                      uint64_t seed, int64_t row_lo, int64_t row_hi) {
+    if (!ctx || !bounds) return PNX_ERR_ARG;
+    const int d = ctx->in_dim;
+    SampleArgs a{};
+    a.mode = mode;
+    a.d = d;
+    a.seed = seed;
+    int64_t total = 1;
+    for (int k = 0; k < d; ++k) {
+        a.lo[k] = bounds[2 * k];
+        a.hi[k] = bounds[2 * k + 1];
+        if (mode != SAMPLE_LHS) {
+            if (!dims || dims[k] <= 0) return fail(ctx, PNX_ERR_ARG, "sample_uniform: zero points on an axis");
+            a.dims[k] = dims[k];
+            total *= dims[k];
+        }
+    }
+    if (mode == SAMPLE_LHS) {
+        if (n_total <= 0) return fail(ctx, PNX_ERR_ARG, "sample_lhs: n must be positive");
+        total = n_total;
+    } else if (mode != SAMPLE_UNIFORM && mode != SAMPLE_LHS_PER_AXIS) {
+        return fail(ctx, PNX_ERR_ARG, "pnx_sample_points: unknown design");
+    }
+    if (row_lo < 0 || row_hi > total || row_hi <= row_lo)
+        return fail(ctx, PNX_ERR_ARG, "residual_loss: empty point set");
+    a.n = total;
+    a.row0 = row_lo;
+    a.nrows = row_hi - row_lo;
+    CK(cudaSetDevice(ctx->device));
+    ctx->samp = a;
+    if (!ctx->rows_dirty && a.nrows == ctx->n_int && ctx->d_coords) {
+        // same row layout (resampling, trainer.cpp:421-434): generate in place
+        if (int r = wait_last_step(ctx)) return r;
+        ctx->int_on_device = true;
+        ctx->h_int_stale = false;
+        return generate_interior(ctx);
+    }
+    ctx->h_int.clear();
+    ctx->h_int_stale = false;
+    ctx->int_on_device = true;
+    ctx->n_int = a.nrows;
+    ctx->rows_dirty = true;  // laid out (and generated) by the next step
+    if (a.nrows * ctx->Kres > ctx->resid_cap) {
+        if (int r = dalloc(ctx, &ctx->d_resid, (size_t)a.nrows * ctx->Kres)) return r;
+        ctx->resid_cap = a.nrows * ctx->Kres;
     }
     return PNX_OK;
 }
@@ -1045,7 +1134,12 @@ int pnx_set_causality(pnx_ctx* ctx, int32_t segments, double epsilon, double t_l
     if (int r = dalloc(ctx, &ctx->d_seg_w, (size_t)segments)) return r;
     CK(cudaMemset(ctx->d_caus_cnt, 0, (size_t)segments * 8));
     if (ctx->n_int > 0) {  // counts of the current shard
-        if (ctx->h_int_stale || ctx->rows_dirty) {
+        if (ctx->int_on_device) {
+            if (!ctx->rows_dirty && ctx->d_coords) {
+                if (int r = wait_last_step(ctx)) return r;
+                if (int r = generate_interior(ctx)) return r;  // regenerates and recounts
+            }
+        } else if (ctx->h_int_stale || ctx->rows_dirty) {
             ctx->rows_dirty = true;  // recounted by the next upload
         } else {
             if (int r = causality_counts(ctx, ctx->h_int.data() + (size_t)(ctx->in_dim - 1) * ctx->n_int, ctx->n_int))
@@ -1312,6 +1406,18 @@ int pnx_adam_step_device(pnx_ctx* ctx, float* d_params, const float* d_grad, flo
 int pnx_capture_residuals(pnx_ctx* ctx, int on) {
     if (!ctx) return PNX_ERR_ARG;
     ctx->capture_resid = on != 0;
+    return PNX_OK;
+}
+
+int pnx_copy_points(pnx_ctx* ctx, double* out) {
+    if (!ctx || !out) return PNX_ERR_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->rows_dirty)
+        if (int r = upload_rows(ctx)) return r;
+    if (int r = wait_last_step(ctx)) return r;
+    for (int a = 0; a < ctx->in_dim; ++a)
+        CK(cudaMemcpy(out + a * ctx->n_int, ctx->d_coords + a * ctx->ld + ctx->int_off_prev, (size_t)ctx->n_int * 8,
+                      cudaMemcpyDeviceToHost));
     return PNX_OK;
 }
 

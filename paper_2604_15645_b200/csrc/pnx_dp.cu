@@ -67,7 +67,7 @@ struct Dev {
 }  // namespace
 
 struct pnx_dp {
-    int R = 0, D = 0;
+    int R = 0, D = 0, in_dim = 0;
     int64_t P = 0;
     std::vector<pnx_ctx*> ctx;  // per rank
     std::vector<int> rank_dev;  // rank -> index into dev
@@ -235,6 +235,7 @@ int pnx_dp_create(const pnx_model_desc* m, const pnx_problem_desc* p, const int*
     *out = nullptr;
     auto* dp = new pnx_dp();
     dp->R = n_ranks;
+    dp->in_dim = m->in_dim;
     std::string msg;
     // devices in first-use order; ranks of one device are its local replicas
     for (int r = 0; r < n_ranks; ++r) {
@@ -354,6 +355,27 @@ int pnx_dp_set_points(pnx_dp* dp, const double* coords, int64_t n, int32_t n_axe
             std::memcpy(shard.data() + (size_t)(a * (hi - lo)), coords + a * n + lo, (size_t)(hi - lo) * 8);
         pnx_ctx* c = dp->ctx[(size_t)r];
         if (int rc = pnx_set_points(c, shard.data(), hi - lo, n_axes)) return dp_fail(dp, rc, pnx_last_error(c));
+    }
+    return PNX_OK;
+}
+
+int pnx_dp_sample_points(pnx_dp* dp, int32_t mode, const double* bounds, const int64_t* dims, int64_t n_total,
+                         uint64_t seed) {
+    if (!dp || !bounds) return PNX_ERR_ARG;
+    int64_t total = n_total;
+    if (mode != 1) {  // grid designs: the product of the axis counts
+        if (!dims) return PNX_ERR_ARG;
+        total = 1;
+        for (int a = 0; a < dp->in_dim; ++a) total *= dims[a] > 0 ? dims[a] : 0;
+    }
+    const int64_t base = total / dp->R;
+    if (base == 0) return dp_fail(dp, PNX_ERR_ARG, "data parallel: fewer interior points than workers");
+    invalidate_graphs(dp);
+    for (int r = 0; r < dp->R; ++r) {  // shard_interior: contiguous, last takes the remainder
+        const int64_t lo = r * base, hi = r + 1 == dp->R ? total : lo + base;
+        pnx_ctx* c = dp->ctx[(size_t)r];
+        if (int rc = pnx_sample_points(c, mode, bounds, dims, n_total, seed, lo, hi))
+            return dp_fail(dp, rc, pnx_last_error(c));
     }
     return PNX_OK;
 }

@@ -157,6 +157,17 @@ def _axis_major(pts: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(pts, dtype=np.float64).T)
 
 
+SAMPLE_DESIGNS = {"uniform": 0, "lhs": 1, "lhs_per_axis": 2}
+
+
+def _design_args(design, bounds, dims, n):
+    b = (C.c_double * (2 * len(bounds)))(*[float(v) for lo_hi in bounds for v in lo_hi])
+    if design == "lhs":
+        return b, None, int(n)
+    d = (C.c_int64 * len(dims))(*[int(x) for x in dims])
+    return b, d, int(np.prod([int(x) for x in dims]))
+
+
 def _descs(spec: ModelSpec, res: ResidualSpec, bc: str, rff_B):
     """pnx_model_desc / pnx_problem_desc of a ModelSpec / ResidualSpec (+ the
     arrays they point to, which must outlive the call)."""
@@ -237,6 +248,16 @@ class Worker:
         self._chk(self.lib.pnx_set_points(self.ctx, a.ctypes.data_as(C.POINTER(C.c_double)),
                                           a.shape[1], a.shape[0]))
         self.n_interior = int(a.shape[1])
+
+    def sample_points(self, design: str, bounds, dims=None, n: int = 0, seed: int = 0, rows=None):
+        """Interior generated on the device (pnx_sample_points): design "uniform"
+        (sample_uniform), "lhs" (sample_lhs, n points) or "lhs_per_axis"
+        (sample_lhs_per_axis); rows = (lo, hi) of the global design (default all)."""
+        b, d, total = _design_args(design, bounds, dims, n)
+        lo, hi = rows if rows is not None else (0, total)
+        self._chk(self.lib.pnx_sample_points(self.ctx, SAMPLE_DESIGNS[design], b, d, int(n), int(seed), int(lo),
+                                             int(hi)))
+        self.n_interior = int(hi - lo)
 
     def set_ic(self, pts: np.ndarray, targets: np.ndarray):
         a = _axis_major(pts)
@@ -332,6 +353,12 @@ class Worker:
 
     def capture_residuals(self, on: bool = True):
         self._chk(self.lib.pnx_capture_residuals(self.ctx, 1 if on else 0))
+
+    def points(self) -> np.ndarray:
+        """The interior points of the next step as [N, d] (device designs included)."""
+        out = np.empty((self.spec.in_dim, self.n_interior), dtype=np.float64)
+        self._chk(self.lib.pnx_copy_points(self.ctx, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out.T.copy()
 
     def residuals(self, n_interior: int) -> np.ndarray:
         out = np.empty((self.res.field_count(), n_interior), dtype=np.float64)
@@ -464,6 +491,11 @@ class DataParallelGroup:
         a = _axis_major(pts)
         self._chk(self.lib.pnx_dp_set_points(self.h, a.ctypes.data_as(C.POINTER(C.c_double)), a.shape[1],
                                              a.shape[0]))
+
+    def sample_points(self, design: str, bounds, dims=None, n: int = 0, seed: int = 0):
+        """The global interior as a device design (pnx_dp_sample_points), sharded over the ranks."""
+        b, d, _ = _design_args(design, bounds, dims, n)
+        self._chk(self.lib.pnx_dp_sample_points(self.h, SAMPLE_DESIGNS[design], b, d, int(n), int(seed)))
 
     def set_ic(self, pts, targets):
         a, t = _axis_major(pts), _axis_major(targets)

@@ -47,6 +47,8 @@ def _args():
     ap.add_argument("--graph", action="store_true",
                     help="time CUDA-graph replays (class timings then come from a separate eager pass)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--host-points", action="store_true",
+                    help="build the C5 interior on the host and upload it (default: device design)")
     return ap.parse_args()
 
 
@@ -144,49 +146,81 @@ class ClockSampler:
 REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "pinnlab_ref_driver")
 
 
-def cpu_reference(wl, seconds: float):
-    """Time the reference train() (trainer.cpp:332; cfg.workers threads,
-    trainer.cpp:445-457) on a bounded sample of the same model/PDE. Falls
-    back to the FP64 numpy restatement (kind "port") when oracle/_ref is
-    absent. Returns the cpu_baseline dict."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _ref_train(wl, n_target, threads, epochs):
+    """Run the compiled reference train() (trainer.cpp:332; cfg.workers std::threads,
+    trainer.cpp:445-457) for `epochs` epochs on a uniform grid of about
+    n_target points; returns (points, dims, per-epoch wall seconds)."""
+    d = len(wl.domain)
+    per = max(2, int(round(n_target ** (1.0 / d))))
+    dims = [per] * d
+    n = int(np.prod(dims))
+    job = {"mode": "train", "model": _spec_json(wl.spec), "seed": 0,
+           "pde": {"id": wl.res.id, "advection_c": wl.res.advection_c, "epsilon": wl.res.epsilon,
+                   "mu": wl.res.mu},
+           "domain": [list(b) for b in wl.domain], "initial": wl.initial, "bc": wl.bc,
+           "collocation": {"mode": "uniform", "dims": dims, "n_ic": wl.n_ic, "n_bc": wl.n_bc},
+           "workers": threads, "train": {"epochs": epochs, "lr": 1e-3, "balancing": False}}
+    with tempfile.TemporaryDirectory() as td:
+        job["out"] = td
+        jp = os.path.join(td, "job.json")
+        json.dump(job, open(jp, "w"))
+        r = subprocess.run([REF_DRIVER, jp], capture_output=True, text=True, timeout=900)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr[-500:])
+        m = json.load(open(os.path.join(td, "meta.json")))["metrics"]
+    wall = [row[8] for row in m]
+    return n, dims, np.diff([0.0] + wall)
+
+
+def cpu_reference(wl, seconds: float, steps: int = 10, warmup: int = 2):
+    """The reference CPU implementation of the path (oracle/_ref: the unmodified
+    reference compiled against the Eigen-API shim) on this host's cores: `warmup`
+    untimed + `steps` timed epochs of train() on a bounded sample of the workload
+    (a uniform grid of the same model / PDE; the reference keeps every N x H
+    float64 graph node, ~0.9 MB per point at 6x256, so the full 1M-point set does
+    not fit). points/s = sample points / median timed epoch: the reference's cost
+    is linear in the points, so the rate extrapolates to the full workload.
+    Also one thread (W_cpu = 1) on a proportionally smaller sample."""
+    if not os.path.exists(REF_DRIVER) or wl.res.id == "ns_steady":
+        raise RuntimeError("oracle/_ref not built (or the workload is outside the reference)")
     cores = os.cpu_count() or 1
-    if os.path.exists(REF_DRIVER) and wl.res.id != "ns_steady":
-        # reference RSS is ~0.9 MB per point for 6x256 (graph keeps every node)
-        per_point_mb = 0.9 * (wl.spec.hidden_dim / 256.0) * (wl.spec.depth / 6.0) * (wl.streams() / 4.0)
-        try:
-            mem_mb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_AVPHYS_PAGES") / 2**20
-        except Exception:
-            mem_mb = 32768
-        threads = min(cores, 64)
-        # size so one epoch takes ~seconds/4 at ~250 pts/s/thread (6x256) scaled by model cost
-        rate = 250.0 * (7_901_184 / wl.flops_per_point()) * threads
-        n = int(min(rate * seconds / 4.0, 0.4 * mem_mb / max(per_point_mb, 1e-3), 65536))
-        n = max(n, threads * 16)
-        d = len(wl.domain)
-        per = max(2, int(round(n ** (1.0 / d))))
-        dims = [per] * d
-        n = int(np.prod(dims))
-        job = {"mode": "train", "model": _spec_json(wl.spec), "seed": 0,
-               "pde": {"id": wl.res.id, "advection_c": wl.res.advection_c, "epsilon": wl.res.epsilon,
-                       "mu": wl.res.mu},
-               "domain": [list(b) for b in wl.domain], "initial": wl.initial, "bc": wl.bc,
-               "collocation": {"mode": "uniform", "dims": dims, "n_ic": wl.n_ic, "n_bc": wl.n_bc},
-               "workers": threads, "train": {"epochs": 4, "lr": 1e-3}}
-        with tempfile.TemporaryDirectory() as td:
-            job["out"] = td
-            jp = os.path.join(td, "job.json")
-            json.dump(job, open(jp, "w"))
-            r = subprocess.run([REF_DRIVER, jp], capture_output=True, text=True, timeout=600)
-            if r.returncode == 0:
-                m = json.load(open(os.path.join(td, "meta.json")))["metrics"]
-                wall = [row[8] for row in m]
-                steps = np.diff([0.0] + wall)[1:]  # drop the first (allocation warm-up) epoch
-                t = float(np.median(steps))
-                return {"value": n / t, "unit": UNIT, "cores": threads, "kind": "reference",
-                        "sample": f"reference train() (oracle/_ref, Eigen-API shim) {n} pts {dims}, "
-                                  f"{threads} worker threads, median of {len(steps)} epochs after 1 warm-up",
-                        "t_step_s": t}
-    raise RuntimeError("oracle/_ref not built")
+    threads = min(cores, 64)
+    per_point_mb = 0.9 * (wl.spec.hidden_dim / 256.0) * (wl.spec.depth / 6.0) * (wl.streams() / 4.0)
+    try:
+        mem_mb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_AVPHYS_PAGES") / 2**20
+    except Exception:
+        mem_mb = 32768
+    # ~`seconds` of timed CPU work in total: one epoch ~ seconds/steps at ~250
+    # points/s per thread (6x256), scaled by the model's cost
+    rate = 250.0 * (7_901_184 / wl.flops_per_point())
+    n = int(min(rate * threads * seconds / max(steps, 1), 0.4 * mem_mb / max(per_point_mb, 1e-3), 65536))
+    n = max(n, threads * 16)
+    npts, dims, dt = _ref_train(wl, n, threads, warmup + steps)
+    timed = dt[warmup:]
+    t = float(np.median(timed))
+    n1 = max(64, n // threads)
+    npts1, dims1, dt1 = _ref_train(wl, n1, 1, 3)  # W_cpu = 1: one warm-up + two timed epochs
+    t1 = float(np.median(dt1[1:]))
+    return {"value": npts / t, "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(), "host_cores": cores,
+            "sample": (f"reference train() (oracle/_ref, Eigen-API shim), {threads} worker threads, "
+                       f"uniform grid {dims} = {npts} points of the workload's model/PDE; "
+                       f"{warmup} warm-up + {steps} timed epochs, median epoch {t:.3f} s; points/s = "
+                       f"sample points / epoch time (the reference's cost is linear in the points, so "
+                       f"this extrapolates to the full set)"),
+            "epochs_timed": steps, "epochs_warmup": warmup, "sample_points": npts, "t_step_s": t,
+            "w_cpu_1": {"value": npts1 / t1, "unit": UNIT, "cores": 1, "sample_points": npts1,
+                        "epochs_timed": 2, "epochs_warmup": 1, "t_step_s": t1}}
 
 
 def _spec_json(s):
@@ -233,9 +267,9 @@ def cpu_port(wl, seconds: float):
             "sample": f"numpy FP64 restatement, {npts} pts {dims}, mean of {k} steps", "t_step_s": t}
 
 
-def cpu_baseline(wl, seconds):
+def cpu_baseline(wl, seconds, steps=10, warmup=2):
     try:
-        return cpu_reference(wl, seconds)
+        return cpu_reference(wl, seconds, steps, warmup)
     except Exception:
         return cpu_port(wl, seconds)
 
@@ -250,14 +284,22 @@ def run_reference(args):
         return 0
     wl, dims, name = workload(args, args.gpus)
     t0 = time.time()
-    cb = cpu_baseline(wl, args.cpu_seconds)
+    # the reference arm times `--steps` epochs after `--warmup` (at least 2) untimed ones
+    warm = max(2, args.warmup)
+    cb = cpu_baseline(wl, args.cpu_seconds, args.steps, warm)
     v = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * cb["t_step_s"],
+            "steps": cb.get("epochs_timed", args.steps), "warmup": cb.get("epochs_warmup", warm),
+            "ms_per_step": 1e3 * cb["t_step_s"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": name, "model": "reference pinnlab CPU",
-                                            "parallelism": f"{cb['cores']} std::threads"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "data": "synthetic (uniform collocation grid; reference Model init)",
+            "config": {"workload": name, "model": "reference pinnlab CPU train()",
+                       "parallelism": f"{cb['cores']} std::threads (trainer.cpp:445-457)",
+                       "sample_points": cb.get("sample_points"),
+                       "points_per_s": "sample points / median epoch (cost linear in points: extrapolated)"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample") if k in cb},
+            "cpu_model": cb.get("cpu_model"), "host_cores": cb.get("host_cores"),
+            "w_cpu_1": cb.get("w_cpu_1"),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.time() - t0}
     print(json.dumps(line), flush=True)
@@ -288,13 +330,25 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     wl, dims, name = workload(args, world)
-    col = configs.collocation(wl, dims)
-    n_total = len(col["interior"])
+    # C5: the interior is the uniform grid generated on the device, each rank its
+    # shard (pnx_sample_points; bit-exact sample_uniform) -- no host point set
+    dev_pts = args.config == "c5" and not args.host_points
+    col = configs.collocation(wl, dims, with_interior=not dev_pts)
+    n_total = int(np.prod(dims))
     lo, hi = pk.shard_interior(n_total, world)[rank]
-    shard = col["interior"][lo:hi]
     flat, rffB = pk.init_params(wl.spec, seed=0)
-    worker = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, shard, col["ic_points"], col["ic_targets"],
-                            col["bc_a"], col["bc_b"], col["bc_targets"], device=local, engine=args.engine)
+    if dev_pts:
+        worker = pk.Worker(wl.spec, wl.res, wl.bc, rffB, device=local, engine=args.engine)
+        worker.sample_points("uniform", wl.domain, dims, rows=(lo, hi))
+        if col["ic_points"] is not None and len(col["ic_points"]):
+            worker.set_ic(col["ic_points"], col["ic_targets"])
+        if wl.bc != "hard":
+            worker.set_bc(col["bc_a"], col["bc_b"], col["bc_targets"])
+        shard = None
+    else:
+        shard = col["interior"][lo:hi]
+        worker = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, shard, col["ic_points"], col["ic_targets"],
+                                col["bc_a"], col["bc_b"], col["bc_targets"], device=local, engine=args.engine)
     P = worker.n_params
     from paper_2604_15645_b200.dist import DataParallelTrainer
     # one CUDA graph per step on a single GPU (the multi-GPU step keeps NCCL eager)
@@ -370,6 +424,8 @@ def main():
 
         def pp(a):
             return a.ctypes.data_as(dptr)
+        if shard is None:  # the host copy of this rank's grid rows, for the host->device leg
+            shard = configs.grid(wl.domain, dims)[lo:hi]
         shard_pinned = torch.from_numpy(np.ascontiguousarray(shard.T)).pin_memory()  # axis-major [d, N]
         g_dev = torch.zeros(P, dtype=torch.float64, device=dev)
         h2d = d2h = 0
@@ -480,7 +536,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak"
             if args.config == "c5" else "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (uniform collocation grid, numpy Xavier init; no dataset)",
+            "data": ("synthetic (uniform collocation grid generated on the device, numpy Xavier init; no dataset)"
+                     if dev_pts else "synthetic (uniform collocation grid, numpy Xavier init; no dataset)"),
             "config": {"workload": name, "pde": wl.res.id, "model": f"tanh MLP {wl.spec.depth}x{H}",
                        "points_total": n_total, "points_per_gpu": rows, "streams": S,
                        "params": P, "engine": args.engine,
@@ -497,7 +554,8 @@ def main():
             "e2e": e2e,
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = {k: v for k, v in cpu_baseline(wl, args.cpu_seconds).items() if k != "t_step_s"}
+            cb = cpu_baseline(wl, args.cpu_seconds, 5, 2)
+            line["cpu_baseline"] = {k: v for k, v in cb.items() if k not in ("t_step_s",)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -75,13 +75,14 @@ def grid(bounds, dims) -> np.ndarray:
     return np.stack([m.ravel() for m in mesh], axis=1)
 
 
-def collocation(w: Workload, dims: Optional[List[int]] = None):
+def collocation(w: Workload, dims: Optional[List[int]] = None, with_interior: bool = True):
     """build_collocation, uniform mode (trainer.cpp:47-128). Returns dict of
-    interior, ic_points, ic_targets, bc_a, bc_b, bc_targets (numpy float64)."""
+    interior, ic_points, ic_targets, bc_a, bc_b, bc_targets (numpy float64);
+    with_interior=False leaves the interior to a device design (pnx_sample_points)."""
     dims = dims or w.dims
     b = w.domain
     F = w.spec.out_dim
-    out = {"interior": grid(b, dims)}
+    out = {"interior": grid(b, dims) if with_interior else None}
     if w.res.id == "ns_steady":
         # steady: no time axis and no IC; 4-wall Dirichlet with lid u = 1 (PAPER.md:790-796)
         n = w.n_bc

@@ -268,6 +268,7 @@ int upload_rows(pnx_ctx* ctx) {
     const int d = ctx->in_dim;
     if (ctx->h_int_stale && ctx->d_coords && !ctx->int_on_device) {  // pull the fast-path interior back before re-layout
         const int64_t off = ctx->int_off_prev;
+        ctx->h_int.resize((size_t)(ctx->n_int * d));  // empty when the previous interior was a device design
         for (int a = 0; a < d; ++a)
             CK(cudaMemcpy(ctx->h_int.data() + a * ctx->n_int, ctx->d_coords + a * ctx->ld + off,
                           (size_t)ctx->n_int * 8, cudaMemcpyDeviceToHost));

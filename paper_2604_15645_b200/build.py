@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpnx.so")
-SOURCES = ["pnx_capi.cu", "pnx_dp.cu", "launch_simt.cu", "launch_tc.cu"]
+SOURCES = ["pnx_capi.cu", "pnx_dp.cu", "launch_simt.cu", "launch_tc.cu", "launch_small.cu"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -40,9 +40,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if p.wait() != 0:
             raise RuntimeError(f"nvcc failed on {src}")
     tmp = LIB + ".tmp"
-    # NCCL (the data-parallel group's all-reduce): the image's libnccl.so.2; in a
-    # process that already loaded torch's bundled libnccl.so.2 the loader reuses it
-    subprocess.run([nvcc, *GENCODE, "-shared", "-o", tmp, *objs, "-lcudart", "-lnccl"], check=True)
+    # NCCL (the data-parallel group's all-reduce): link the libnccl.so.2 that torch
+    # bundles (nvidia-nccl wheel, newer than the image's /usr/lib 2.27) when it is
+    # there, with an rpath to it: whichever of libpnx / torch loads first, the one
+    # libnccl.so.2 in the process satisfies both (libtorch_cuda needs 2.28 symbols)
+    nccl = []
+    try:
+        import nvidia.nccl as _n  # noqa: F401  (namespace package)
+        d = os.path.join(list(_n.__path__)[0], "lib")
+        if os.path.exists(os.path.join(d, "libnccl.so.2")):
+            nccl = ["-L" + d, "-Xlinker", "-rpath=" + d]
+    except Exception:
+        pass
+    subprocess.run([nvcc, *GENCODE, "-shared", "-o", tmp, *objs, "-lcudart", *nccl, "-l:libnccl.so.2"], check=True)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

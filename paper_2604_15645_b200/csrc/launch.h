@@ -58,4 +58,8 @@ void launch_layer0_wgrad(int L, const InputArgs& a, const float* Zb0, int H, dou
 int launch_tc_layer(int L, int mode, int pro, const TcGemmArgs& g, cudaStream_t st);
 int launch_tc2_fwd(int L, int pro, const TcGemmArgs& g, cudaStream_t st);
 int launch_tc2_wgrad(int L, int pro, const TcWgradArgs& w, int ntiles, int wrows, cudaStream_t st);
+struct SmallArgs;
+int launch_small(int pde, int HP, const SmallArgs& a, int grid, cudaStream_t st);
+void launch_small_finalize(const double* slot, int nblk, int64_t P, const double* loss_part, const double* inv_n,
+                           float* grad, double* losses, cudaStream_t st);
 }  // namespace pnx

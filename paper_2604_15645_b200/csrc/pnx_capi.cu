@@ -24,6 +24,7 @@
 #include "tc_gemm.cuh"
 #include "launch.h"
 #include "sampling.cuh"
+#include "small_net.cuh"
 
 using namespace pnx;
 
@@ -126,6 +127,7 @@ struct pnx_ctx {
     // pass 1 when the whole step is one chunk: same parameters, same points
     bool reuse_fwd = false;
     TcWorkspace tc{};
+    double* d_sn_slot = nullptr;  // single-kernel narrow step: [grid][P] FP64 gradient slots
     // kernel-class timing with CUDA events on the launching stream (bench roofline)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -367,12 +369,89 @@ int upload_rows(pnx_ctx* ctx) {
     return PNX_OK;
 }
 
+// The whole step as one kernel (small_net.cuh) for narrow tanh networks: H <= 64,
+// embedding only (no RFF, RWF or trainable period), first- or second-order
+// 1-D / Maxwell layouts, hard or Dirichlet BC, no causality / Poynting, and the
+// weights plus a 32-row tile of every layer's jets fit in shared memory.
+// Taken by the default engine (AUTO); PNX_ENGINE_FFMA keeps the multi-kernel
+// FFMA path (both are tested), PNX_SMALL_OFF=1 disables it (A/B).
+int small_hp(const pnx_ctx* c) {
+    static const bool off = getenv("PNX_SMALL_OFF") != nullptr;
+    if (off || c->engine != PNX_ENGINE_AUTO) return 0;
+    if (c->act != ACT_TANH || c->H > 64 || c->rff_w > 0 || c->rwf || c->train_period || c->E > SN_MAXK0) return 0;
+    if (c->pde == PNX_PDE_NS_STEADY || c->bc == PNX_BC_SOFT_PERIODIC || c->caus_M > 0 || c->n_poy > 0) return 0;
+    const int HP = c->H <= 32 ? 32 : 64;
+    if (sn_smem_floats(HP, c->S, c->depth) * 4 > 227 * 1024) return 0;
+    return HP;
+}
+
+int run_small(pnx_ctx* ctx, int HP, const float* d_params, const double lam[3], float* d_grad, double* d_losses,
+              cudaStream_t st) {
+    const int64_t T = ctx->ld;
+    const int grid = (int)std::min<int64_t>(ctx->nsm, (T + SN_TR - 1) / SN_TR);
+    if (!ctx->d_sn_slot)
+        if (int r = dalloc(ctx, &ctx->d_sn_slot, (size_t)ctx->nsm * ctx->P)) return r;
+    SmallArgs a{};
+    a.ia.coords = ctx->d_coords;
+    a.ia.ld = T;
+    a.ia.in_dim = ctx->in_dim;
+    for (int k = 0; k < kMaxAxes; ++k) {
+        a.ia.periodic[k] = ctx->periodic[k];
+        a.ia.period[k] = ctx->period[k];
+        a.ia.period_off[k] = ctx->period_off[k];
+    }
+    a.ia.params = d_params;
+    a.ia.E = ctx->E;
+    a.ia.K0 = ctx->K0;
+    a.params = d_params;
+    a.tab = ctx->tab;
+    a.D = ctx->depth;
+    a.H = ctx->H;
+    a.K0 = ctx->K0;
+    a.T = T;
+    a.bca0 = 0;
+    a.bca1 = ctx->n_bca;
+    a.ic0 = ctx->n_bca + ctx->n_bcb;
+    a.ic1 = a.ic0 + ctx->n_ic;
+    a.int0 = a.ic1 + ctx->n_poy;
+    a.int1 = a.int0 + ctx->n_int;
+    a.bc_mode = ctx->bc;
+    a.ic_t = ctx->d_ic_t;
+    a.bc_t = ctx->d_bc_t;
+    a.w_pde = (float)(2.0 * lam[0] / (double)ctx->n_int);
+    a.w_ic = ctx->n_ic ? (float)(2.0 * lam[1] / (double)ctx->n_ic) : 0.0f;
+    a.w_bc = ctx->n_bca ? (float)(2.0 * lam[2] / (double)ctx->n_bca) : 0.0f;
+    a.pc = ctx->pc;
+    a.bad = ctx->d_bad;
+    a.resid_out = ctx->capture_resid ? ctx->d_resid : nullptr;
+    a.slot = ctx->d_sn_slot;
+    a.loss_part = ctx->d_loss_part;
+    a.P = ctx->P;
+    prof_begin(ctx, PC_FWD, st);
+    if (launch_small(ctx->pde, HP, a, grid, st)) return fail(ctx, PNX_ERR_CUDA, "small-network step launch");
+    prof_end(ctx, st);
+    CKL();
+    prof_begin(ctx, PC_FINAL, st);
+    launch_small_finalize(ctx->d_sn_slot, grid, ctx->P, ctx->d_loss_part, ctx->d_losses + 3, d_grad,
+                          d_losses ? d_losses : ctx->d_losses, st);
+    prof_end(ctx, st);
+    CKL();
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusNone) {
+        CK(cudaEventRecord(ctx->ev_done, st));
+        ctx->ev_pending = true;
+    }
+    return PNX_OK;
+}
+
 int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_grad, double* d_losses,
              cudaStream_t st) {
     if (ctx->n_int <= 0) return fail(ctx, PNX_ERR_STATE, "pnx_step: no interior points (call pnx_set_points)");
     if (ctx->rows_dirty)
         if (int r = upload_rows(ctx)) return r;
     ctx->launches = 0;
+    if (const int HP = small_hp(ctx)) return run_small(ctx, HP, d_params, lam, d_grad, d_losses, st);
     const LayerTab& t = ctx->tab;
     const int Lw = t.n;  // linear layers
     const int S = ctx->S;
@@ -1021,6 +1100,7 @@ void pnx_destroy(pnx_ctx* ctx) {
     cudaFree(ctx->d_bad);
     cudaFree(ctx->d_amax);
     cudaFree(ctx->d_resid);
+    cudaFree(ctx->d_sn_slot);
     tc_workspace_free(ctx->tc);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);

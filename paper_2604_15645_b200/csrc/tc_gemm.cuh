@@ -1422,6 +1422,11 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
             const uint32_t tempty0 = PAIR ? tc::mapa(tc::smem_u32(&tempty), 0) : tc::smem_u32(&tempty);
             float us = 1.0f;
             if constexpr (F16) us = ldexpf(1.0f, -sA) * ldexpf(1.0f, -sB);
+            // the slot is re-read by every segment drain: keep it in L2 while the
+            // operand stream passes through (ncu: without the hint the slot lines were
+            // evicted and written back, ~1 GB of DRAM writes + 1 GB of reads per launch)
+            uint64_t keep;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
             for (int seg = 0; seg < nseg; ++seg) {
                 const bool last = seg + 1 == nseg;
                 tc::mbar_wait(&tfull, (uint32_t)(seg & 1));
@@ -1445,8 +1450,9 @@ __global__ void __launch_bounds__(TCW_THREADS, 1) k_tc2_wgrad(const __grid_const
                         }
 #pragma unroll
                         for (int j = 0; j < 16; ++j)
-                            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + c + 4 * j),
-                                         "f"(a[4 * j]), "f"(a[4 * j + 1]), "f"(a[4 * j + 2]), "f"(a[4 * j + 3])
+                            asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(
+                                             dst + c + 4 * j),
+                                         "f"(a[4 * j]), "f"(a[4 * j + 1]), "f"(a[4 * j + 2]), "f"(a[4 * j + 3]), "l"(keep)
                                          : "memory");
                     }
                 }

@@ -102,3 +102,15 @@ def test_flops_per_point_match_survey():
     assert configs.get_config("c2").flops_per_point() == 1_476_864
     assert configs.get_config("c3").flops_per_point() == 1_985_280
     assert configs.get_config("c4").flops_per_point() == 7_901_184
+
+
+def test_library_loads_before_torch():
+    """libpnx links the libnccl.so.2 torch bundles (rpath): loading it first must
+    not shadow torch's NCCL (libtorch_cuda needs symbols the image's older
+    /usr/lib libnccl lacks)."""
+    import subprocess
+    import sys
+    from paper_2604_15645_b200 import _lib
+    code = f"import ctypes; ctypes.CDLL({_lib.LIB_PATH!r}); import torch; print(torch.__version__)"
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]

@@ -400,6 +400,11 @@ def main():
         prof = worker.profile_read()
         worker.profile(False)
     worker.check()
+    replicas_equal = None
+    if world > 1:  # replica consistency after the synchronized steps (param_hash / on_sync, trainer.cpp:540-544)
+        from paper_2604_15645_b200.dist import replica_hashes
+        hs = replica_hashes(wl.spec, trainer.params_host(), world)
+        replicas_equal = len(set(hs)) == 1
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -550,6 +555,7 @@ def main():
             "roofline": roof,
             "kernel_ms_per_step": {k: prof[k][0] / args.steps for k in prof},
             "gpu_launches": int(launches_per_step * args.steps),
+            "replica_hashes_equal": replicas_equal,
             "clocks": clocks,
             "e2e": e2e,
         }

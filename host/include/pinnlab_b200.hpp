@@ -91,7 +91,9 @@ private:
     Tensor rff_B_;
 };
 
-enum class PdeId { advection, allen_cahn, burgers, maxwell_te, ns_steady };
+// + extensions: ns_steady and maxwell_te_eh, the TE system with
+// fields (Ex, Ey, Hz) (the reference's maxwell_te is the (Ez, Hx, Hy) system)
+enum class PdeId { advection, allen_cahn, burgers, maxwell_te, ns_steady, maxwell_te_eh };
 
 struct ResidualSpec {
     PdeId id = PdeId::advection;
@@ -100,8 +102,10 @@ struct ResidualSpec {
     double mu = 1.0;
     double reynolds = 100.0;  // ns_steady extension
 
-    std::size_t field_count() const { return (id == PdeId::maxwell_te || id == PdeId::ns_steady) ? 3 : 1; }
-    std::size_t coord_count() const { return id == PdeId::maxwell_te ? 3 : 2; }
+    std::size_t field_count() const {
+        return (id == PdeId::maxwell_te || id == PdeId::maxwell_te_eh || id == PdeId::ns_steady) ? 3 : 1;
+    }
+    std::size_t coord_count() const { return (id == PdeId::maxwell_te || id == PdeId::maxwell_te_eh) ? 3 : 2; }
 };
 
 struct Points {

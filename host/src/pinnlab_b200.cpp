@@ -281,6 +281,7 @@ int pde_code(PdeId id) {
         case PdeId::burgers: return PNX_PDE_BURGERS;
         case PdeId::maxwell_te: return PNX_PDE_MAXWELL_TE;
         case PdeId::ns_steady: return PNX_PDE_NS_STEADY;
+        case PdeId::maxwell_te_eh: return PNX_PDE_MAXWELL_TE_EH;
     }
     return -1;
 }

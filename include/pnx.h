@@ -38,9 +38,12 @@ typedef struct pnx_ctx pnx_ctx;
 
 /* Activation (model.hpp:12). */
 enum { PNX_ACT_TANH = 0, PNX_ACT_SINE = 1, PNX_ACT_SWISH = 2 };
-/* PdeId (losses.hpp:14) + the ns_steady extension. */
+/* PdeId (losses.hpp:14) + the ns_steady extension and the
+ * TE-mode naming of Maxwell with fields (Ex, Ey, Hz) (BASELINE configs[3];
+ * eps Ex_t = Hz_y, eps Ey_t = -Hz_x, mu Hz_t = Ex_y - Ey_x; extension: the
+ * reference's maxwell_te is the (Ez, Hx, Hy) system, losses.cpp:57-72). */
 enum { PNX_PDE_ADVECTION = 0, PNX_PDE_ALLEN_CAHN = 1, PNX_PDE_BURGERS = 2,
-       PNX_PDE_MAXWELL_TE = 3, PNX_PDE_NS_STEADY = 4 };
+       PNX_PDE_MAXWELL_TE = 3, PNX_PDE_NS_STEADY = 4, PNX_PDE_MAXWELL_TE_EH = 5 };
 /* TrainingProblem::Bc (trainer.hpp:23-27). */
 enum { PNX_BC_HARD = 0, PNX_BC_SOFT_PERIODIC = 1, PNX_BC_DIRICHLET_ZERO = 2 };
 /* Contraction engine for the hidden layers. */

@@ -35,7 +35,8 @@ class Workload:
         return int(np.prod(self.dims))
 
     def streams(self) -> int:
-        return {"advection": 3, "burgers": 3, "allen_cahn": 4, "maxwell_te": 4, "ns_steady": 5}[self.res.id]
+        return {"advection": 3, "burgers": 3, "allen_cahn": 4, "maxwell_te": 4, "maxwell_te_eh": 4,
+                "ns_steady": 5}[self.res.id]
 
     def sum_in_out(self) -> int:
         s = self.spec

@@ -115,6 +115,7 @@ void launch_head(int pde, int act, const HeadArgs& h, int grid, cudaStream_t st)
         case PDE_ALLEN_CAHN: launch_head_p<PDE_ALLEN_CAHN>(act, h, grid, st); break;
         case PDE_BURGERS: launch_head_p<PDE_BURGERS>(act, h, grid, st); break;
         case PDE_MAXWELL: launch_head_p<PDE_MAXWELL>(act, h, grid, st); break;
+        case PDE_MAXWELL_EH: launch_head_p<PDE_MAXWELL_EH>(act, h, grid, st); break;
         case PDE_NS: launch_head_p<PDE_NS>(act, h, grid, st); break;
     }
 }

@@ -27,6 +27,7 @@ int launch_small(int pde, int HP, const SmallArgs& a, int grid, cudaStream_t st)
         case PDE_ALLEN_CAHN: return launch_small_p<PDE_ALLEN_CAHN>(HP, a, grid, st);
         case PDE_BURGERS: return launch_small_p<PDE_BURGERS>(HP, a, grid, st);
         case PDE_MAXWELL: return launch_small_p<PDE_MAXWELL>(HP, a, grid, st);
+        case PDE_MAXWELL_EH: return launch_small_p<PDE_MAXWELL_EH>(HP, a, grid, st);
     }
     return -1;
 }

@@ -9,6 +9,7 @@
 // replicated IC/BC sets (trainer.cpp:225-232) ride in the first chunk and carry
 // value-only seeds, interior rows carry residual seeds (losses.cpp:77-95).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool (nsys) is attached
 
 #include <algorithm>
 #include <climits>
@@ -170,8 +171,13 @@ int dalloc(pnx_ctx* ctx, T** p, size_t n) {
 
 enum ProfClass { PC_INPUT = 0, PC_FWD = 1, PC_HEAD = 2, PC_BWD = 3, PC_WGRAD = 4, PC_FINAL = 5 };
 
-// Record an event before a kernel of class `cls`; returns the pair index.
+const char* const kClassName[8] = {"pnx input", "pnx forward GEMM", "pnx head", "pnx reverse GEMM",
+                                   "pnx weight gradient", "pnx finalize", "pnx", "pnx"};
+
+// NVTX range per kernel class (nsys timelines), and with profiling on a CUDA
+// event pair on the launching stream around the launch.
 void prof_begin(pnx_ctx* c, int cls, cudaStream_t st) {
+    nvtxRangePushA(kClassName[cls & 7]);
     if (!c->prof) return;
     if (c->ev_used + 2 > c->ev_pool.size()) {
         for (int i = 0; i < 64; ++i) {
@@ -184,6 +190,7 @@ void prof_begin(pnx_ctx* c, int cls, cudaStream_t st) {
     c->ev_cls.push_back(cls);
 }
 void prof_end(pnx_ctx* c, cudaStream_t st) {
+    nvtxRangePop();
     if (!c->prof) return;
     cudaEventRecord(c->ev_pool[c->ev_used + 1], st);
     c->ev_used += 2;
@@ -205,7 +212,8 @@ int pde_layout(int pde) {
         case PNX_PDE_ADVECTION:
         case PNX_PDE_BURGERS: return LAY_XT;
         case PNX_PDE_ALLEN_CAHN: return LAY_AC;
-        case PNX_PDE_MAXWELL_TE: return LAY_MX;
+        case PNX_PDE_MAXWELL_TE:
+        case PNX_PDE_MAXWELL_TE_EH: return LAY_MX;
         case PNX_PDE_NS_STEADY: return LAY_NS;
     }
     return -1;
@@ -925,8 +933,9 @@ int pnx_create(const pnx_model_desc* m, const pnx_problem_desc* p, int device, p
         g_create_error = "unknown pde";
         return PNX_ERR_ARG;
     }
-    const int fields = (p->pde == PNX_PDE_MAXWELL_TE || p->pde == PNX_PDE_NS_STEADY) ? 3 : 1;
-    const int coords = (p->pde == PNX_PDE_MAXWELL_TE) ? 3 : 2;
+    const bool mx = p->pde == PNX_PDE_MAXWELL_TE || p->pde == PNX_PDE_MAXWELL_TE_EH;
+    const int fields = (mx || p->pde == PNX_PDE_NS_STEADY) ? 3 : 1;
+    const int coords = mx ? 3 : 2;
     if (m->out_dim != fields) {  // losses.cpp:31-32
         g_create_error = "residual: model field count does not match the equation";
         return PNX_ERR_ARG;

@@ -19,6 +19,7 @@
 //     captured once in a CUDA graph and replayed while the loss weights stay.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <condition_variable>
@@ -169,7 +170,10 @@ int enqueue_step(pnx_dp* dp, Dev& v, const double lam[3], bool update, std::stri
             DPCK(cudaGetLastError());
         }
     }
-    DPNC(ncclAllReduce(v.d_pack, v.d_pack, (size_t)n, ncclFloat, ncclSum, v.comm, v.stream));
+    nvtxRangePushA("pnx_dp ncclAllReduce [grad | losses]");
+    const ncclResult_t nr = ncclAllReduce(v.d_pack, v.d_pack, (size_t)n, ncclFloat, ncclSum, v.comm, v.stream);
+    nvtxRangePop();
+    DPNC(nr);
     if (update) {
         pnx_ctx* c = dp->ctx[(size_t)v.ranks[0]];
         if (int r = ctx_call(c, pnx_adam_step_device_state(c, v.d_params, v.d_pack, v.d_m, v.d_v, dp->P, v.d_state,

@@ -8,7 +8,7 @@
 
 namespace pnx {
 
-enum Pde : int { PDE_ADVECTION = 0, PDE_ALLEN_CAHN = 1, PDE_BURGERS = 2, PDE_MAXWELL = 3, PDE_NS = 4 };
+enum Pde : int { PDE_ADVECTION = 0, PDE_ALLEN_CAHN = 1, PDE_BURGERS = 2, PDE_MAXWELL = 3, PDE_NS = 4, PDE_MAXWELL_EH = 5 };
 
 template <int P> struct PdeTraits;
 template <> struct PdeTraits<PDE_ADVECTION> { static constexpr int L = LAY_XT, F = 1, K = 1; };
@@ -16,6 +16,7 @@ template <> struct PdeTraits<PDE_ALLEN_CAHN> { static constexpr int L = LAY_AC, 
 template <> struct PdeTraits<PDE_BURGERS> { static constexpr int L = LAY_XT, F = 1, K = 1; };
 template <> struct PdeTraits<PDE_MAXWELL> { static constexpr int L = LAY_MX, F = 3, K = 3; };
 template <> struct PdeTraits<PDE_NS> { static constexpr int L = LAY_NS, F = 3, K = 3; };
+template <> struct PdeTraits<PDE_MAXWELL_EH> { static constexpr int L = LAY_MX, F = 3, K = 3; };
 
 struct PdeConst {
     float c, eps, mu, inv_re;
@@ -37,6 +38,10 @@ __device__ __forceinline__ void residual(const float* o, float* r, const PdeCons
         r[0] = pc.eps * O(3, 0) - (O(1, 2) - O(2, 1));
         r[1] = pc.mu * O(3, 1) + O(2, 0);
         r[2] = pc.mu * O(3, 2) - O(1, 0);
+    } else if constexpr (P == PDE_MAXWELL_EH) {  // TE (Ex, Ey, Hz): SURVEY 8(a) a10c, extension
+        r[0] = pc.eps * O(3, 0) - O(2, 2);              // eps Ex_t = Hz_y
+        r[1] = pc.eps * O(3, 1) + O(1, 2);              // eps Ey_t = -Hz_x
+        r[2] = pc.mu * O(3, 2) - (O(2, 0) - O(1, 1));   // mu Hz_t = Ex_y - Ey_x
     } else {  // NS steady: fields u,v,p; streams u, _x, _y, _xx, _yy
         const float u = O(0, 0), v = O(0, 1);
         r[0] = O(1, 0) + O(2, 1);
@@ -76,6 +81,14 @@ __device__ __forceinline__ void residual_seed(const float* o, const float* rb, f
         OB(2, 0) += rb[1];
         OB(3, 2) += pc.mu * rb[2];
         OB(1, 0) += -rb[2];
+    } else if constexpr (P == PDE_MAXWELL_EH) {
+        OB(3, 0) += pc.eps * rb[0];
+        OB(2, 2) += -rb[0];
+        OB(3, 1) += pc.eps * rb[1];
+        OB(1, 2) += rb[1];
+        OB(3, 2) += pc.mu * rb[2];
+        OB(2, 0) += -rb[2];
+        OB(1, 1) += rb[2];
     } else {
         const float u = O(0, 0), v = O(0, 1);
         const float ux = O(1, 0), uy = O(2, 0), vx = O(1, 1), vy = O(2, 1);

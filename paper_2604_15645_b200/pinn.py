@@ -26,7 +26,7 @@ import numpy as np
 from . import _lib
 
 ACTIVATIONS = {"tanh": 0, "sine": 1, "swish": 2}
-PDES = {"advection": 0, "allen_cahn": 1, "burgers": 2, "maxwell_te": 3, "ns_steady": 4}
+PDES = {"advection": 0, "allen_cahn": 1, "burgers": 2, "maxwell_te": 3, "ns_steady": 4, "maxwell_te_eh": 5}
 BCS = {"hard": 0, "soft_periodic": 1, "dirichlet_zero": 2}
 ENGINES = {"auto": 0, "ffma": 1, "tc3xtf32": 2, "tc3xf16": 3}
 
@@ -97,10 +97,10 @@ class ResidualSpec:
     reynolds: float = 100.0
 
     def field_count(self) -> int:
-        return 3 if self.id in ("maxwell_te", "ns_steady") else 1
+        return 3 if self.id in ("maxwell_te", "maxwell_te_eh", "ns_steady") else 1
 
     def coord_count(self) -> int:
-        return 3 if self.id == "maxwell_te" else 2
+        return 3 if self.id in ("maxwell_te", "maxwell_te_eh") else 2
 
 
 def param_layout(spec: ModelSpec) -> List[Tuple[str, Tuple[int, ...]]]:

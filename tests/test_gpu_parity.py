@@ -499,3 +499,28 @@ def test_device_adam_rejects_nonfinite_gradient():
     torch.cuda.synchronize()
     w.check()
     assert not torch.equal(p, p0)
+
+
+@pytest.mark.parametrize("hidden,engine", [(256, "auto"), (256, "ffma"), (16, "auto"), (16, "ffma")])
+def test_maxwell_te_eh_alias_vs_oracle(hidden, engine):
+    """The TE system with fields (Ex, Ey, Hz) (BASELINE configs[3]; extension: the
+    reference's maxwell_te is (Ez, Hx, Hy)) on the width-256 tensor-core path, the
+    single-kernel narrow step and the FFMA kernels, vs the FP64 oracle."""
+    import dataclasses
+    pk = _pkg()
+    from paper_2604_15645_b200 import configs
+    wl = configs.get_config("c4")
+    spec = dataclasses.replace(wl.spec, hidden_dim=hidden, depth=6 if hidden == 256 else 3)
+    res = pk.ResidualSpec("maxwell_te_eh", epsilon=1.0, mu=1.0)
+    col = configs.collocation(wl, [12, 10, 8])
+    col["ic_targets"] = col["ic_targets"][:, ::-1].copy()  # the pulse on Hz
+    flat, rffB = pk.init_params(spec, seed=2)
+    ospec = gi.spec_from_json(_spec_json(spec))
+    ores = po.ResidualSpec("maxwell_te_eh", 0.0, 1.0, 1.0, 100.0)
+    ocol = po.Collocation(col["interior"], col["ic_points"], col["ic_targets"], col["bc_a"], col["bc_b"],
+                          col["bc_targets"])
+    ref, outs = po.data_parallel_gradient(ospec, flat, rffB, ores, ocol, wl.bc, 1)
+    grad, losses = pk.data_parallel_gradient(spec, res, wl.bc, flat, rffB, workers=1, engine=engine, **col)
+    assert rel_l2(grad, ref) <= _tol(engine), rel_l2(grad, ref)
+    for k in ("pde", "ic"):
+        assert abs(losses[0][k] - outs[0][k]) <= LOSS_RTOL * abs(outs[0][k]) + 1e-12

@@ -185,3 +185,32 @@ def test_spec_known_answers():
     p = np.array([1.0, -2.0])
     a.step(p, np.array([0.3, -5.0]))
     np.testing.assert_allclose(p, [0.9, -1.9], atol=1e-7)
+
+
+def test_maxwell_te_eh_extension():
+    """maxwell_te_eh (fields Ex, Ey, Hz; BASELINE configs[3] naming) is not in the
+    reference (its maxwell_te is the (Ez, Hx, Hy) system, losses.cpp:57-72):
+    pinned by a TE plane wave (Hz = Ey = cos(kx - wt), Ex = 0, w = k, eps = mu = 1:
+    residuals vanish) and by central FD of the loss gradient on the oracle."""
+    streams = po.pde_streams("maxwell_te_eh")
+    x = np.linspace(-1, 1, 7)
+    t = np.linspace(0, 1, 7)
+    k = 2.3
+    ph = k * x - k * t
+    O = np.zeros((len(streams), x.size, 3))
+    c, s = np.cos(ph), np.sin(ph)
+    # value, d/dx, d/dy, d/dt of Ex = 0, Ey = cos, Hz = cos
+    for f in (1, 2):
+        O[0, :, f] = c
+        O[streams.index((1, 0)), :, f] = -k * s
+        O[streams.index((1, 2)), :, f] = k * s
+    r = po.residuals(po.ResidualSpec("maxwell_te_eh"), O, streams)
+    assert np.max(np.abs(r)) <= 1e-14
+    spec = po.ModelSpec(in_dim=3, hidden_dim=8, depth=2, out_dim=3, activation="tanh")
+    res = po.ResidualSpec("maxwell_te_eh", epsilon=1.3, mu=0.7)
+    flat, _ = po.init_params(spec, 5)
+    pts = po.sample_uniform([(-1, 1), (-1, 1), (0, 1)], [3, 3, 3])
+    ic = po.sample_uniform([(-1, 1), (-1, 1), (0, 0)], [3, 3, 1])
+    col = po.Collocation(pts, ic, np.stack([np.zeros(9), np.zeros(9), np.exp(-25 * (ic[:, 0] ** 2 + ic[:, 1] ** 2))], 1))
+    rng = np.random.default_rng(1)
+    _fd_check(spec, res, flat, None, col, "hard", rng.choice(flat.size, 12, replace=False))

@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
             for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int c = 0; c < NC; ++c) z[s][c] = 0.0f;
+#pragma unroll 2
             for (int k = 0; k < Kd; k += 4) {
                 float4 av[S];
 #pragma unroll
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
             for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int c = 0; c < NC; ++c) hb[s][c] = 0.0f;
+#pragma unroll 2
             for (int n = 0; n < HP; n += 4) {
                 float4 zv[S];
 #pragma unroll
@@ -409,8 +411,9 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
 static __global__ void k_small_finalize(const double* __restrict__ slot, int nblk, int64_t P,
                                         const double* __restrict__ loss_part, const double* __restrict__ inv_n,
                                         float* __restrict__ grad, double* __restrict__ losses) {
+    // one thread per entry (coalesced across the warp), four interleaved partial
+    // sums over the slots (loads in flight), combined in fixed order
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-        // four interleaved partial sums (loads in flight), combined in fixed order
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int b = 0;
         for (; b + 4 <= nblk; b += 4) {

@@ -1516,6 +1516,10 @@ template <int L, bool PAIR, bool F16 = false>
 __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constant__ TcGemmArgs g) {
     using Cfg = Tc5BwdCfg<L, PAIR>;
     constexpr int NST = Cfg::NST, NF = Cfg::NF;
+    constexpr int NEW = 8;              // epilogue warps (9-16)
+    constexpr int ECOLS = 4 * NF / NEW;  // columns per epilogue warp and pass: 128
+    constexpr int NCH = ECOLS / 16;      // 16-column chunks per warp and pass
+    constexpr int NBUF = 2;              // staging buffers per warp
     static_assert(L == LAY_XT || L == LAY_MX, "first-order layouts only");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
@@ -1546,8 +1550,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
             tc::mbar_init(&empty[i], 1);
         }
         tc::mbar_init(&tfull, 1);
-        tc::mbar_init(&tempty, 8);                 // this CTA's epilogue -> its producers
-        tc::mbar_init(&tempty_all, PAIR ? 16 : 8);  // both epilogues -> the MMA issuer
+        tc::mbar_init(&tempty, NEW);                      // this CTA's epilogue -> its producers
+        tc::mbar_init(&tempty_all, PAIR ? 2 * NEW : NEW);  // both epilogues -> the MMA issuer
         tc::fence_barrier_init();
     }
     if (warp == 8) {
@@ -1563,6 +1567,162 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
     const uint32_t sP = sbase + NST * Cfg::STAGE;
     const uint32_t full0 = PAIR ? tc::mapa(tc::smem_u32(&full[0]), 0) : tc::smem_u32(&full[0]);
     const uint32_t tempty_all0 = PAIR ? tc::mapa(tc::smem_u32(&tempty_all), 0) : tc::smem_u32(&tempty_all);
+
+    // ---------------- epilogue: 16-column chunks, Z_in staged by cp.async ----------------
+    // staging tiles: row r, 16 B chunk c at r*64 + ((c ^ ((r>>1)&3)) << 4): conflict-free
+    // for both the row-per-lane reads and the 8-rows-per-instruction copies.
+    // Double-buffered: the tiles of chunk i+1 are in flight while chunk i computes.
+    // Epilogue warp e = warp - 9: TMEM lane quarter warp % 4, column block cq.
+    // (Measured and dropped: the producer warps joining the epilogue -- 16 warps,
+    // 64 columns each, single-buffered staging -- bwd 16.9 -> 17.7 ms/step.)
+    auto run_epilogue = [&](int pass) {
+        const int ew = warp - 9;
+        const int q = warp & 3, cq = (warp - 9) >> 2;
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t stg0 = sbase + (uint32_t)ew * NBUF * 3 * Cfg::TILE;
+        const uint32_t pbuf = sP + (uint32_t)ew * ECOLS * 32 * 4;  // [col/4][lane][4]: one 16 B access per 4 columns
+        const int64_t rbase = (int64_t)(r0 + q * 32) * NF;
+        const int lr = lane >> 2, lcv = lane & 3;
+        auto soff = [](int r, int c) { return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4)); };
+        const int s0 = Cfg::sa(pass), s1 = Cfg::sb(pass);
+        // Z_in tiles this pass needs: t (stream 0) and z of its first-order streams
+        const int zA = s0 > 0 ? s0 : -1, zB = s1 > 0 ? s1 : -1;
+        auto issue = [&](int cch) {
+            const uint32_t stg = stg0 + (uint32_t)(cch % NBUF) * 3 * Cfg::TILE;
+            const int c0 = cq * ECOLS + cch * 16;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int sz = u == 0 ? 0 : (u == 1 ? zA : zB);
+                if (sz < 0) continue;
+                const float* src = g.Zlow + sz * RN + rbase + c0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    cp_async16(stg + u * Cfg::TILE + soff(8 * k + lr, lcv), src + (int64_t)(8 * k + lr) * NF + lcv * 4);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        float usa = 1.0f, usb = 1.0f;  // 3xFP16 unscale of the two accumulators
+        if constexpr (F16) {
+            const float usw = ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w));
+            usa = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s0]));
+            if (s1 >= 0) usb = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s1]));
+        }
+        float mxa = 0.0f, mxb = 0.0f;
+        tc::mbar_wait(&tfull, (uint32_t)pass);
+        tc::tc_fence_after();
+        TC_T0();
+        issue(0);
+#pragma unroll 1
+        for (int cch = 0; cch < NCH; ++cch) {
+            const int c0 = cq * ECOLS + cch * 16;
+            const uint32_t stg = stg0 + (uint32_t)(cch % NBUF) * 3 * Cfg::TILE;
+            float ha[16], hb[16];
+            tc::tmem_ld16(tl + (uint32_t)c0, ha);
+            if (s1 >= 0) tc::tmem_ld16(tl + (uint32_t)(NF + c0), hb);
+            if (NBUF == 2 && cch + 1 < NCH) {
+                issue(cch + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncwarp();
+            tc::tmem_ld_wait();
+            if constexpr (F16) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    ha[j] *= usa;
+                    hb[j] *= usb;
+                }
+            }
+#pragma unroll
+            for (int j4 = 0; j4 < 16; j4 += 4) {
+                const uint32_t ro = soff(lane, j4 >> 2);
+                const float4 t4 = lds128(stg + ro);
+                const float tt[4] = {t4.x, t4.y, t4.z, t4.w};
+                float za[4] = {0.f, 0.f, 0.f, 0.f}, zb2[4] = {0.f, 0.f, 0.f, 0.f}, pp[4] = {0.f, 0.f, 0.f, 0.f};
+                if (zA >= 0) {
+                    const float4 v = lds128(stg + Cfg::TILE + ro);
+                    za[0] = v.x; za[1] = v.y; za[2] = v.z; za[3] = v.w;
+                }
+                if (zB >= 0) {
+                    const float4 v = lds128(stg + 2 * Cfg::TILE + ro);
+                    zb2[0] = v.x; zb2[1] = v.y; zb2[2] = v.z; zb2[3] = v.w;
+                }
+                if (pass == 1) {
+                    const float4 v = lds128(pbuf + (uint32_t)((((cch * 16 + j4) >> 2) * 32 + lane) * 16));
+                    pp[0] = v.x; pp[1] = v.y; pp[2] = v.z; pp[3] = v.w;
+                }
+                float oa[4], ob[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = j4 + e;
+                    const float t = tt[e];
+                    const float d = 1.0f - t * t;
+                    if (pass == 0) {
+                        // streams 1, 2: zb_s = d hb_s ; P = z_1 hb_1 + z_2 hb_2
+                        oa[e] = d * ha[j];
+                        ob[e] = d * hb[j];
+                        float P = 0.0f;
+                        P += za[e] * ha[j];
+                        P += zb2[e] * hb[j];
+                        pp[e] = P;
+                    } else if (Streams<L>::S == 4) {
+                        // streams 3, 0: zb_3 = d hb_3 ; zb_0 = d (hb_0 - 2 t (P + z_3 hb_3))
+                        oa[e] = d * ha[j];
+                        float P = pp[e];
+                        P += za[e] * ha[j];
+                        float tbar = hb[j];
+                        tbar += -2.0f * t * P;
+                        ob[e] = d * tbar;
+                    } else {
+                        // XT stream 0: zb_0 = d (hb_0 - 2 t P)
+                        float tbar = ha[j];
+                        tbar += -2.0f * t * pp[e];
+                        oa[e] = d * tbar;
+                        ob[e] = 0.0f;
+                    }
+                }
+                if (pass == 0)
+                    sts128(pbuf + (uint32_t)((((cch * 16 + j4) >> 2) * 32 + lane) * 16),
+                           make_float4(pp[0], pp[1], pp[2], pp[3]));
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    mxa = fmaxf(mxa, fabsf(oa[e]));
+                    mxb = fmaxf(mxb, fabsf(ob[e]));
+                }
+                // outputs in place: stream s0 -> its z tile (the t tile when s0 = 0),
+                // stream s1 -> its z tile (the t tile when s1 = 0)
+                sts128(stg + (zA >= 0 ? Cfg::TILE : 0) + ro, make_float4(oa[0], oa[1], oa[2], oa[3]));
+                if (s1 >= 0) sts128(stg + (zB >= 0 ? 2 * Cfg::TILE : 0) + ro, make_float4(ob[0], ob[1], ob[2], ob[3]));
+            }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int so = u == 0 ? s0 : s1;
+                if (so < 0) continue;
+                const int slot = u == 0 ? (zA >= 0 ? 1 : 0) : (zB >= 0 ? 2 : 0);
+                float* dst = g.out + so * RN + rbase + c0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float4 v = lds128(stg + slot * Cfg::TILE + soff(8 * k + lr, lcv));
+                    *reinterpret_cast<float4*>(dst + (int64_t)(8 * k + lr) * NF + lcv * 4) = v;
+                }
+            }
+            __syncwarp();
+        }
+        if (g.amax_out) {
+            tc::warp_amax(g.amax_out + s0, __float_as_uint(mxa));
+            if (s1 >= 0) tc::warp_amax(g.amax_out + s1, __float_as_uint(mxb));
+        }
+        if (warp == 9 && lane == 0) TC_ACC(3);
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            tc::mbar_arrive(&tempty);
+            if constexpr (PAIR) tc::mbar_arrive_cluster(tempty_all0);
+            else tc::mbar_arrive(&tempty_all);
+        }
+    };
 
     if (F16 && warp < 8) {
         // ---------------- producers (3xFP16): one 16-wide k-step per stage ----------------
@@ -1744,157 +1904,8 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
         }
         __syncwarp();
     } else {
-        // ---------------- epilogue: 16-column chunks, Z_in staged by cp.async ----------------
-        // staging tiles: row r, 16 B chunk c at r*64 + ((c ^ ((r>>1)&3)) << 4): conflict-free
-        // for both the row-per-lane reads and the 8-rows-per-instruction copies.
-        // Double-buffered: the tiles of chunk i+1 are in flight while chunk i computes.
-        const int q = warp & 3, half = (warp - 9) >> 2, ew = warp - 9;
-        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-        const uint32_t stg0 = sbase + (uint32_t)ew * 2 * 3 * Cfg::TILE;
-        const uint32_t pbuf = sP + (uint32_t)ew * 128 * 32 * 4;     // [col/4][lane][4]: one 16 B access per 4 columns
-        const int64_t rbase = (int64_t)(r0 + q * 32) * NF;
-        const int lr = lane >> 2, lcv = lane & 3;
-        auto soff = [](int r, int c) { return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4)); };
-        for (int pass = 0; pass < 2; ++pass) {
-            const int s0 = Cfg::sa(pass), s1 = Cfg::sb(pass);
-            // Z_in tiles this pass needs: t (stream 0) and z of its first-order streams
-            const int zA = s0 > 0 ? s0 : -1, zB = s1 > 0 ? s1 : -1;
-            auto issue = [&](int cch) {
-                const uint32_t stg = stg0 + (uint32_t)(cch & 1) * 3 * Cfg::TILE;
-                const int c0 = half * 128 + cch * 16;
-#pragma unroll
-                for (int u = 0; u < 3; ++u) {
-                    const int sz = u == 0 ? 0 : (u == 1 ? zA : zB);
-                    if (sz < 0) continue;
-                    const float* src = g.Zlow + sz * RN + rbase + c0;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        cp_async16(stg + u * Cfg::TILE + soff(8 * k + lr, lcv), src + (int64_t)(8 * k + lr) * NF + lcv * 4);
-                }
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            };
-            float usa = 1.0f, usb = 1.0f;  // 3xFP16 unscale of the two accumulators
-            if constexpr (F16) {
-                const float usw = ldexpf(1.0f, -tc::f16_exp_bits(*g.amax_w));
-                usa = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s0]));
-                if (s1 >= 0) usb = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s1]));
-            }
-            float mxa = 0.0f, mxb = 0.0f;
-            tc::mbar_wait(&tfull, (uint32_t)pass);
-            tc::tc_fence_after();
-            TC_T0();
-            issue(0);
 #pragma unroll 1
-            for (int cch = 0; cch < 8; ++cch) {
-                const int c0 = half * 128 + cch * 16;
-                const uint32_t stg = stg0 + (uint32_t)(cch & 1) * 3 * Cfg::TILE;
-                float ha[16], hb[16];
-                tc::tmem_ld16(tl + (uint32_t)c0, ha);
-                if (s1 >= 0) tc::tmem_ld16(tl + (uint32_t)(NF + c0), hb);
-                if (cch + 1 < 8) {
-                    issue(cch + 1);
-                    asm volatile("cp.async.wait_group 1;" ::: "memory");
-                } else {
-                    asm volatile("cp.async.wait_group 0;" ::: "memory");
-                }
-                __syncwarp();
-                tc::tmem_ld_wait();
-                if constexpr (F16) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        ha[j] *= usa;
-                        hb[j] *= usb;
-                    }
-                }
-#pragma unroll
-                for (int j4 = 0; j4 < 16; j4 += 4) {
-                    const uint32_t ro = soff(lane, j4 >> 2);
-                    const float4 t4 = lds128(stg + ro);
-                    const float tt[4] = {t4.x, t4.y, t4.z, t4.w};
-                    float za[4] = {0.f, 0.f, 0.f, 0.f}, zb2[4] = {0.f, 0.f, 0.f, 0.f}, pp[4] = {0.f, 0.f, 0.f, 0.f};
-                    if (zA >= 0) {
-                        const float4 v = lds128(stg + Cfg::TILE + ro);
-                        za[0] = v.x; za[1] = v.y; za[2] = v.z; za[3] = v.w;
-                    }
-                    if (zB >= 0) {
-                        const float4 v = lds128(stg + 2 * Cfg::TILE + ro);
-                        zb2[0] = v.x; zb2[1] = v.y; zb2[2] = v.z; zb2[3] = v.w;
-                    }
-                    if (pass == 1) {
-                        const float4 v = lds128(pbuf + (uint32_t)((((cch * 16 + j4) >> 2) * 32 + lane) * 16));
-                        pp[0] = v.x; pp[1] = v.y; pp[2] = v.z; pp[3] = v.w;
-                    }
-                    float oa[4], ob[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int j = j4 + e;
-                        const float t = tt[e];
-                        const float d = 1.0f - t * t;
-                        if (pass == 0) {
-                            // streams 1, 2: zb_s = d hb_s ; P = z_1 hb_1 + z_2 hb_2
-                            oa[e] = d * ha[j];
-                            ob[e] = d * hb[j];
-                            float P = 0.0f;
-                            P += za[e] * ha[j];
-                            P += zb2[e] * hb[j];
-                            pp[e] = P;
-                        } else if (Streams<L>::S == 4) {
-                            // streams 3, 0: zb_3 = d hb_3 ; zb_0 = d (hb_0 - 2 t (P + z_3 hb_3))
-                            oa[e] = d * ha[j];
-                            float P = pp[e];
-                            P += za[e] * ha[j];
-                            float tbar = hb[j];
-                            tbar += -2.0f * t * P;
-                            ob[e] = d * tbar;
-                        } else {
-                            // XT stream 0: zb_0 = d (hb_0 - 2 t P)
-                            float tbar = ha[j];
-                            tbar += -2.0f * t * pp[e];
-                            oa[e] = d * tbar;
-                            ob[e] = 0.0f;
-                        }
-                    }
-                    if (pass == 0)
-                        sts128(pbuf + (uint32_t)((((cch * 16 + j4) >> 2) * 32 + lane) * 16),
-                               make_float4(pp[0], pp[1], pp[2], pp[3]));
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        mxa = fmaxf(mxa, fabsf(oa[e]));
-                        mxb = fmaxf(mxb, fabsf(ob[e]));
-                    }
-                    // outputs in place: stream s0 -> its z tile (the t tile when s0 = 0),
-                    // stream s1 -> its z tile (the t tile when s1 = 0)
-                    sts128(stg + (zA >= 0 ? Cfg::TILE : 0) + ro, make_float4(oa[0], oa[1], oa[2], oa[3]));
-                    if (s1 >= 0) sts128(stg + (zB >= 0 ? 2 * Cfg::TILE : 0) + ro, make_float4(ob[0], ob[1], ob[2], ob[3]));
-                }
-                __syncwarp();
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int so = u == 0 ? s0 : s1;
-                    if (so < 0) continue;
-                    const int slot = u == 0 ? (zA >= 0 ? 1 : 0) : (zB >= 0 ? 2 : 0);
-                    float* dst = g.out + so * RN + rbase + c0;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const float4 v = lds128(stg + slot * Cfg::TILE + soff(8 * k + lr, lcv));
-                        *reinterpret_cast<float4*>(dst + (int64_t)(8 * k + lr) * NF + lcv * 4) = v;
-                    }
-                }
-                __syncwarp();
-            }
-            if (g.amax_out) {
-                tc::warp_amax(g.amax_out + s0, __float_as_uint(mxa));
-                if (s1 >= 0) tc::warp_amax(g.amax_out + s1, __float_as_uint(mxb));
-            }
-            if (warp == 9 && lane == 0) TC_ACC(3);
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                tc::mbar_arrive(&tempty);
-                if constexpr (PAIR) tc::mbar_arrive_cluster(tempty_all0);
-                else tc::mbar_arrive(&tempty_all);
-            }
-        }
+        for (int pass = 0; pass < 2; ++pass) run_epilogue(pass);
     }
     tc::tc_fence_before();
     if constexpr (PAIR) tc::cluster_sync();

@@ -47,6 +47,8 @@ def _args():
     ap.add_argument("--graph", action="store_true",
                     help="time CUDA-graph replays (class timings then come from a separate eager pass)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collective backend for N>1 (gloo: a host-side check of the N>1 path, e.g. 2 ranks on 1 GPU)")
     ap.add_argument("--host-points", action="store_true",
                     help="build the C5 interior on the host and upload it (default: device design)")
     return ap.parse_args()
@@ -324,10 +326,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         world = max(world, 1)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    gpu = local % max(1, torch.cuda.device_count())  # one rank per GPU (gloo check: ranks may share one)
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     wl, dims, name = workload(args, world)
     # C5: the interior is the uniform grid generated on the device, each rank its
@@ -338,7 +344,7 @@ def main():
     lo, hi = pk.shard_interior(n_total, world)[rank]
     flat, rffB = pk.init_params(wl.spec, seed=0)
     if dev_pts:
-        worker = pk.Worker(wl.spec, wl.res, wl.bc, rffB, device=local, engine=args.engine)
+        worker = pk.Worker(wl.spec, wl.res, wl.bc, rffB, device=gpu, engine=args.engine)
         worker.sample_points("uniform", wl.domain, dims, rows=(lo, hi))
         if col["ic_points"] is not None and len(col["ic_points"]):
             worker.set_ic(col["ic_points"], col["ic_targets"])
@@ -348,7 +354,7 @@ def main():
     else:
         shard = col["interior"][lo:hi]
         worker = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, shard, col["ic_points"], col["ic_targets"],
-                                col["bc_a"], col["bc_b"], col["bc_targets"], device=local, engine=args.engine)
+                                col["bc_a"], col["bc_b"], col["bc_targets"], device=gpu, engine=args.engine)
     P = worker.n_params
     from paper_2604_15645_b200.dist import DataParallelTrainer
     # one CUDA graph per step on a single GPU (the multi-GPU step keeps NCCL eager)
@@ -378,7 +384,7 @@ def main():
 
     # ---- timed region (device-resident inputs); class times by CUDA events on the
     # launching stream inside it unless graph replays are timed ----
-    clk = ClockSampler(local)
+    clk = ClockSampler(gpu)
     if not trainer.graph:
         worker.profile(True)
     clk.start()

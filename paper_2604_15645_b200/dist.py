@@ -65,7 +65,9 @@ def replica_hashes(spec, params, world: int, group=None) -> Sequence[int]:
         return [h]
     import torch
     import torch.distributed as dist
-    t = torch.tensor([h & 0x7FFFFFFFFFFFFFFF, h >> 63], dtype=torch.int64)
+    # NCCL gathers device tensors; gloo (CPU tests) host tensors
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else None
+    t = torch.tensor([h & 0x7FFFFFFFFFFFFFFF, h >> 63], dtype=torch.int64, device=dev)
     out = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(out, t, group=group)
     return [int(o[0]) | (int(o[1]) << 63) for o in out]

@@ -153,3 +153,17 @@ def test_dist_trainer_two_processes_match_reference():
             assert abs(row[k] - m[ep, 1 + k]) <= TRAJ_RTOL * abs(m[ep, 1 + k]) + 1e-9, (ep, k, row[k])
     for hs in res["hashes"]:
         assert len(hs) == 2 and hs[0] == hs[1]
+
+
+def test_bench_two_ranks_gloo():
+    """bench.py's N>1 path (torchrun, contiguous shards, packed all-reduce, max
+    over ranks, replica hashes) with two ranks on the one GPU over gloo."""
+    root = gi.ROOT
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29562", os.path.join(root, "bench.py"), "--gpus", "2",
+           "--dist-backend", "gloo", "--steps", "3", "--warmup", "3", "--config", "c1", "--no-e2e"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().split("\n")[-1])
+    assert line["n_gpus"] == 2 and line["replica_hashes_equal"] is True
+    assert line["value"] > 0 and line["config"]["parallelism"] == "dp2"

@@ -44,8 +44,10 @@ def _args():
     ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc3xtf32", "tc3xf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--graph", action="store_true",
-                    help="time CUDA-graph replays (class timings then come from a separate eager pass)")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="time CUDA-graph replays of the whole step (default; class timings then come from a "
+                         "separate eager pass)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="time eager launches")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for N>1 (gloo: a host-side check of the N>1 path, e.g. 2 ranks on 1 GPU)")
@@ -492,11 +494,14 @@ def main():
         nh = wl.spec.depth - 1                               # hidden->hidden layers
         sum_fwd = K0 * H + H * H * nh                        # layers 0..depth-1 (head excluded)
         sum_bwd = H * H * nh                                 # reverse GEMMs of layers 1..depth-1
+        # the single-kernel narrow step (width <= 64) does all of it: F_pt flops per
+        # row, and its only HBM traffic is the coordinates (8 B per axis)
         flops_cls = {"fwd_gemm": 2.0 * S * rows * sum_fwd, "bwd_gemm": 2.0 * S * rows * sum_bwd,
-                     "wgrad_gemm": 2.0 * S * rows * sum_fwd}
+                     "wgrad_gemm": 2.0 * S * rows * sum_fwd, "fused_step": float(wl.flops_per_point()) * rows}
         bytes_cls = {"fwd_gemm": rows * (S * 4.0 * 2 * H * nh + S * 4.0 * H + 8.0 * d_in),
                      "bwd_gemm": rows * S * 4.0 * 3 * H * nh,
-                     "wgrad_gemm": rows * (S * 4.0 * 2 * H * nh + S * 4.0 * H)}
+                     "wgrad_gemm": rows * (S * 4.0 * 2 * H * nh + S * 4.0 * H),
+                     "fused_step": rows * 8.0 * d_in}
         dom = max(flops_cls, key=lambda k: prof[k][0])
         tms, nl = prof[dom]
         t_s = (tms / 1e3) / args.steps                       # class seconds per step
@@ -540,7 +545,8 @@ def main():
         key = f"{name}:{dom}"
         roof["traffic"] = traffic_db.get(key)
         # one hidden-layer launch's algorithmic bytes, the comparand of `traffic`
-        roof["algorithmic_bytes_per_launch"] = rows * S * 4.0 * H * (3 if dom == "bwd_gemm" else 2)
+        roof["algorithmic_bytes_per_launch"] = (bytes_cls[dom] if dom == "fused_step" else
+                                                rows * S * 4.0 * H * (3 if dom == "bwd_gemm" else 2))
         roof["launches_per_step"] = nl / args.steps
         step_flops = wl.flops_per_point() * n_total
         line = {
@@ -553,7 +559,8 @@ def main():
                        "points_total": n_total, "points_per_gpu": rows, "streams": S,
                        "params": P, "engine": args.engine,
                        "contraction": ("3xFP16 split operands, FP32 accumulate" if use_f16 else
-                                       "3xTF32 split operands, FP32 accumulate" if use_tc else "FP32 FFMA"),
+                                       "3xTF32 split operands, FP32 accumulate" if use_tc else
+                                       "FP32 FFMA, whole step in one kernel" if dom == "fused_step" else "FP32 FFMA"),
                        "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (per-step activations >> 126 MB)",
                        "cuda_graph": bool(trainer.graph)},

@@ -176,7 +176,8 @@ int pnx_last_launch_count(const pnx_ctx* ctx, int64_t* n);
 
 /* Kernel-class timing with CUDA events recorded on the launching stream around
  * every launch of a class (0 input, 1 forward GEMM, 2 head, 3 reverse GEMM,
- * 4 weight-gradient GEMM, 5 finalize). pnx_profile(ctx, 1) resets and enables;
+ * 4 weight-gradient GEMM, 5 finalize, 6 the single-kernel step of a narrow
+ * network). pnx_profile(ctx, 1) resets and enables;
  * pnx_profile_read synchronizes and returns accumulated ms and launch counts. */
 int pnx_profile(pnx_ctx* ctx, int on);
 int pnx_profile_read(pnx_ctx* ctx, double* ms, int64_t* counts, int n);

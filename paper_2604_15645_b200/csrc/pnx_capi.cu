@@ -169,10 +169,10 @@ int dalloc(pnx_ctx* ctx, T** p, size_t n) {
     return PNX_OK;
 }
 
-enum ProfClass { PC_INPUT = 0, PC_FWD = 1, PC_HEAD = 2, PC_BWD = 3, PC_WGRAD = 4, PC_FINAL = 5 };
+enum ProfClass { PC_INPUT = 0, PC_FWD = 1, PC_HEAD = 2, PC_BWD = 3, PC_WGRAD = 4, PC_FINAL = 5, PC_FUSED = 6 };
 
 const char* const kClassName[8] = {"pnx input", "pnx forward GEMM", "pnx head", "pnx reverse GEMM",
-                                   "pnx weight gradient", "pnx finalize", "pnx", "pnx"};
+                                   "pnx weight gradient", "pnx finalize", "pnx single-kernel step", "pnx"};
 
 // NVTX range per kernel class (nsys timelines), and with profiling on a CUDA
 // event pair on the launching stream around the launch.
@@ -435,7 +435,7 @@ int run_small(pnx_ctx* ctx, int HP, const float* d_params, const double lam[3], 
     a.slot = ctx->d_sn_slot;
     a.loss_part = ctx->d_loss_part;
     a.P = ctx->P;
-    prof_begin(ctx, PC_FWD, st);
+    prof_begin(ctx, PC_FUSED, st);
     if (launch_small(ctx->pde, HP, a, grid, st)) return fail(ctx, PNX_ERR_CUDA, "small-network step launch");
     prof_end(ctx, st);
     CKL();

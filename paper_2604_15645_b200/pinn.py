@@ -370,11 +370,11 @@ class Worker:
 
     def profile_read(self):
         """{class: (ms, launches)} accumulated since profile(True)."""
-        ms = (C.c_double * 6)()
-        n = (C.c_int64 * 6)()
-        self._chk(self.lib.pnx_profile_read(self.ctx, ms, n, 6))
-        names = ["input", "fwd_gemm", "head", "bwd_gemm", "wgrad_gemm", "finalize"]
-        return {names[i]: (ms[i], n[i]) for i in range(6)}
+        ms = (C.c_double * 7)()
+        n = (C.c_int64 * 7)()
+        self._chk(self.lib.pnx_profile_read(self.ctx, ms, n, 7))
+        names = ["input", "fwd_gemm", "head", "bwd_gemm", "wgrad_gemm", "finalize", "fused_step"]
+        return {names[i]: (ms[i], n[i]) for i in range(7)}
 
     def launch_count(self) -> int:
         n = C.c_int64()

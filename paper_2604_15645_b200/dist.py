@@ -228,9 +228,16 @@ class DataParallelTrainer:
         return self.losses
 
     def check(self):
-        """Raise TensorError for a non-finite residual or gradient since the last check."""
+        """Raise TensorError for a non-finite residual or gradient since the last
+        check and, with several ranks, if the replicas' parameter hashes differ
+        (param_hash / on_sync, trainer.cpp:540-544)."""
         for w in self.workers:
             w.check()
+        if self.world > 1:
+            from .pinn import TensorError
+            hs = replica_hashes(self.worker.spec, self.params.double().cpu().numpy(), self.world, self.group)
+            if len(set(hs)) != 1:
+                raise TensorError(f"data parallel: replica parameter hashes differ after step {self.t}: {hs}")
 
     def should_switch(self, policy) -> bool:
         """SwitchPolicy check after a step (trainer.cpp:532-554): the history is

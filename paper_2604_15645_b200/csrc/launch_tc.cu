@@ -2,6 +2,7 @@
 #include "launch.h"
 
 #include <cudaTypedefs.h>
+#include <algorithm>
 #include <cstdlib>
 
 namespace pnx {
@@ -63,7 +64,13 @@ int launch_tc5_bwd_t(const TcGemmArgs& g, cudaStream_t st) {
                              false))
         return -1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g.Rpad / TC_M);
+    // persistent: one CTA (pair) per SM (pair of SMs) walking the row tiles;
+    // PNX_TC5_ONESHOT=1: one tile per CTA (the round-1 launch, A/B)
+    static const bool oneshot = getenv("PNX_TC5_ONESHOT") != nullptr;
+    const int nsm = device_sm_count();
+    const int ntiles = g.Rpad / (PAIR ? 256 : TC_M);
+    const int groups = oneshot ? ntiles : (PAIR ? std::min(nsm / 2, ntiles) : std::min(nsm, ntiles));
+    cfg.gridDim = dim3(PAIR ? 2 * groups : groups);
     cfg.blockDim = dim3(TC3_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = st;

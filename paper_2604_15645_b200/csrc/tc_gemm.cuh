@@ -1528,7 +1528,14 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0;
-    const int r0 = PAIR ? (int)(blockIdx.x >> 1) * 256 + (int)rank * 128 : (int)blockIdx.x * TC_M;
+    // persistent: group `grp` (a CTA, or a pair) walks tiles grp, grp + ngrp, ...;
+    // every ring / accumulator barrier keeps counting across tiles (pass index
+    // gp = 2 * local tile + pass), so the producers prefetch the next tile's
+    // operands into registers while the epilogue drains the current one
+    const int ngrp = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x, grp = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int ntiles = g.Rpad / (PAIR ? 256 : TC_M);
+    const int nloc = grp < ntiles ? (ntiles - 1 - grp) / ngrp + 1 : 0;
+    auto row0 = [&](int lt) { return PAIR ? (grp + lt * ngrp) * 256 + (int)rank * 128 : (grp + lt * ngrp) * TC_M; };
     const int nkb = g.K / (F16 ? 16 : 8);
     const int64_t RK = (int64_t)g.Rpad * g.K, RN = (int64_t)g.Rpad * NF;
     // weight stage copy of k-step kk into `stage` (tid 0 of the producers)
@@ -1575,7 +1582,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
     // Epilogue warp e = warp - 9: TMEM lane quarter warp % 4, column block cq.
     // (Measured and dropped: the producer warps joining the epilogue -- 16 warps,
     // 64 columns each, single-buffered staging -- bwd 16.9 -> 17.7 ms/step.)
-    auto run_epilogue = [&](int pass) {
+    auto run_epilogue = [&](int pass, int gp, int r0) {
         const int ew = warp - 9;
         const int q = warp & 3, cq = (warp - 9) >> 2;
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
@@ -1608,7 +1615,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
             if (s1 >= 0) usb = usw * ldexpf(1.0f, -tc::f16_exp_bits(g.amax_in[s1]));
         }
         float mxa = 0.0f, mxb = 0.0f;
-        tc::mbar_wait(&tfull, (uint32_t)pass);
+        tc::mbar_wait(&tfull, (uint32_t)gp & 1u);
         tc::tc_fence_after();
         TC_T0();
         issue(0);
@@ -1727,10 +1734,11 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
     if (F16 && warp < 8) {
         // ---------------- producers (3xFP16): one 16-wide k-step per stage ----------------
         const int prow = tid >> 1, pc = tid & 1;
-        const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 8;
         const uint32_t aoff = tc::sw32_chunk((uint32_t)prow, (uint32_t)pc);
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int gp = 0; gp < 2 * nloc; ++gp) {
+            const int pass = gp & 1;
+            const float* asrc = g.A + (int64_t)(row0(gp >> 1) + prow) * g.K + pc * 8;
             const int s0 = Cfg::sa(pass), s1 = Cfg::sb(pass);
             const float sc0 = ldexpf(1.0f, tc::f16_exp_bits(g.amax_in[s0]));
             const float sc1 = s1 >= 0 ? ldexpf(1.0f, tc::f16_exp_bits(g.amax_in[s1])) : 1.0f;
@@ -1744,7 +1752,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                     rb[d][u] = (s1 >= 0 && d < nkb) ? ldg4(asrc + s1 * RK + d * 16 + 4 * u)
                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
-            if (pass == 1) tc::mbar_wait(&tempty, 0);  // the epilogue released the stage ring
+            if (gp > 0) tc::mbar_wait(&tempty, (uint32_t)(gp - 1) & 1u);  // the epilogue released the stage ring
 #pragma unroll 1
             for (int kb0 = 0; kb0 < nkb; kb0 += D)
 #pragma unroll
@@ -1767,7 +1775,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                             if (s1 >= 0) rb[cur][u] = ldg4(asrc + s1 * RK + (kb + D) * 16 + 4 * u);
                         }
                     }
-                    const int it = pass * nkb + kb, st = it % NST;
+                    const int it = gp * nkb + kb, st = it % NST;
                     const uint32_t stage = sbase + st * Cfg::STAGE;
                     tc::mbar_wait(&empty[st], ((uint32_t)(it / NST) & 1u) ^ 1u);
                     if (tid == 0) load_w(kb, st, stage, full0);
@@ -1788,10 +1796,11 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
     } else if (warp < 8) {
         // ---------------- producers: A tiles of the pass's two streams ----------------
         const int prow = tid >> 1, pc = tid & 1;
-        const float* asrc = g.A + (int64_t)(r0 + prow) * g.K + pc * 4;
         const uint32_t aoff = tc::sw32_off((uint32_t)prow, (uint32_t)(pc * 4));
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int gp = 0; gp < 2 * nloc; ++gp) {
+            const int pass = gp & 1;
+            const float* asrc = g.A + (int64_t)(row0(gp >> 1) + prow) * g.K + pc * 4;
             const int s0 = Cfg::sa(pass), s1 = Cfg::sb(pass);
             constexpr int D = 4;  // k-steps of A prefetched in registers
             float4 ra[D], rb[D];
@@ -1800,7 +1809,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                 ra[d] = d < nkb ? ldg4(asrc + s0 * RK + d * 8) : make_float4(0.f, 0.f, 0.f, 0.f);
                 rb[d] = (s1 >= 0 && d < nkb) ? ldg4(asrc + s1 * RK + d * 8) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            if (pass == 1) tc::mbar_wait(&tempty, 0);  // the epilogue released the stage ring
+            if (gp > 0) tc::mbar_wait(&tempty, (uint32_t)(gp - 1) & 1u);  // the epilogue released the stage ring
             // two k-steps per iteration: their stores share one proxy fence
 #pragma unroll 1
             for (int kb0 = 0; kb0 < nkb; kb0 += D)
@@ -1821,7 +1830,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                 }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                    const int it = pass * nkb + kb + u, st = it % NST;
+                    const int it = gp * nkb + kb + u, st = it % NST;
                     const uint32_t stage = sbase + st * Cfg::STAGE;
                     {
                         TC_T0();
@@ -1841,7 +1850,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
                 if (lane == 0)
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
-                        const int st = (pass * nkb + kb + u) % NST;
+                        const int st = (gp * nkb + kb + u) % NST;
                         if constexpr (PAIR) tc::mbar_arrive_cluster(full0 + st * 8);
                         else tc::mbar_arrive(&full[st]);
                     }
@@ -1852,12 +1861,13 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
         if (lane == 0 && rank == 0) {
             constexpr uint32_t idesc = F16 ? tc::make_idesc_f16(PAIR ? 2 * TC_M : TC_M, NF, 0, 0)
                                            : tc::make_idesc_tf32(PAIR ? 2 * TC_M : TC_M, NF, 0, 0);
-            for (int pass = 0; pass < 2; ++pass) {
+            for (int gp = 0; gp < 2 * nloc; ++gp) {
+                const int pass = gp & 1;
                 const bool two = Cfg::sb(pass) >= 0;
-                if (pass == 1) tc::mbar_wait(&tempty_all, 0);
+                if (gp > 0) tc::mbar_wait(&tempty_all, (uint32_t)(gp - 1) & 1u);  // TMEM drained
                 tc::tc_fence_after();
                 for (int kb = 0; kb < nkb; ++kb) {
-                    const int it = pass * nkb + kb, st = it % NST;
+                    const int it = gp * nkb + kb, st = it % NST;
                     const uint32_t stage = sbase + st * Cfg::STAGE;
                     {
                         TC_T0();
@@ -1905,7 +1915,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc5_bwd(const __grid_constan
         __syncwarp();
     } else {
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) run_epilogue(pass);
+        for (int gp = 0; gp < 2 * nloc; ++gp) run_epilogue(gp & 1, gp, row0(gp >> 1));
     }
     tc::tc_fence_before();
     if constexpr (PAIR) tc::cluster_sync();

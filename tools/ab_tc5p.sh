@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B: persistent backward (default) vs one tile per CTA (PNX_TC5_ONESHOT=1), same box
-for v in "" "PNX_TC5_ONESHOT=1" "" "PNX_TC5_ONESHOT=1"; do
+for v in ${VARIANTS:-"" "PNX_TC5_ONESHOT=1" "" "PNX_TC5_ONESHOT=1"}; do
   env $v python bench.py --no-cpu-baseline --no-e2e --steps 10 > gpurun_out/abp.json 2>&1
   python - "$v" <<'PY'
 import json, sys

@@ -62,16 +62,18 @@ __host__ __device__ inline int64_t sn_smem_floats(int HP, int S, int D) {
     return w + (int64_t)J * SN_MAXK0 + (int64_t)(D + 2) * J * LD + (int64_t)SN_TR * S * 4;
 }
 
-template <int P, int HP>
-__global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
+template <int P, int HP, int NT = SN_THREADS>
+__global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
     using Tr = PdeTraits<P>;
     constexpr int L = Tr::L, F = Tr::F, K = Tr::K;
     constexpr int S = Streams<L>::S;
     constexpr int TR = SN_TR, J = S * TR, LD = HP + 4;
-    constexpr int NC = HP / 16;            // output features per warp in the row GEMMs
-    constexpr int BN = HP == 64 ? 4 : 2;   // dW block per thread: BK x BN
-    constexpr int BK = HP == 64 ? 2 : 1;
-    static_assert(HP * HP == SN_THREADS * BK * BN, "dW blocks tile the weight");
+    constexpr int NWARP = NT / 32;
+    constexpr int NC = HP / NWARP;                                 // output features per warp in the row GEMMs
+    constexpr int EPT = HP * HP / NT;                              // dW entries per thread: BK x BN
+    constexpr int BN = EPT >= 4 ? 4 : EPT;
+    constexpr int BK = EPT / BN;
+    static_assert(HP * HP == NT * BK * BN && NC >= 1, "dW blocks tile the weight");
     extern __shared__ float4 sn_smem4[];
     float* sm = reinterpret_cast<float*>(sn_smem4);
     const int D = a.D, H = a.H, K0 = a.K0;
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
     float* Hb = Zs + (int64_t)D * J * LD;              // [J][LD] act(Z) / reverse scratch
     float* ZB = Hb + J * LD;                           // [J][LD] adjoints of the current layer
     float* OB = ZB + J * LD;                           // [TR][S][4] output seeds
-    __shared__ double lacc[SN_THREADS / 32][3];
+    __shared__ double lacc[NWARP][3];
 
     // ---- weights -> shared memory, zero-padded ----
     const LayerTab& t = a.tab;
@@ -95,14 +97,14 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
         const int Kl = t.K[l], Nl = t.N[l];
         const int rows = l == 0 ? SN_MAXK0 : HP, cols = l == D ? 4 : HP;
         float* dst = wlayer(l);
-        for (int i = tid; i < rows * cols; i += SN_THREADS) {
+        for (int i = tid; i < rows * cols; i += NT) {
             const int k = i / cols, n = i % cols;
             dst[i] = (k < Kl && n < Nl) ? a.params[t.offW[l] + (int64_t)k * Nl + n] : 0.0f;
         }
         const int bn = l == D ? 4 : HP;
-        for (int n = tid; n < bn; n += SN_THREADS) Bs[l * HP + n] = n < Nl ? a.params[t.offB[l] + n] : 0.0f;
+        for (int n = tid; n < bn; n += NT) Bs[l * HP + n] = n < Nl ? a.params[t.offB[l] + n] : 0.0f;
     }
-    if (tid < 3 * (SN_THREADS / 32)) lacc[tid / 3][tid % 3] = 0.0;
+    if (tid < 3 * NWARP) lacc[tid / 3][tid % 3] = 0.0;
     double* slot = a.slot + (int64_t)blockIdx.x * a.P;
     const int ntiles = (int)((a.T + TR - 1) / TR);
     bool first = true;
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
         }
 
         // ---- head: outputs, residual / IC / BC losses and seeds (two rows per warp) ----
-        for (int rr = warp; rr < TR; rr += SN_THREADS / 32) {
+        for (int rr = warp; rr < TR; rr += NWARP) {
             float o[S * F];
 #pragma unroll
             for (int i = 0; i < S * F; ++i) o[i] = 0.0f;
@@ -264,15 +266,15 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
             for (int s = 0; s < S; ++s)
                 for (int r = 0; r < TR; ++r) v = fmaf(Hb[(s * TR + r) * LD + k], OB[(r * S + s) * 4 + f], v);
             if (k < H) acc_slot(t.offW[D] + (int64_t)k * F + f, v);
-        } else if (tid >= 512 - F) {
-            const int f = tid - (512 - F);
+        } else if (tid >= NT - F) {
+            const int f = tid - (NT - F);
             double v = 0.0;
             for (int r = 0; r < TR; ++r) v += (double)OB[(r * S) * 4 + f];
             acc_slot(t.offB[D] + f, v);
         }
         {
             const float* Zl = Zs + (int64_t)(D - 1) * J * LD;
-            for (int e = tid; e < TR * HP; e += SN_THREADS) {
+            for (int e = tid; e < TR * HP; e += NT) {
                 const int r = e / HP, k = e % HP;
                 float zz[S], hb[S], zb[S];
 #pragma unroll
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
             const int lda = l == 0 ? SN_MAXK0 : LD;
             if (l > 0) {  // Hb = act(Z_{l-1}) (the layer's input activations)
                 const float* Zp = Zs + (int64_t)(l - 1) * J * LD;
-                for (int e = tid; e < TR * HP; e += SN_THREADS) {
+                for (int e = tid; e < TR * HP; e += NT) {
                     const int r = e / HP, k = e % HP;
                     float zz[S], hh[S];
 #pragma unroll
@@ -319,7 +321,14 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
 #pragma unroll 4
                 for (int jj = 0; jj < J; ++jj) {
                     float av[BK], bv[BN];
-                    if constexpr (BK == 2 && BN == 4) {  // LDS.64 + LDS.128 (16 B-aligned rows)
+                    if constexpr (BK == 1 && BN == 4) {  // LDS.32 + LDS.128
+                        const float4 b4 = *reinterpret_cast<const float4*>(ZB + jj * LD + nb);
+                        av[0] = A[jj * lda + kb];
+                        bv[0] = b4.x;
+                        bv[1] = b4.y;
+                        bv[2] = b4.z;
+                        bv[3] = b4.w;
+                    } else if constexpr (BK == 2 && BN == 4) {  // LDS.64 + LDS.128 (16 B-aligned rows)
                         const float2 a2 = *reinterpret_cast<const float2*>(A + jj * lda + kb);
                         const float4 b4 = *reinterpret_cast<const float4*>(ZB + jj * LD + nb);
                         av[0] = a2.x;
@@ -345,7 +354,7 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
                     for (int j = 0; j < BN; ++j)
                         if (kb + i < Kl && nb + j < H) acc_slot(t.offW[l] + (int64_t)(kb + i) * H + nb + j, acc[i][j]);
             } else {
-                for (int e = tid; e < K0 * HP; e += SN_THREADS) {
+                for (int e = tid; e < K0 * HP; e += NT) {
                     const int k = e / HP, n = e % HP;
                     float v = 0.0f;
                     for (int jj = 0; jj < J; ++jj) v = fmaf(A[jj * lda + k], ZB[jj * LD + n], v);
@@ -402,7 +411,7 @@ __global__ void __launch_bounds__(SN_THREADS, 1) k_small_step(SmallArgs a) {
     __syncthreads();
     if (tid < 3) {  // fixed-order fold of the warps' loss sums
         double v = 0.0;
-        for (int w = 0; w < SN_THREADS / 32; ++w) v += lacc[w][tid];
+        for (int w = 0; w < NWARP; ++w) v += lacc[w][tid];
         a.loss_part[blockIdx.x * 3 + tid] = v;
     }
 }

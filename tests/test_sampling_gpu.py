@@ -132,3 +132,24 @@ def test_dp_group_device_design():
     lb, gb = b.step(update=False, want_grad=True)
     assert np.array_equal(ga, gb) and la == lb
     assert np.linalg.norm(ga - g["grad_w2"]) <= 1e-5 * np.linalg.norm(g["grad_w2"])
+
+
+def test_device_design_with_chunked_rows_matches_uploaded_points():
+    """A device design laid out over several chunks (the 64M-point path: rows
+    beyond the activation budget stream through in chunks) gives the step of the
+    same points uploaded from the host, bit for bit."""
+    pk = _pkg()
+    from paper_2604_15645_b200 import configs
+    wl = configs.get_config("c4")
+    col = configs.collocation(wl, [10, 10, 6])
+    flat, rffB = pk.init_params(wl.spec, seed=4)
+    dom = wl.domain
+    a = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, **col)
+    a.sample_points("lhs", dom, n=1500, seed=9)
+    a.set_chunk_rows(512)
+    ga, la = a.step(flat)
+    pts = a.points()
+    b = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, **dict(col, interior=pts))
+    b.set_chunk_rows(512)
+    gb, lb = b.step(flat)
+    assert np.array_equal(ga, gb) and la == lb

@@ -1,5 +1,11 @@
-for n in A B A B; do
-  if [ $n = B ]; then export PNX_LIB_PATH=$PWD/build_var/libpnx_B.so; else unset PNX_LIB_PATH; fi
-  timeout 200 python bench.py --no-cpu-baseline --no-e2e --steps 8 > gpurun_out/v.log 2>&1
-  python -c "import json;d=json.loads(open('gpurun_out/v.log').read().strip().splitlines()[-1]);k=d['kernel_ms_per_step'];print('$n', round(d['ms_per_step'],2), {a:round(b,2) for a,b in k.items() if b}, d['clocks']['sm_mhz'])"
+#!/bin/bash
+# A/B of two builds of libpnx on the same box: ab_base/libpnx.so (PNX_LIB_PATH) vs the in-tree one
+for lib in ab_base/libpnx.so "" ab_base/libpnx.so ""; do
+  PNX_LIB_PATH=$lib python bench.py --no-cpu-baseline --no-e2e --steps 10 > gpurun_out/ablib.json 2>&1
+  python - "${lib:-new}" <<'PY'
+import json, sys
+l = json.loads(open("gpurun_out/ablib.json").read().strip().split("\n")[-1])
+print(sys.argv[1], "%.2f ms" % l["ms_per_step"], {k: round(v, 2) for k, v in l["kernel_ms_per_step"].items() if v},
+      "clk", l["clocks"]["sm_mhz"])
+PY
 done

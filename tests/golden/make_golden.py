@@ -46,6 +46,13 @@ CASES = {
                              model={"in_dim": 3, "hidden_dim": 256, "depth": 6, "out_dim": 3, "activation": "tanh"},
                              collocation={"mode": "uniform", "dims": [8, 6, 5], "n_ic": 16},
                              workers=[1, 2]),
+    # C2 at full width: RFF (128 features, sigma 10) + RWF, tanh 4x128, small grid
+    "burgers_c2_shape": dict(BURGERS, bc="dirichlet_zero",
+                             model={"in_dim": 2, "hidden_dim": 128, "depth": 4, "out_dim": 1, "activation": "tanh",
+                                    "rff": {"width": 128, "sigma": 10.0, "mean": 0.0},
+                                    "rwf": {"mean": 1.0, "stddev": 0.1}},
+                             collocation={"mode": "uniform", "dims": [16, 12], "n_ic": 32, "n_bc": 16},
+                             workers=[1, 2]),
     # C2 family: RFF + RWF
     "burgers_rff_rwf": dict(BURGERS, bc="dirichlet_zero",
                             model={"in_dim": 2, "hidden_dim": 16, "depth": 2, "out_dim": 1, "activation": "tanh",

@@ -733,15 +733,43 @@ TrainResult train(Model& model, const TrainingProblem& prob, const TrainConfig& 
     return result;
 }
 
+namespace {
+
+// one Adam pass over [lo, hi) (optim.cpp:7-41, the same expression order)
+void adam_range(double* __restrict p, double* __restrict m, double* __restrict v, const double* __restrict g,
+                std::size_t lo, std::size_t hi, double lr, double b1, double b2, double eps, double bc1,
+                double bc2) {
+    for (std::size_t k = lo; k < hi; ++k) {
+        m[k] = b1 * m[k] + (1.0 - b1) * g[k];
+        v[k] = b2 * v[k] + (1.0 - b2) * g[k] * g[k];
+        p[k] -= lr * (m[k] / bc1) / (std::sqrt(v[k] / bc2) + eps);
+    }
+}
+
+}  // namespace
+
 void adam_update(double* p, double* m, double* v, const double* g, std::size_t n, double lr,
                  const AdamConfig& a, std::int64_t t) {
     const double bc1 = 1.0 - std::pow(a.beta1, static_cast<double>(t));
     const double bc2 = 1.0 - std::pow(a.beta2, static_cast<double>(t));
-    for (std::size_t k = 0; k < n; ++k) {
-        m[k] = a.beta1 * m[k] + (1.0 - a.beta1) * g[k];
-        v[k] = a.beta2 * v[k] + (1.0 - a.beta2) * g[k] * g[k];
-        p[k] -= lr * (m[k] / bc1) / (std::sqrt(v[k] / bc2) + a.eps);
+    // elementwise and divide/sqrt-bound: large vectors split over host threads
+    // (each element is computed exactly as in the serial loop)
+    const std::size_t kMinPerThread = 32768;
+    std::size_t nt = std::min<std::size_t>(std::max(1u, std::thread::hardware_concurrency()), 16);
+    nt = std::max<std::size_t>(1, std::min(nt, n / kMinPerThread));
+    if (nt <= 1) {
+        adam_range(p, m, v, g, 0, n, lr, a.beta1, a.beta2, a.eps, bc1, bc2);
+        return;
     }
+    std::vector<std::thread> pool;
+    pool.reserve(nt - 1);
+    const std::size_t per = (n + nt - 1) / nt;
+    for (std::size_t i = 1; i < nt; ++i) {
+        const std::size_t lo = std::min(n, i * per), hi = std::min(n, lo + per);
+        pool.emplace_back(adam_range, p, m, v, g, lo, hi, lr, a.beta1, a.beta2, a.eps, bc1, bc2);
+    }
+    adam_range(p, m, v, g, 0, std::min(n, per), lr, a.beta1, a.beta2, a.eps, bc1, bc2);
+    for (auto& th : pool) th.join();
 }
 
 }  // namespace pinnlab_b200

@@ -12,12 +12,14 @@
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool (nsys) is attached
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pnx.h"
@@ -101,6 +103,9 @@ struct pnx_ctx {
     // graph capture): host-side writes to step inputs wait on it
     cudaEvent_t ev_done = nullptr;
     bool ev_pending = false;
+    // pinned FP32 staging of the host-buffer step (pnx_step): params in, gradient out
+    float* h_stage = nullptr;
+    int64_t stage_cap = 0;
     // 3xFP16 operand bounds (float bits): [|W_l|] [|Z_l[s]|] [|Zb_l[s]|]
     unsigned* d_amax = nullptr;
     float* d_resid = nullptr;
@@ -249,6 +254,24 @@ int causality_counts(pnx_ctx* ctx, const double* tcol, int64_t n) {
     }
     CK(cudaMemcpy(ctx->d_caus_cnt, cnt.data(), cnt.size() * 8, cudaMemcpyHostToDevice));
     return PNX_OK;
+}
+
+// [0, n) split over a few host threads when n is large (the FP64 <-> FP32
+// conversions of pnx_step: ~P elements each way per step)
+template <class F>
+static void host_par_for(int64_t n, F&& f) {
+    const int64_t kMinPerThread = 65536;
+    int nt = (int)std::min<int64_t>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())),
+                                    n / kMinPerThread);
+    if (nt <= 1) {
+        f((int64_t)0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const int64_t per = (n + nt - 1) / nt;
+    for (int i = 1; i < nt; ++i) pool.emplace_back([&, i] { f(std::min(n, i * per), std::min(n, (i + 1) * per)); });
+    f((int64_t)0, std::min(n, per));
+    for (auto& t : pool) t.join();
 }
 
 int wait_last_step(pnx_ctx* ctx);
@@ -1113,6 +1136,7 @@ void pnx_destroy(pnx_ctx* ctx) {
     tc_workspace_free(ctx->tc);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1402,24 +1426,45 @@ int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double
              double losses_out[3]) {
     if (!ctx || !params || !lambdas) return PNX_ERR_ARG;
     CK(cudaSetDevice(ctx->device));
-    std::vector<float> p32((size_t)ctx->P);
-    for (int64_t i = 0; i < ctx->P; ++i) p32[(size_t)i] = (float)params[i];
-    CK(cudaMemcpyAsync(ctx->d_params, p32.data(), p32.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    const int64_t P = ctx->P;
+    if (ctx->stage_cap < 2 * P) {  // pinned: the copies are DMA at link speed, not staged by the driver
+        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+        ctx->h_stage = nullptr;
+        ctx->stage_cap = 0;
+        CK(cudaMallocHost(&ctx->h_stage, (size_t)(2 * P) * 4));
+        ctx->stage_cap = 2 * P;
+    }
+    float* p32 = ctx->h_stage;
+    float* g32 = ctx->h_stage + P;
+    if (int r = wait_last_step(ctx)) return r;  // an earlier step may still read the staging buffer
+    host_par_for(P, [&](int64_t lo, int64_t hi) {
+        for (int64_t i = lo; i < hi; ++i) p32[i] = (float)params[i];
+    });
+    CK(cudaMemcpyAsync(ctx->d_params, p32, (size_t)P * 4, cudaMemcpyHostToDevice, ctx->stream));
     if (int r = run_step(ctx, ctx->d_params, lambdas, ctx->d_grad, ctx->d_losses, ctx->stream)) return r;
-    std::vector<float> g32((size_t)ctx->P);
     double losses[3];
-    CK(cudaMemcpyAsync(g32.data(), ctx->d_grad, g32.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(g32, ctx->d_grad, (size_t)P * 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(losses, ctx->d_losses, sizeof(losses), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (int r = pnx_check(ctx)) return r;
     for (int t = 0; t < 3; ++t)
         if (!std::isfinite(losses[t])) return fail(ctx, PNX_ERR_NONFINITE, "non-finite loss in worker step");
-    if (grad_out)
-        for (int64_t i = 0; i < ctx->P; ++i) {
-            if (!std::isfinite(g32[(size_t)i]))
-                return fail(ctx, PNX_ERR_NONFINITE, "non-finite gradient entry " + std::to_string(i));
-            grad_out[i] = (double)g32[(size_t)i];
-        }
+    if (grad_out) {
+        std::vector<int64_t> first_bad(8, INT64_MAX);  // first non-finite entry per thread range
+        std::atomic<int> slot{0};
+        host_par_for(P, [&](int64_t lo, int64_t hi) {
+            const int me = slot.fetch_add(1);
+            for (int64_t i = lo; i < hi; ++i) {
+                if (!std::isfinite(g32[i])) {
+                    first_bad[me] = i;
+                    return;
+                }
+                grad_out[i] = (double)g32[i];
+            }
+        });
+        const int64_t bad = *std::min_element(first_bad.begin(), first_bad.end());
+        if (bad != INT64_MAX) return fail(ctx, PNX_ERR_NONFINITE, "non-finite gradient entry " + std::to_string(bad));
+    }
     if (losses_out)
         for (int t = 0; t < 3; ++t) losses_out[t] = losses[t];
     return PNX_OK;

@@ -19,8 +19,8 @@ for f in gpurun_out/ncu2/full_*.ncu-rep; do
     python tools/ncu_summary.py "$f" > "${f%.ncu-rep}.txt" 2>&1
     python tools/ncu_lines.py "$f" 25 > "${f%.ncu-rep}_lines.txt" 2>&1
 done
-python tools/ncu_launches.py gpurun_out/ncu2/launches_bench.csv 4 \
-    "# ncu launch list of: $BENCH (C5 @ 1,048,576 points, 1 GPU, engine auto; warm-up + eager + 2 timed steps = 4 steps)" \
+python tools/ncu_launches.py gpurun_out/ncu2/launches_bench.csv 6 \
+    "# ncu launch list of: $BENCH (C5 @ 1,048,576 points, 1 GPU, engine auto; CUDA-graph mode: 1 warm-up + 1 eager + 2 eager per-class profiling + 2 timed graph replays = 6 steps; ncu profiles graph nodes as launches)" \
     > gpurun_out/ncu2/launches_bench_summary.txt 2>&1
 [ -n "${KEEP_REPORTS:-}" ] || rm -f gpurun_out/ncu2/*.ncu-rep
 ls -la gpurun_out/ncu2

@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "collocation points/s per train step (residual+grad), 1/2/4/8 B200 vs CPU"
 UNIT = "points/s"
+L2_BYTES = 126e6  # B200 L2 (B200_PROFILING.md)
 
 
 def _args():
@@ -396,10 +397,26 @@ def main():
     clk.mark()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
+    # per-step device working set: Z and Zb of every hidden layer (multi-kernel
+    # path), or just the coordinates and parameters (single-kernel step); a set
+    # that fits in L2 is timed step by step with an L2 flush (a 512 MB write)
+    # between steps, outside the per-step events
+    work_bytes = ((hi - lo) * 8.0 * len(wl.domain) + P * 4.0) if worker.launch_count() < 8 else \
+        (hi - lo) * wl.streams() * 4.0 * wl.spec.hidden_dim * wl.spec.depth * 2
+    l2_flush = work_bytes < 2 * L2_BYTES
+    if l2_flush:
+        scrub = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for a, b in ev:
+            scrub.fill_(1)
+            a.record(stream)
+            step()
+            b.record(stream)
+    else:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -413,7 +430,7 @@ def main():
         from paper_2604_15645_b200.dist import replica_hashes
         hs = replica_hashes(wl.spec, trainer.params_host(), world)
         replicas_equal = len(set(hs)) == 1
-    ms = e0.elapsed_time(e1)
+    ms = sum(a.elapsed_time(b) for a, b in ev) if l2_flush else e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -562,7 +579,9 @@ def main():
                                        "3xTF32 split operands, FP32 accumulate" if use_tc else
                                        "FP32 FFMA, whole step in one kernel" if dom == "fused_step" else "FP32 FFMA"),
                        "parallelism": f"dp{world}",
-                       "l2": "inputs larger than L2 (per-step activations >> 126 MB)",
+                       "l2": (f"working set {work_bytes / 1e6:.1f} MB fits in L2: each timed step preceded by a "
+                              f"512 MB L2 flush outside its CUDA events (steps timed one by one)" if l2_flush else
+                              f"inputs larger than L2 (per-step activations {work_bytes / 1e9:.2f} GB >> 126 MB)"),
                        "cuda_graph": bool(trainer.graph)},
             "tflops_step": step_flops / (ms_step / 1e3) / 1e12,
             "roofline": roof,

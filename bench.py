@@ -460,18 +460,20 @@ def main():
         g_dev = torch.zeros(P, dtype=torch.float64, device=dev)
         h2d = d2h = 0
 
+        g_buf = np.empty(P, dtype=np.float64)
+        pts = shard_pinned.numpy()
+        ptr_p, ptr_m, ptr_v, ptr_g = pp(host_params), pp(opt_m), pp(opt_v), pp(g_buf)  # updated in place
+
         def e2e_step(k):
             nonlocal h2d, d2h
-            pts = shard_pinned.numpy()
-            worker.set_points(pts, axis_major=True)     # H2D of this step's collocation batch
-            g_host, l = worker.step(host_params, lam)   # H2D params, D2H grad + losses
+            worker.set_points(pts, axis_major=True)          # H2D of this step's collocation batch
+            _, l = worker.step(host_params, lam, out=g_buf)  # H2D params, D2H grad + losses
             if world > 1:
-                g_dev.copy_(torch.from_numpy(g_host))
+                g_dev.copy_(torch.from_numpy(g_buf))
                 dist.all_reduce(g_dev, op=dist.ReduceOp.SUM)
-                g_host = g_dev.cpu().numpy() / world
-            g_host = np.ascontiguousarray(g_host)
+                g_buf[:] = g_dev.cpu().numpy() / world
             # host Adam in place (optim.cpp:7-41), the C++ host mirror's fused loop
-            hadam(pp(host_params), pp(opt_m), pp(opt_v), pp(g_host), P, 1e-3, 0.9, 0.999, 1e-8, k)
+            hadam(ptr_p, ptr_m, ptr_v, ptr_g, P, 1e-3, 0.9, 0.999, 1e-8, k)
             h2d = pts.nbytes + P * 4
             d2h = P * 4 + 3 * 8
 

@@ -1400,6 +1400,8 @@ int pnx_step_device(pnx_ctx* ctx, const float* d_params, const double lambdas[3]
     return run_step(ctx, d_params, lambdas, d_grad, d_losses, reinterpret_cast<cudaStream_t>(stream));
 }
 
+static int report_bad(pnx_ctx* ctx, const int* bad);
+
 int pnx_check(pnx_ctx* ctx) {
     if (!ctx) return PNX_ERR_ARG;
     CK(cudaSetDevice(ctx->device));
@@ -1407,6 +1409,11 @@ int pnx_check(pnx_ctx* ctx) {
     int bad[5];
     CK(cudaDeviceSynchronize());  // Adam may run on another stream than the step
     CK(cudaMemcpy(bad, ctx->d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+    return report_bad(ctx, bad);
+}
+
+// the sticky flags as read back: PNX_OK, or reset them and raise the first one
+static int report_bad(pnx_ctx* ctx, const int* bad) {
     bool any = false;
     for (int k = 0; k < 5; ++k) any |= bad[k] != kBadNone;
     if (!any) return PNX_OK;
@@ -1431,22 +1438,28 @@ int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double
         if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
         ctx->h_stage = nullptr;
         ctx->stage_cap = 0;
-        CK(cudaMallocHost(&ctx->h_stage, (size_t)(2 * P) * 4));
+        CK(cudaMallocHost(&ctx->h_stage, (size_t)(2 * P) * 4 + 64));
         ctx->stage_cap = 2 * P;
     }
+    // pinned layout: [params f32 P][grad f32 P][losses f64 x3][flags i32 x5] (2P floats keep 8 B alignment)
     float* p32 = ctx->h_stage;
     float* g32 = ctx->h_stage + P;
+    double* hl = reinterpret_cast<double*>(ctx->h_stage + 2 * P);
+    int* hbad = reinterpret_cast<int*>(hl + 3);
     if (int r = wait_last_step(ctx)) return r;  // an earlier step may still read the staging buffer
     host_par_for(P, [&](int64_t lo, int64_t hi) {
         for (int64_t i = lo; i < hi; ++i) p32[i] = (float)params[i];
     });
     CK(cudaMemcpyAsync(ctx->d_params, p32, (size_t)P * 4, cudaMemcpyHostToDevice, ctx->stream));
     if (int r = run_step(ctx, ctx->d_params, lambdas, ctx->d_grad, ctx->d_losses, ctx->stream)) return r;
-    double losses[3];
+    // gradient, losses and the sticky non-finite flags (written by this step's
+    // kernels on ctx->stream) in one pinned read-back, one synchronisation
     CK(cudaMemcpyAsync(g32, ctx->d_grad, (size_t)P * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(losses, ctx->d_losses, sizeof(losses), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(hl, ctx->d_losses, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(hbad, ctx->d_bad, 5 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (int r = pnx_check(ctx)) return r;
+    if (int r = report_bad(ctx, hbad)) return r;
+    const double losses[3] = {hl[0], hl[1], hl[2]};
     for (int t = 0; t < 3; ++t)
         if (!std::isfinite(losses[t])) return fail(ctx, PNX_ERR_NONFINITE, "non-finite loss in worker step");
     if (grad_out) {

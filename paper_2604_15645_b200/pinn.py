@@ -278,12 +278,16 @@ class Worker:
                                       b.ctypes.data_as(P) if b is not None else None,
                                       t.ctypes.data_as(P) if t is not None else None, a.shape[1]))
 
-    def step(self, params: np.ndarray, lambdas=(1.0, 1.0, 1.0)):
-        """run_worker_epoch equivalent: returns (grad float64 [P], losses dict)."""
-        p = np.ascontiguousarray(np.asarray(params, dtype=np.float64))
+    def step(self, params: np.ndarray, lambdas=(1.0, 1.0, 1.0), out: np.ndarray = None):
+        """run_worker_epoch equivalent: returns (grad float64 [P], losses dict);
+        `out` (float64 [P], contiguous) receives the gradient when given."""
+        p = params if (isinstance(params, np.ndarray) and params.dtype == np.float64 and params.flags.c_contiguous) \
+            else np.ascontiguousarray(np.asarray(params, dtype=np.float64))
         if p.size != self.n_params:
             raise TensorError("adam: parameter/gradient count mismatch")
-        g = np.empty(self.n_params, dtype=np.float64)
+        if out is not None and not (out.dtype == np.float64 and out.flags.c_contiguous and out.size == self.n_params):
+            raise TensorError("adam: parameter/gradient count mismatch")
+        g = out if out is not None else np.empty(self.n_params, dtype=np.float64)
         lam = (C.c_double * 3)(*lambdas)
         losses = (C.c_double * 3)()
         P = C.POINTER(C.c_double)

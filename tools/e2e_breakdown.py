@@ -15,8 +15,9 @@ import paper_2604_15645_b200 as pk
 from paper_2604_15645_b200 import configs
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-wl = configs.get_config("c4")
-dims = configs.weak_scaling_dims(1 << 20, 1)
+cfg = sys.argv[2] if len(sys.argv) > 2 else "c5"
+wl = configs.get_config("c4" if cfg == "c5" else cfg)
+dims = configs.weak_scaling_dims(1 << 20, 1) if cfg == "c5" else wl.dims
 col = configs.collocation(wl, dims)
 flat, rffB = pk.init_params(wl.spec, seed=0)
 w = pk.make_worker(wl.spec, wl.res, wl.bc, rffB, **col)

@@ -45,9 +45,10 @@ def _args():
     ap.add_argument("--engine", default="auto", choices=["auto", "ffma", "tc3xtf32", "tc3xf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
-                    help="time CUDA-graph replays of the whole step (default; class timings then come from a "
-                         "separate eager pass)")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=None,
+                    help="time CUDA-graph replays of the whole step (default on one GPU; class timings then come "
+                         "from a separate eager pass). Multi-rank runs default to eager launches: capturing the "
+                         "torch NCCL all-reduce in a graph is not exercised on this single-GPU pool")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="time eager launches")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -360,8 +361,10 @@ def main():
                                 col["bc_a"], col["bc_b"], col["bc_targets"], device=gpu, engine=args.engine)
     P = worker.n_params
     from paper_2604_15645_b200.dist import DataParallelTrainer
-    # one CUDA graph per step on a single GPU (the multi-GPU step keeps NCCL eager)
-    trainer = DataParallelTrainer(worker, flat, world=world, lr=1e-3, device=dev, graph=args.graph)
+    # one CUDA graph per step on a single GPU; multi-rank steps launch eagerly unless --graph
+    # (at C5 a step is ~43 ms of device work, so ~60 launches hide behind it)
+    use_graph = args.graph if args.graph is not None else world == 1
+    trainer = DataParallelTrainer(worker, flat, world=world, lr=1e-3, device=dev, graph=use_graph)
     stream = torch.cuda.current_stream(dev)
     st = stream.cuda_stream
     lam = (1.0, 1.0, 1.0)

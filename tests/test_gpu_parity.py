@@ -68,6 +68,12 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
+def elementwise_ratio(a, b, tol):
+    """SURVEY.md 8(c)'s elementwise bound |a_i - b_i| <= tol max|b| + tol |b_i|, as the
+    largest ratio of error to bound (<= 1 passes)."""
+    return float(np.max(np.abs(a - b) / (tol * np.max(np.abs(b)) + tol * np.abs(b) + 1e-300)))
+
+
 @pytest.mark.parametrize("engine", ["ffma", "auto"])
 @pytest.mark.parametrize("name", gi.CASE_NAMES)
 def test_golden_gradients_and_losses(name, engine):
@@ -82,6 +88,7 @@ def test_golden_gradients_and_losses(name, engine):
         ref = g[f"grad_w{w}"]
         tol = _tol(engine)
         assert rel_l2(grad, ref) <= tol, (name, w, rel_l2(grad, ref))
+        assert elementwise_ratio(grad, ref, tol) <= 1.0, (name, w, elementwise_ratio(grad, ref, tol))
         for o, r in zip(losses, g["meta"]["worker_losses"][str(w)]):
             for k in ("pde", "ic", "bc"):
                 assert abs(o[k] - r[k]) <= LOSS_RTOL * abs(r[k]) + 1e-12, (name, w, k, o[k], r[k])
@@ -146,6 +153,7 @@ def test_config_shapes_vs_oracle(cfg, dims, workers, engine):
                                              engine=engine, **col)
     tol = _tol(engine)
     assert rel_l2(grad, ref) <= tol, rel_l2(grad, ref)
+    assert elementwise_ratio(grad, ref, tol) <= 1.0, elementwise_ratio(grad, ref, tol)
     for o, r in zip(losses, outs):
         for k in ("pde", "ic", "bc"):
             assert abs(o[k] - r[k]) <= LOSS_RTOL * abs(r[k]) + 1e-12
@@ -196,6 +204,7 @@ def test_bench_scale_gradient_vs_fp64_fixture(engine):
     err = rel_l2(g, ref)
     print(f"bench-size gradient rel-L2 ({engine}) vs FP64: {err:.3e}")
     assert err <= _tol(engine), err
+    assert elementwise_ratio(g, ref, _tol(engine)) <= 1.0, elementwise_ratio(g, ref, _tol(engine))
     for k, r in zip(("pde", "ic", "bc"), z["losses"]):
         assert abs(l[k] - r) <= LOSS_RTOL * abs(r) + 1e-12, (k, l[k], r)
 

@@ -762,13 +762,19 @@ void adam_update(double* p, double* m, double* v, const double* g, std::size_t n
         return;
     }
     std::vector<std::thread> pool;
-    pool.reserve(nt - 1);
     const std::size_t per = (n + nt - 1) / nt;
-    for (std::size_t i = 1; i < nt; ++i) {
+    auto range = [&](std::size_t i) {
         const std::size_t lo = std::min(n, i * per), hi = std::min(n, lo + per);
-        pool.emplace_back(adam_range, p, m, v, g, lo, hi, lr, a.beta1, a.beta2, a.eps, bc1, bc2);
+        adam_range(p, m, v, g, lo, hi, lr, a.beta1, a.beta2, a.eps, bc1, bc2);
+    };
+    std::size_t started = 1;
+    try {  // pinnlab_adam_step is a C entry point: ranges without a thread run here
+        pool.reserve(nt - 1);
+        for (; started < nt; ++started) pool.emplace_back(range, started);
+    } catch (...) {
     }
-    adam_range(p, m, v, g, 0, std::min(n, per), lr, a.beta1, a.beta2, a.eps, bc1, bc2);
+    range(0);
+    for (std::size_t i = started; i < nt; ++i) range(i);
     for (auto& th : pool) th.join();
 }
 

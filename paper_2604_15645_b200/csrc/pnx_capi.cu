@@ -269,8 +269,15 @@ static void host_par_for(int64_t n, F&& f) {
     }
     std::vector<std::thread> pool;
     const int64_t per = (n + nt - 1) / nt;
-    for (int i = 1; i < nt; ++i) pool.emplace_back([&, i] { f(std::min(n, i * per), std::min(n, (i + 1) * per)); });
-    f((int64_t)0, std::min(n, per));
+    auto range = [&](int i) { f(std::min(n, i * per), std::min(n, (i + 1) * per)); };
+    int started = 1;
+    try {  // no exception may cross the C ABI: ranges without a thread run here
+        pool.reserve((size_t)nt - 1);
+        for (; started < nt; ++started) pool.emplace_back(range, started);
+    } catch (...) {
+    }
+    range(0);
+    for (int i = started; i < nt; ++i) range(i);
     for (auto& t : pool) t.join();
 }
 

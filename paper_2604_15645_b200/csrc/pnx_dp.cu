@@ -296,7 +296,13 @@ int pnx_dp_create(const pnx_model_desc* m, const pnx_problem_desc* p, const int*
     }
     dp->rc.assign((size_t)dp->D, PNX_OK);
     dp->msg.assign((size_t)dp->D, std::string());
-    for (int d = 0; d < dp->D; ++d) dp->th.emplace_back(dp_thread, dp, d);
+    try {  // no exception may cross the C ABI
+        for (int d = 0; d < dp->D; ++d) dp->th.emplace_back(dp_thread, dp, d);
+    } catch (...) {
+        pnx::set_create_error("pnx_dp_create: cannot start the per-device host threads");
+        pnx_dp_destroy(dp);  // joins the threads that did start
+        return PNX_ERR_CUDA;
+    }
     *out = dp;
     return PNX_OK;
 }

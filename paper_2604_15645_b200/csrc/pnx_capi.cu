@@ -103,6 +103,9 @@ struct pnx_ctx {
     // graph capture): host-side writes to step inputs wait on it
     cudaEvent_t ev_done = nullptr;
     bool ev_pending = false;
+    // PNX_GUARD=1: every context buffer carries a tail of kGuardBytes set to
+    // kGuardByte, verified by pnx_check (a memcheck stand-in for out-of-bounds writes)
+    std::vector<std::pair<void*, size_t>> guards;  // (buffer, payload bytes)
     // pinned FP32 staging of the host-buffer step (pnx_step): params in, gradient out
     float* h_stage = nullptr;
     int64_t stage_cap = 0;
@@ -165,12 +168,63 @@ int fail(pnx_ctx* c, int code, const std::string& msg) {
             return fail(ctx, PNX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
     } while (0)
 
+constexpr size_t kGuardBytes = 512;
+constexpr int kGuardByte = 0xA5;
+inline bool guard_on() {
+    static const bool on = getenv("PNX_GUARD") && (getenv("PNX_GUARD")[0] == '1' || !strcmp(getenv("PNX_GUARD"), "poke"));
+    return on;
+}
+// PNX_GUARD=poke: the negative control -- one byte past the end of every buffer
+// is overwritten right after allocation, so the first check must report it
+inline bool guard_poke() {
+    static const bool on = getenv("PNX_GUARD") && !strcmp(getenv("PNX_GUARD"), "poke");
+    return on;
+}
+
+// a buffer leaves the guard list before it is freed / joins it (tail set) after allocation
+static void guard_forget(pnx_ctx* ctx, const void* p) {
+    for (size_t i = 0; i < ctx->guards.size(); ++i)
+        if (ctx->guards[i].first == p) {
+            ctx->guards.erase(ctx->guards.begin() + (std::ptrdiff_t)i);
+            return;
+        }
+}
+static int guard_add(pnx_ctx* ctx, void* p, size_t bytes) {
+    if (!guard_on() || !p) return PNX_OK;
+    guard_forget(ctx, p);
+    CK(cudaMemset(reinterpret_cast<uint8_t*>(p) + bytes, kGuardByte, kGuardBytes));
+    if (guard_poke()) CK(cudaMemset(reinterpret_cast<uint8_t*>(p) + bytes, 0, 1));
+    ctx->guards.emplace_back(p, bytes);
+    return PNX_OK;
+}
+
 template <class T>
 int dalloc(pnx_ctx* ctx, T** p, size_t n) {
-    if (*p) cudaFree(*p);
+    if (*p) {
+        guard_forget(ctx, *p);
+        cudaFree(*p);
+    }
     *p = nullptr;
     if (n == 0) return PNX_OK;
-    CK(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+    const size_t bytes = n * sizeof(T);
+    CK(cudaMalloc(reinterpret_cast<void**>(p), bytes + (guard_on() ? kGuardBytes : 0)));
+    return guard_add(ctx, *p, bytes);
+}
+
+// PNX_GUARD=1: every guard tail still holds its pattern (call after a device sync)
+static int guard_check(pnx_ctx* ctx) {
+    if (!guard_on()) return PNX_OK;
+    std::vector<uint8_t> h(kGuardBytes);
+    for (size_t i = 0; i < ctx->guards.size(); ++i) {
+        const auto& gd = ctx->guards[i];
+        CK(cudaMemcpy(h.data(), reinterpret_cast<const uint8_t*>(gd.first) + gd.second, kGuardBytes,
+                      cudaMemcpyDeviceToHost));
+        for (size_t k = 0; k < kGuardBytes; ++k)
+            if (h[k] != (uint8_t)kGuardByte)
+                return fail(ctx, PNX_ERR_CUDA,
+                            "guard: write past the end of a " + std::to_string(gd.second) + "-byte device buffer (byte " +
+                                std::to_string(k) + " of its guard)");
+    }
     return PNX_OK;
 }
 
@@ -389,7 +443,19 @@ int upload_rows(pnx_ctx* ctx) {
         for (int i = 0; i < 2; ++i)
             if (int r = dalloc(ctx, &ctx->d_Zb[i], SR * ctx->H)) return r;
         CK(cudaMemset(ctx->d_Hin, 0, SR * ctx->K0 * 4));
-        if (int r = tc_workspace_alloc(ctx->tc, (int)ctx->S, Rp, ctx->H, ctx->K0)) return fail(ctx, r, "tc workspace alloc");
+        {
+            const void* old[3] = {ctx->tc.red, ctx->tc.wpart, ctx->tc.dbpart};
+            if (int r = tc_workspace_alloc(ctx->tc, (int)ctx->S, Rp, ctx->H, ctx->K0, guard_on() ? kGuardBytes : 0))
+                return fail(ctx, r, "tc workspace alloc");
+            void* now[3] = {ctx->tc.red, ctx->tc.wpart, ctx->tc.dbpart};
+            const size_t bytes[3] = {(size_t)ctx->tc.red_cap * 8, (size_t)ctx->tc.wpart_cap * 4,
+                                     (size_t)ctx->tc.dbpart_cap * 8};
+            for (int i = 0; i < 3; ++i)
+                if (now[i] != old[i]) {
+                    guard_forget(ctx, old[i]);
+                    if (int r = guard_add(ctx, now[i], bytes[i])) return r;
+                }
+        }
     }
     // wgrad splits per layer (fill ~4 waves of 148 SMs)
     const int L = ctx->tab.n;
@@ -560,9 +626,13 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
             }
         }
         if (need > ctx->tc.img_cap) {
-            if (ctx->tc.img) cudaFree(ctx->tc.img);
+            if (ctx->tc.img) {
+                guard_forget(ctx, ctx->tc.img);
+                cudaFree(ctx->tc.img);
+            }
             ctx->tc.img = nullptr;
-            CK(cudaMalloc(&ctx->tc.img, need * sizeof(float)));
+            CK(cudaMalloc(&ctx->tc.img, need * sizeof(float) + (guard_on() ? kGuardBytes : 0)));
+            if (int r = guard_add(ctx, ctx->tc.img, (size_t)need * sizeof(float))) return r;
             ctx->tc.img_cap = need;
         }
         // AUTO: 3xFP16 wherever the kernels support it, 3xTF32 elsewhere
@@ -1416,6 +1486,7 @@ int pnx_check(pnx_ctx* ctx) {
     int bad[5];
     CK(cudaDeviceSynchronize());  // Adam may run on another stream than the step
     CK(cudaMemcpy(bad, ctx->d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+    if (int r = guard_check(ctx)) return r;
     return report_bad(ctx, bad);
 }
 
@@ -1465,6 +1536,7 @@ int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double
     CK(cudaMemcpyAsync(hl, ctx->d_losses, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(hbad, ctx->d_bad, 5 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (int r = guard_check(ctx)) return r;
     if (int r = report_bad(ctx, hbad)) return r;
     const double losses[3] = {hl[0], hl[1], hl[2]};
     for (int t = 0; t < 3; ++t)

@@ -321,13 +321,14 @@ inline bool tc_enabled(int engine, int H, int S, int act) {
     return (H == 128 || H == 256) && S <= 5 && act == ACT_TANH;
 }
 
-inline int tc_workspace_alloc(TcWorkspace& ws, int, int64_t Rpad, int H, int K0) {
+// extra_bytes: allocated past every buffer (the context's PNX_GUARD tails)
+inline int tc_workspace_alloc(TcWorkspace& ws, int, int64_t Rpad, int H, int K0, size_t extra_bytes = 0) {
     {
         const int64_t kmax0 = H > K0 ? H : K0;
         const int64_t need_red = (int64_t)TC_WRED_G * (kmax0 * H + H);
         if (need_red > ws.red_cap) {
             if (ws.red) cudaFree(ws.red);
-            if (cudaMalloc(&ws.red, need_red * sizeof(double)) != cudaSuccess) return -2;
+            if (cudaMalloc(&ws.red, need_red * sizeof(double) + extra_bytes) != cudaSuccess) return -2;
             ws.red_cap = need_red;
         }
     }
@@ -337,12 +338,12 @@ inline int tc_workspace_alloc(TcWorkspace& ws, int, int64_t Rpad, int H, int K0)
     const int64_t need = tiles * kmax * H;
     if (need > ws.wpart_cap) {
         if (ws.wpart) cudaFree(ws.wpart);
-        if (cudaMalloc(&ws.wpart, need * sizeof(float)) != cudaSuccess) return -2;
+        if (cudaMalloc(&ws.wpart, need * sizeof(float) + extra_bytes) != cudaSuccess) return -2;
         ws.wpart_cap = need;
     }
     if (tiles * H > ws.dbpart_cap) {
         if (ws.dbpart) cudaFree(ws.dbpart);
-        if (cudaMalloc(&ws.dbpart, tiles * H * sizeof(double)) != cudaSuccess) return -2;
+        if (cudaMalloc(&ws.dbpart, tiles * H * sizeof(double) + extra_bytes) != cudaSuccess) return -2;
         ws.dbpart_cap = tiles * H;
     }
     return 0;

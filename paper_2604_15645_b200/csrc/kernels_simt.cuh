@@ -1109,13 +1109,41 @@ struct FinalArgs {
 };
 
 // reduce splits of layer l into dWscratch (double)
-static __global__ void k_reduce_splits(const double* __restrict__ part, int nsplit, int64_t len,
-                                double* __restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * len + i];
-        out[i] = s;
+// out[i] = sum_p part[p][i] in a fixed order: a 32 x 8 block takes 32 consecutive
+// entries; thread row y sums the splits p = y, y + 8, ... into four interleaved
+// partials (loads in flight), the rows are folded in order y = 0..7. Many
+// splits of a short vector (the head's per-block partials) and few splits of a
+// long one both keep every SM busy.
+constexpr int kRsX = 32, kRsY = 8;
+static __global__ void __launch_bounds__(kRsX* kRsY) k_reduce_splits(const double* __restrict__ part, int nsplit,
+                                                                   int64_t len, double* __restrict__ out) {
+    __shared__ double acc[kRsY][kRsX];
+    const int x = threadIdx.x % kRsX, y = threadIdx.x / kRsX;
+    for (int64_t i0 = (int64_t)blockIdx.x * kRsX; i0 < len; i0 += (int64_t)gridDim.x * kRsX) {
+        const int64_t i = i0 + x;
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        if (i < len) {
+            int p = y;
+            for (; p + 3 * kRsY < nsplit; p += 4 * kRsY) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) s[u] += part[(int64_t)(p + u * kRsY) * len + i];
+            }
+            for (int u = 0; p < nsplit; p += kRsY, ++u) s[u] += part[(int64_t)p * len + i];
+        }
+        acc[y][x] = (s[0] + s[1]) + (s[2] + s[3]);
+        __syncthreads();
+        if (y == 0 && i < len) {
+            double t = acc[0][x];
+#pragma unroll
+            for (int r = 1; r < kRsY; ++r) t += acc[r][x];
+            out[i] = t;
+        }
+        __syncthreads();
     }
+}
+inline unsigned reduce_splits_grid(int64_t len) {
+    const int64_t b = (len + kRsX - 1) / kRsX;
+    return (unsigned)(b < 4096 ? b : 4096);
 }
 
 // write layer l's flat grads from the reduced dW (K*N) + db (N)
@@ -1133,12 +1161,21 @@ static __global__ void k_write_layer_grad(const double* __restrict__ red, const 
         } else {
             const int n = (int)(i - total);
             grad[offB + n] = (float)(red[total + n] * scale);
-            if (offS >= 0) {  // ds_n = exp(s_n) * sum_k dW[k][n] * V[k][n]
-                double acc = 0.0;
-                for (int k = 0; k < K; ++k) acc += red[(int64_t)k * N + n] * (double)params[offW + (int64_t)k * N + n];
-                grad[offS + n] = (float)(exp((double)params[offS + n]) * acc * scale);
-            }
         }
+    }
+}
+
+// RWF scale gradient ds_n = exp(s_n) * sum_k dW[k][n] V[k][n] (model.cpp:117-126):
+// one warp per n, lanes stride k, a fixed shuffle tree
+static __global__ void k_write_rwf_ds(const double* __restrict__ red, const float* __restrict__ params, int K, int N,
+                                      int64_t offW, int64_t offS, float scale, float* __restrict__ grad) {
+    const int lane = threadIdx.x & 31;
+    for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += gridDim.x * (blockDim.x >> 5)) {
+        double acc = 0.0;
+        for (int k = lane; k < K; k += 32) acc += red[(int64_t)k * N + n] * (double)params[offW + (int64_t)k * N + n];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) grad[offS + n] = (float)(exp((double)params[offS + n]) * acc * scale);
     }
 }
 

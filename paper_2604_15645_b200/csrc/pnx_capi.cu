@@ -941,11 +941,16 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
         const double* part = l < Lw - 1 ? ctx->d_part[l] : ctx->d_head_part;
         const int ns = l < Lw - 1 ? ctx->nsplit[l] : ctx->head_grid;
         const int64_t len = (int64_t)t.K[l] * t.N[l] + t.N[l];
-        k_reduce_splits<<<(unsigned)std::min<int64_t>((len + 255) / 256, 1024), 256, 0, st>>>(part, ns, len, ctx->d_red);
+        k_reduce_splits<<<reduce_splits_grid(len), kRsX * kRsY, 0, st>>>(part, ns, len, ctx->d_red);
         CKL();
         k_write_layer_grad<<<(unsigned)std::min<int64_t>((len + 255) / 256, 1024), 256, 0, st>>>(
             ctx->d_red, d_params, t.K[l], t.N[l], t.offW[l], t.offS[l], t.offB[l], 1.0f, d_grad);
         CKL();
+        if (t.offS[l] >= 0) {
+            k_write_rwf_ds<<<(unsigned)((t.N[l] + 7) / 8), 256, 0, st>>>(ctx->d_red, d_params, t.K[l], t.N[l], t.offW[l],
+                                                                       t.offS[l], 1.0f, d_grad);
+            CKL();
+        }
     }
     {
         // 1/n per term and the period offsets live in d_losses[3..] (uploaded with the

@@ -1233,23 +1233,28 @@ static __global__ void k_write_scalar_grads(const double* __restrict__ partP, in
                                      const double* __restrict__ loss_part, int nloss_blk,
                                      const double* inv_n, double* __restrict__ losses_out,
                                      const double* __restrict__ pde_override = nullptr) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        for (int ax = 0; ax < naxes; ++ax) {
-            if (offs[ax] < 0) continue;
-            double s = 0.0;
-            for (int b = 0; b < nblk; ++b) s += partP[b * kMaxAxes + ax];
-            grad[offs[ax]] = (float)(s * scale);
-        }
-        if (losses_out) {
-            for (int t = 0; t < 3; ++t) {
-                double s = 0.0;
-                for (int b = 0; b < nloss_blk; ++b) s += loss_part[b * 3 + t];
-                losses_out[t] = s * inv_n[t];
-            }
-            if (pde_override) losses_out[0] = *pde_override;
-        }
+    // one warp per sum (warps 0-2: the loss terms, 3..: the period axes): lanes
+    // stride the blocks, then a fixed shuffle tree (launched with 32 * (3 + kMaxAxes) threads)
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (blockIdx.x != 0) return;
+    if (w < 3) {
+        if (!losses_out) return;
+        double s = 0.0;
+        for (int b = lane; b < nloss_blk; b += 32) s += loss_part[b * 3 + w];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) losses_out[w] = (w == 0 && pde_override) ? *pde_override : s * inv_n[w];
+    } else if (w - 3 < naxes) {
+        const int ax = w - 3;
+        if (offs[ax] < 0) return;
+        double s = 0.0;
+        for (int b = lane; b < nblk; b += 32) s += partP[b * kMaxAxes + ax];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) grad[offs[ax]] = (float)(s * scale);
     }
 }
+constexpr int kScalarGradThreads = 32 * (3 + kMaxAxes);
 
 // ---------------------------------------------------------------------------
 // Adam (optim.cpp:7-41) fused with the 1/W average (trainer.cpp:278-280)

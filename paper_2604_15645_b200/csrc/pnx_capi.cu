@@ -955,7 +955,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
     {
         // 1/n per term and the period offsets live in d_losses[3..] (uploaded with the
         // rows, so the step itself enqueues kernels and memsets only: graph-capturable)
-        k_write_scalar_grads<<<1, 32, 0, st>>>(ctx->d_partP, ctx->ibwd_grid,
+        k_write_scalar_grads<<<1, kScalarGradThreads, 0, st>>>(ctx->d_partP, ctx->ibwd_grid,
                                                reinterpret_cast<const int64_t*>(ctx->d_losses + 8), ctx->in_dim,
                                                1.0f, d_grad, ctx->d_loss_part, ctx->head_grid, ctx->d_losses + 3,
                                                d_losses ? d_losses : ctx->d_losses,

@@ -136,6 +136,64 @@ __device__ __forceinline__ void embed_row(const InputArgs& a, int64_t g, double 
     }
 }
 
+// m[s] = sum_k e[s][k] B[k][col] for one row without materialising e (a local
+// array indexed by the runtime embedding layout lived in local memory): the
+// same terms in the same order as embed_row followed by the dot product
+template <int L>
+__device__ __forceinline__ void embed_dot(const InputArgs& a, int64_t g, int col, double (&m)[Streams<L>::S]) {
+    using St = Streams<L>;
+    constexpr int S = St::S;
+#pragma unroll
+    for (int s = 0; s < S; ++s) m[s] = 0.0;
+    int k = 0;
+#pragma unroll
+    for (int ax = 0; ax < kMaxAxes; ++ax) {
+        if (ax >= a.in_dim) break;
+        const double x = a.coords[(int64_t)ax * a.ld + g];
+        if (!a.periodic[ax]) {
+            const double b = a.rffB[(int64_t)k * a.rff_w + col];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const double e = (s == 0) ? x : ((St::order(s) == 1 && St::axis(s) == ax) ? 1.0 : 0.0);
+                m[s] += e * b;
+            }
+            k += 1;
+            continue;
+        }
+        double kappa, phi;
+        if (a.period_off[ax] >= 0) {  // as embed_row (model.cpp:144-149)
+            const double P = (double)a.params[a.period_off[ax]];
+            kappa = 2.0 * CUDART_PI * (1.0 / P);
+            phi = 2.0 * CUDART_PI * (x * (1.0 / P));
+        } else {
+            kappa = 2.0 * CUDART_PI / a.period[ax];
+            phi = x * kappa;
+        }
+        double sp, cp;
+        sincos(phi, &sp, &cp);
+        const double b0 = a.rffB[(int64_t)k * a.rff_w + col], b1 = a.rffB[(int64_t)(k + 1) * a.rff_w + col];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            double C = 0.0, Sn = 0.0;
+            if (s == 0) {
+                C = cp;
+                Sn = sp;
+            } else if (St::axis(s) == ax) {
+                if (St::order(s) == 1) {
+                    C = -sp * kappa;
+                    Sn = cp * kappa;
+                } else {
+                    C = -cp * kappa * kappa;
+                    Sn = -sp * kappa * kappa;
+                }
+            }
+            m[s] += C * b0;
+            m[s] += Sn * b1;
+        }
+        k += 2;
+    }
+}
+
 template <int L>
 static __global__ void k_input(InputArgs a) {
     using St = Streams<L>;
@@ -160,9 +218,9 @@ static __global__ void k_input(InputArgs a) {
             }
             continue;
         }
-        double e[S][2 * kMaxAxes];
-        embed_row<L>(a, a.row0 + r, e);
         if (a.rff_w == 0) {
+            double e[S][2 * kMaxAxes];
+            embed_row<L>(a, a.row0 + r, e);
 #pragma unroll
             for (int s = 0; s < S; ++s)
                 for (int k = 0; k < a.E; ++k) out[s * RK + k] = (float)e[s][k];
@@ -170,12 +228,7 @@ static __global__ void k_input(InputArgs a) {
         }
         // m = e B  (B frozen, float64), then [cos m, sin m] jets
         double m[S];
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            double acc = 0.0;
-            for (int k = 0; k < a.E; ++k) acc += e[s][k] * a.rffB[(int64_t)k * a.rff_w + c];
-            m[s] = acc;
-        }
+        embed_dot<L>(a, a.row0 + r, c, m);
         double sm, cm;
         sincos(m[0], &sm, &cm);
 #pragma unroll

@@ -86,6 +86,7 @@ struct InputArgs {
     const double* rffB;     // [E][rff_w]
     int K0;                 // feature width written (E or 2*rff_w)
     float* Hin;             // [S][Rpad][K0]
+    unsigned* amax_out;     // k_input: per-stream max |Hin| (float bits, atomicMax), or null
 };
 
 // embedding jets e[s][c] (c < E) for one row, float64
@@ -198,6 +199,10 @@ template <int L>
 static __global__ void k_input(InputArgs a) {
     using St = Streams<L>;
     constexpr int S = St::S;
+    // per-stream bounds of the written features (3xFP16 operand scales of layer 0)
+    float mx[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) mx[s] = 0.0f;
     const int per_row = a.rff_w > 0 ? a.rff_w : 1;
     const int64_t total = (int64_t)a.Rpad * per_row;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -223,7 +228,10 @@ static __global__ void k_input(InputArgs a) {
             embed_row<L>(a, a.row0 + r, e);
 #pragma unroll
             for (int s = 0; s < S; ++s)
-                for (int k = 0; k < a.E; ++k) out[s * RK + k] = (float)e[s][k];
+                for (int k = 0; k < a.E; ++k) {
+                    out[s * RK + k] = (float)e[s][k];
+                    mx[s] = fmaxf(mx[s], fabsf((float)e[s][k]));
+                }
             continue;
         }
         // m = e B  (B frozen, float64), then [cos m, sin m] jets
@@ -247,6 +255,22 @@ static __global__ void k_input(InputArgs a) {
             }
             out[s * RK + c] = (float)C;
             out[s * RK + a.rff_w + c] = (float)Sn;
+            mx[s] = fmaxf(mx[s], fmaxf(fabsf((float)C), fabsf((float)Sn)));
+        }
+    }
+    if (a.amax_out) {  // warp, then block maxima: one atomic per block and stream
+        __shared__ unsigned bm[32][S];
+        const int w = threadIdx.x >> 5;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const unsigned v = __reduce_max_sync(0xffffffffu, __float_as_uint(mx[s]));
+            if ((threadIdx.x & 31) == 0) bm[w][s] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < S) {
+            unsigned v = 0;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) v = max(v, bm[k][threadIdx.x]);
+            atomicMax(a.amax_out + threadIdx.x, v);
         }
     }
 }

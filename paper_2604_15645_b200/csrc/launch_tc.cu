@@ -166,10 +166,13 @@ int launch_tc2_fwd_l(int pro, const TcGemmArgs& g, cudaStream_t st) {
         return pro == ACT_NONE ? launch_tc4_fwd_t<L, ACT_NONE, false>(g, st)
                                : launch_tc4_fwd_t<L, ACT_TANH, false>(g, st);
     }
-    if (g.f16) {  // 3xFP16 single-CTA forward (tanh inputs: the producer records their bounds)
-        if (pro == ACT_NONE) return -1;
-        if (g.N == 256) return launch_tc2_fwd_t<L, ACT_TANH, 256, true>(g, st);
-        if (g.N == 128) return launch_tc2_fwd_t<L, ACT_TANH, 128, true>(g, st);
+    if (g.f16) {  // 3xFP16 single-CTA forward (the producer -- a layer or k_input -- recorded the bounds)
+        if (g.N == 256)
+            return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 256, true>(g, st)
+                                   : launch_tc2_fwd_t<L, ACT_TANH, 256, true>(g, st);
+        if (g.N == 128)
+            return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 128, true>(g, st)
+                                   : launch_tc2_fwd_t<L, ACT_TANH, 128, true>(g, st);
         return -1;
     }
     if (g.N == 256) return pro == ACT_NONE ? launch_tc2_fwd_t<L, ACT_NONE, 256>(g, st) : launch_tc2_fwd_t<L, ACT_TANH, 256>(g, st);

@@ -285,10 +285,12 @@ int pde_layout(int pde) {
 constexpr int kL0Blocks = 296;
 // layer 0 fused with the input jets (narrow embedding: no RFF, K0 <= 8, H % 4 == 0)
 constexpr int kAmaxS = 8;
-constexpr int kAmaxLen = kMaxLayers * (1 + 2 * kAmaxS);
+constexpr int kAmaxLen = kMaxLayers * (1 + 2 * kAmaxS) + kAmaxS;
 inline unsigned* amax_w(pnx_ctx* c, int l) { return c->d_amax + l; }
 inline unsigned* amax_z(pnx_ctx* c, int l) { return c->d_amax + kMaxLayers + l * kAmaxS; }
 inline unsigned* amax_zb(pnx_ctx* c, int l) { return c->d_amax + kMaxLayers * (1 + kAmaxS) + l * kAmaxS; }
+// bounds of the unfused input features Hin (k_input: RFF or a wide embedding)
+inline unsigned* amax_hin(pnx_ctx* c) { return c->d_amax + kMaxLayers * (1 + 2 * kAmaxS); }
 bool layer0_fused(const pnx_ctx* c) { return c->rff_w == 0 && c->K0 <= 8 && c->H % 4 == 0 && c->H <= 512; }
 
 int64_t bytes_per_row(const pnx_ctx* c) {
@@ -602,6 +604,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
     ia.rffB = ctx->d_rffB;
     ia.K0 = ctx->K0;
     ia.Hin = ctx->d_Hin;
+    ia.amax_out = amax_hin(ctx);
 
     const bool tc_on = tc_enabled(ctx->engine, ctx->H, S, act);
     bool tc_fwd[kMaxLayers] = {}, tc_bwd[kMaxLayers] = {}, tc_wg[kMaxLayers] = {};
@@ -651,6 +654,9 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 f16_wg[l] = f16 && tc_wg[l] && rec && recb;  // A = Z_{l-1}, B = Zb_l
                 rec = tc_fwd[l] && (tc_mask & 1);
             } else if (!layer0_fused(ctx)) {
+                // k_input records the bounds of the features it writes (RFF / wide embedding)
+                f16_fwd[0] = f16 && tc_fwd[0] && (tc_mask & 1);
+                f16_wg[0] = f16 && tc_wg[0] && recb;
                 rec = tc_fwd[0] && (tc_mask & 1);  // the tcgen05 layer 0 records Z_0 bounds too
             }
             // the general (all streams in TMEM) backward gains from 3xFP16 only up to four
@@ -717,7 +723,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 tg.K = g.K;
                 tg.N = g.N;
                 tg.f16 = f16_fwd[l] ? 1 : 0;
-                tg.amax_in = l > 0 ? amax_z(ctx, l - 1) : nullptr;
+                tg.amax_in = l > 0 ? amax_z(ctx, l - 1) : amax_hin(ctx);
                 tg.amax_w = amax_w(ctx, l);
                 tg.amax_out = amax_z(ctx, l);
                 if (launch_tc2_fwd(L, pro, tg, st)) return fail(ctx, PNX_ERR_CUDA, "tc forward launch");
@@ -871,7 +877,7 @@ int run_step(pnx_ctx* ctx, const float* d_params, const double lam[3], float* d_
                 tw.Kin = t.K[l];
                 tw.N = t.N[l];
                 tw.f16 = f16_wg[l] ? 1 : 0;
-                tw.amaxA = l > 0 ? amax_z(ctx, l - 1) : nullptr;
+                tw.amaxA = l > 0 ? amax_z(ctx, l - 1) : amax_hin(ctx);
                 tw.amaxB = amax_zb(ctx, l);
                 const int ntl = std::min(tc_wgrad_groups(Rpad, t.K[l], ctx->nsm), TC_WG_MAX_GROUPS);
                 const int wr = tc_wgrad_seg();

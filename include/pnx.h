@@ -90,7 +90,9 @@ const char* pnx_create_error(void);
 int pnx_param_count(const pnx_ctx* ctx, int64_t* n);
 
 /* Interior collocation shard (WorkerTask::interior, trainer.cpp:192), axis-major
- * float64 [n_axes][n] (Points::coords, losses.hpp:39-43; space first, time last). */
+ * float64 [n_axes][n] (Points::coords, losses.hpp:39-43; space first, time last).
+ * The caller's buffer is copied before the call returns (the copy waits for the
+ * last enqueued step that reads the points); pinned buffers are copied by DMA. */
 int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes);
 /* Interior points generated on the device instead (sampling.cpp:10-103): design
  * mode 0 = uniform tensor grid of linspace axes, last axis fastest
@@ -158,6 +160,11 @@ int pnx_last_penalty(pnx_ctx* ctx, double* pen);
  * non-finite check is deferred: call pnx_check(ctx) after synchronizing. */
 int pnx_step_device(pnx_ctx* ctx, const float* d_params, const double lambdas[3], float* d_grad,
                     double* d_losses, void* stream);
+/* Synchronizes the device and reports the sticky non-finite flags (residual
+ * point index, Adam gradient entry and step); with the environment variable
+ * PNX_GUARD=1 set at load time it also verifies the 512-byte guard tail of
+ * every context buffer ("guard: write past the end ..."), a debug stand-in for
+ * a memory checker. */
 int pnx_check(pnx_ctx* ctx);
 
 /* Device Adam (optim.cpp:7-41) with ExponentialLr lr = base*gamma^epoch

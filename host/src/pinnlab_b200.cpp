@@ -754,8 +754,8 @@ void adam_update(double* p, double* m, double* v, const double* g, std::size_t n
     const double bc2 = 1.0 - std::pow(a.beta2, static_cast<double>(t));
     // elementwise and divide/sqrt-bound: large vectors split over host threads
     // (each element is computed exactly as in the serial loop)
-    const std::size_t kMinPerThread = 32768;
-    std::size_t nt = std::min<std::size_t>(std::max(1u, std::thread::hardware_concurrency()), 16);
+    const std::size_t kMinPerThread = 16384;
+    std::size_t nt = std::min<std::size_t>(std::max(1u, std::thread::hardware_concurrency()), 8);
     nt = std::max<std::size_t>(1, std::min(nt, n / kMinPerThread));
     if (nt <= 1) {
         adam_range(p, m, v, g, 0, n, lr, a.beta1, a.beta2, a.eps, bc1, bc2);

@@ -106,6 +106,12 @@ struct pnx_ctx {
     // PNX_GUARD=1: every context buffer carries a tail of kGuardBytes set to
     // kGuardByte, verified by pnx_check (a memcheck stand-in for out-of-bounds writes)
     std::vector<std::pair<void*, size_t>> guards;  // (buffer, payload bytes)
+    // pnx_step's CUDA graph: every call that can change what a step enqueues bumps
+    // state_ver; the first step after a change runs eagerly (uploads, allocations),
+    // the second captures the device step, later ones replay it (same lambdas)
+    uint64_t state_ver = 1, g_ver = 0, g_warm_ver = 0;
+    double g_lam[3] = {0, 0, 0}, g_warm_lam[3] = {0, 0, 0};
+    cudaGraphExec_t g_exec = nullptr;
     // pinned FP32 staging of the host-buffer step (pnx_step): params in, gradient out
     float* h_stage = nullptr;
     int64_t stage_cap = 0;
@@ -1225,6 +1231,7 @@ void pnx_destroy(pnx_ctx* ctx) {
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    if (ctx->g_exec) cudaGraphExecDestroy(ctx->g_exec);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1255,6 +1262,7 @@ int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes
         ctx->h_int_stale = true;
         return causality_counts(ctx, coords + (int64_t)(n_axes - 1) * n, n);
     }
+    ++ctx->state_ver;  // new row layout (the same-size path above only rewrites device memory)
     ctx->h_int.assign(coords, coords + n * n_axes);
     ctx->h_int_stale = false;
     ctx->int_on_device = false;
@@ -1270,6 +1278,7 @@ int pnx_set_points(pnx_ctx* ctx, const double* coords, int64_t n, int32_t n_axes
 int pnx_sample_points(pnx_ctx* ctx, int32_t mode, const double* bounds, const int64_t* dims, int64_t n_total,
                       uint64_t seed, int64_t row_lo, int64_t row_hi) {
     if (!ctx || !bounds) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     const int d = ctx->in_dim;
     SampleArgs a{};
     a.mode = mode;
@@ -1319,6 +1328,7 @@ int pnx_sample_points(pnx_ctx* ctx, int32_t mode, const double* bounds, const in
 
 int pnx_set_causality(pnx_ctx* ctx, int32_t segments, double epsilon, double t_lo, double t_hi) {
     if (!ctx) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     CK(cudaSetDevice(ctx->device));
     if (segments <= 0) {
         ctx->caus_M = 0;
@@ -1353,6 +1363,7 @@ int pnx_set_causality(pnx_ctx* ctx, int32_t segments, double epsilon, double t_l
 
 int pnx_set_poynting(pnx_ctx* ctx, double weight, int32_t grid, int32_t time_samples, const double box[6]) {
     if (!ctx) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     CK(cudaSetDevice(ctx->device));
     if (weight == 0.0 || ctx->pde != PNX_PDE_MAXWELL_TE) {  // trainer.cpp:240: maxwell_te only
         if (ctx->n_poy) ctx->rows_dirty = true;
@@ -1406,6 +1417,7 @@ int pnx_last_penalty(pnx_ctx* ctx, double* pen) {
 
 int pnx_set_ic(pnx_ctx* ctx, const double* coords, const double* targets, int64_t n) {
     if (!ctx) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     if (n < 0 || (n > 0 && (!coords || !targets))) return fail(ctx, PNX_ERR_ARG, "ic_loss: empty point set");
     ctx->h_ic.assign(coords, coords + n * ctx->in_dim);
     ctx->h_ic_t.resize((size_t)(n * ctx->F));
@@ -1417,6 +1429,7 @@ int pnx_set_ic(pnx_ctx* ctx, const double* coords, const double* targets, int64_
 
 int pnx_set_bc(pnx_ctx* ctx, const double* a, const double* b, const double* targets, int64_t n) {
     if (!ctx) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     if (ctx->bc == PNX_BC_HARD) {
         if (n != 0) return fail(ctx, PNX_ERR_ARG, "pnx_set_bc: problem has hard (architectural) BC");
         return PNX_OK;
@@ -1442,12 +1455,14 @@ int pnx_set_bc(pnx_ctx* ctx, const double* a, const double* b, const double* tar
 
 int pnx_set_engine(pnx_ctx* ctx, int engine) {
     if (!ctx || engine < 0 || engine > 3) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     ctx->engine = engine;
     return PNX_OK;
 }
 
 int pnx_set_chunk_rows(pnx_ctx* ctx, int64_t rows) {
     if (!ctx || rows < 0) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     ctx->chunk_override = rows;
     ctx->rows_dirty = true;
     return PNX_OK;
@@ -1455,6 +1470,7 @@ int pnx_set_chunk_rows(pnx_ctx* ctx, int64_t rows) {
 
 int pnx_profile(pnx_ctx* ctx, int on) {
     if (!ctx) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     ctx->prof = on != 0;
     prof_collect(ctx);
     for (int i = 0; i < 8; ++i) {
@@ -1484,8 +1500,47 @@ int pnx_last_launch_count(const pnx_ctx* ctx, int64_t* n) {
 int pnx_step_device(pnx_ctx* ctx, const float* d_params, const double lambdas[3], float* d_grad,
                     double* d_losses, void* stream) {
     if (!ctx || !d_params || !d_grad || !lambdas) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     CK(cudaSetDevice(ctx->device));
     return run_step(ctx, d_params, lambdas, d_grad, d_losses, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// pnx_step's device step through the context's CUDA graph (PNX_STEP_GRAPH=0: eager)
+static int step_graphed(pnx_ctx* ctx, const double lam[3]) {
+    static const bool off = getenv("PNX_STEP_GRAPH") && getenv("PNX_STEP_GRAPH")[0] == '0';
+    const bool graphable = !off && !ctx->reuse_fwd && !ctx->no_penalty && !ctx->capture_resid && !ctx->prof;
+    auto same = [&](const double* a) { return a[0] == lam[0] && a[1] == lam[1] && a[2] == lam[2]; };
+    if (graphable && ctx->g_exec && ctx->g_ver == ctx->state_ver && same(ctx->g_lam)) {
+        CK(cudaGraphLaunch(ctx->g_exec, ctx->stream));
+    } else if (graphable && ctx->g_warm_ver == ctx->state_ver && same(ctx->g_warm_lam)) {
+        if (ctx->g_exec) cudaGraphExecDestroy(ctx->g_exec);
+        ctx->g_exec = nullptr;
+        ctx->g_ver = 0;
+        cudaGraph_t gr = nullptr;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        const int r = run_step(ctx, ctx->d_params, lam, ctx->d_grad, ctx->d_losses, ctx->stream);
+        const cudaError_t e = cudaStreamEndCapture(ctx->stream, &gr);
+        if (r != PNX_OK) {
+            if (gr) cudaGraphDestroy(gr);
+            return r;
+        }
+        CK(e);
+        const cudaError_t ei = cudaGraphInstantiate(&ctx->g_exec, gr, 0);
+        cudaGraphDestroy(gr);
+        CK(ei);
+        ctx->g_ver = ctx->state_ver;
+        for (int k = 0; k < 3; ++k) ctx->g_lam[k] = lam[k];
+        CK(cudaGraphLaunch(ctx->g_exec, ctx->stream));
+    } else {
+        if (int r = run_step(ctx, ctx->d_params, lam, ctx->d_grad, ctx->d_losses, ctx->stream)) return r;
+        ctx->g_warm_ver = ctx->state_ver;
+        for (int k = 0; k < 3; ++k) ctx->g_warm_lam[k] = lam[k];
+        return PNX_OK;
+    }
+    // a replayed step is ordered for later host writes like an eager one
+    CK(cudaEventRecord(ctx->ev_done, ctx->stream));
+    ctx->ev_pending = true;
+    return PNX_OK;
 }
 
 static int report_bad(pnx_ctx* ctx, const int* bad);
@@ -1540,7 +1595,7 @@ int pnx_step(pnx_ctx* ctx, const double* params, const double lambdas[3], double
         for (int64_t i = lo; i < hi; ++i) p32[i] = (float)params[i];
     });
     CK(cudaMemcpyAsync(ctx->d_params, p32, (size_t)P * 4, cudaMemcpyHostToDevice, ctx->stream));
-    if (int r = run_step(ctx, ctx->d_params, lambdas, ctx->d_grad, ctx->d_losses, ctx->stream)) return r;
+    if (int r = step_graphed(ctx, lambdas)) return r;
     // gradient, losses and the sticky non-finite flags (written by this step's
     // kernels on ctx->stream) in one pinned read-back, one synchronisation
     CK(cudaMemcpyAsync(g32, ctx->d_grad, (size_t)P * 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1590,6 +1645,7 @@ int pnx_step_terms(pnx_ctx* ctx, const double* params, double* grad_terms_out, d
 
 int pnx_step_terms_device(pnx_ctx* ctx, const float* d_params, float* d_grads, double* d_losses, void* stream) {
     if (!ctx || !d_params || !d_grads) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     CK(cudaSetDevice(ctx->device));
     ctx->no_penalty = true;
     int r = PNX_OK;
@@ -1643,6 +1699,7 @@ int pnx_adam_step_device(pnx_ctx* ctx, float* d_params, const float* d_grad, flo
 // the last pnx_step, component-major [K][n_int] float64.
 int pnx_capture_residuals(pnx_ctx* ctx, int on) {
     if (!ctx) return PNX_ERR_ARG;
+    ++ctx->state_ver;
     ctx->capture_resid = on != 0;
     return PNX_OK;
 }

@@ -64,6 +64,10 @@ def _fixed():
         dict(base, pde="maxwell_te", width=128, depth=3, act="tanh", bc="soft_periodic", n=390, seed=17, engine="tc3xtf32"),
         dict(base, pde="advection", width=256, depth=1, act="tanh", bc="hard", n=257, seed=18, periodic=True,
              trainable=True),
+        dict(base, pde="maxwell_te", width=512, depth=2, act="tanh", bc="hard", n=300, seed=19),  # beyond the tc widths
+        dict(base, pde="burgers", width=384, depth=1, act="sine", bc="dirichlet_zero", n=200, seed=20),
+        dict(base, pde="allen_cahn", width=1, depth=1, act="tanh", bc="hard", n=50, seed=21),
+        dict(base, pde="burgers", width=64, depth=6, act="tanh", bc="soft_periodic", n=513, seed=22),  # deep narrow
     ]
     return out
 

@@ -55,12 +55,51 @@ struct SmallArgs {
     int64_t P;
 };
 
+// width 64: the hidden-layer contractions run as 3xTF32 warp MMAs
+// (mma.sync m16n8k8: the FFMA loops were shared-memory-bandwidth bound --
+// l1tex 73% busy -- and a fragment moves the same operands in 2.3x fewer
+// shared-memory wavefronts); the weights then sit at a row stride of HP + 8
+// (conflict-free B fragments of the forward)
+__host__ __device__ constexpr bool sn_mma(int HP) { return HP == 64; }
+__host__ __device__ constexpr int sn_ws(int HP) { return sn_mma(HP) ? HP + 8 : HP; }
+
 // shared-memory footprint (floats) of a configuration
 __host__ __device__ inline int64_t sn_smem_floats(int HP, int S, int D) {
-    const int J = S * SN_TR, LD = HP + 4;
-    const int64_t w = (int64_t)SN_MAXK0 * HP + (int64_t)(D - 1) * HP * HP + (int64_t)HP * 4 + (int64_t)D * HP + 4;
+    const int J = S * SN_TR, LD = HP + 4, WS = sn_ws(HP);
+    const int64_t w = (int64_t)SN_MAXK0 * WS + (int64_t)(D - 1) * HP * WS + (int64_t)HP * 4 + (int64_t)D * HP + 4;
     return w + (int64_t)J * SN_MAXK0 + (int64_t)(D + 2) * J * LD + (int64_t)SN_TR * S * 4;
 }
+
+namespace sn {
+// hi = x with the 13 low mantissa bits cleared (exact in TF32), lo = x - hi
+// (exact in FP32); the tensor core reads lo's TF32 part, so |x - hi - lo'| is
+// within 2^-21 |x| -- two integer/FP ops instead of two conversions
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+    const uint32_t h = __float_as_uint(x) & 0xffffe000u;
+    hi = h;
+    lo = __float_as_uint(x - __uint_as_float(h));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+// 3xTF32: c += al bh + ah bl + ah bh
+__device__ __forceinline__ void mma3(float (&c)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4],
+                                     const uint32_t (&bh)[2], const uint32_t (&bl)[2]) {
+    mma_tf32(c, al, bh);
+    mma_tf32(c, ah, bl);
+    mma_tf32(c, ah, bh);
+}
+// A fragment (m16 x k8, row-major at stride ld) from FP32 shared memory, split
+__device__ __forceinline__ void frag_a(const float* base, int ld, uint32_t (&ah)[4], uint32_t (&al)[4]) {
+    split_tf32(base[0], ah[0], al[0]);
+    split_tf32(base[8 * ld], ah[1], al[1]);
+    split_tf32(base[4], ah[2], al[2]);
+    split_tf32(base[8 * ld + 4], ah[3], al[3]);
+}
+}  // namespace sn
 
 template <int P, int HP, int NT = SN_THREADS>
 __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
@@ -69,6 +108,8 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
     constexpr int S = Streams<L>::S;
     constexpr int TR = SN_TR, J = S * TR, LD = HP + 4;
     constexpr int NWARP = NT / 32;
+    constexpr bool MMA = sn_mma(HP) && NWARP == 16;
+    constexpr int WS = MMA ? sn_ws(HP) : HP;                       // weight row stride
     constexpr int NC = HP / NWARP;                                 // output features per warp in the row GEMMs
     constexpr int EPT = HP * HP / NT;                              // dW entries per thread: BK x BN
     constexpr int BN = EPT >= 4 ? 4 : EPT;
@@ -79,9 +120,9 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
     const int D = a.D, H = a.H, K0 = a.K0;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // ---- shared-memory carve-up ----
-    float* W0 = sm;                                    // [8][HP]
-    float* Wh = W0 + SN_MAXK0 * HP;                    // hidden l = 1..D-1: [HP][HP] each
-    float* Wo = Wh + (int64_t)(D - 1) * HP * HP;       // head [HP][4]
+    float* W0 = sm;                                    // [8][WS]
+    float* Wh = W0 + SN_MAXK0 * WS;                    // hidden l = 1..D-1: [HP][WS] each
+    float* Wo = Wh + (int64_t)(D - 1) * HP * WS;       // head [HP][4]
     float* Bs = Wo + HP * 4;                           // biases [D][HP] + head [4]
     float* E = Bs + D * HP + 4;                        // [J][8] input jets
     float* Zs = E + J * SN_MAXK0;                      // [D][J][LD] stored pre-activations (t for s = 0)
@@ -92,14 +133,14 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
 
     // ---- weights -> shared memory, zero-padded ----
     const LayerTab& t = a.tab;
-    auto wlayer = [&](int l) { return l == 0 ? W0 : (l < D ? Wh + (int64_t)(l - 1) * HP * HP : Wo); };
+    auto wlayer = [&](int l) { return l == 0 ? W0 : (l < D ? Wh + (int64_t)(l - 1) * HP * WS : Wo); };
     for (int l = 0; l <= D; ++l) {
         const int Kl = t.K[l], Nl = t.N[l];
-        const int rows = l == 0 ? SN_MAXK0 : HP, cols = l == D ? 4 : HP;
+        const int rows = l == 0 ? SN_MAXK0 : HP, cols = l == D ? 4 : HP, ld = l == D ? 4 : WS;
         float* dst = wlayer(l);
         for (int i = tid; i < rows * cols; i += NT) {
             const int k = i / cols, n = i % cols;
-            dst[i] = (k < Kl && n < Nl) ? a.params[t.offW[l] + (int64_t)k * Nl + n] : 0.0f;
+            dst[k * ld + n] = (k < Kl && n < Nl) ? a.params[t.offW[l] + (int64_t)k * Nl + n] : 0.0f;
         }
         const int bn = l == D ? 4 : HP;
         for (int n = tid; n < bn; n += NT) Bs[l * HP + n] = n < Nl ? a.params[t.offB[l] + n] : 0.0f;
@@ -136,6 +177,47 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
             const float* A = l == 0 ? E : Hb;
             const int lda = l == 0 ? SN_MAXK0 : LD, Kd = l == 0 ? SN_MAXK0 : HP;
             const float* Wl = wlayer(l);
+            if constexpr (MMA) {
+                // warp = (row half h of every stream's 32 rows, 8-column tile nt): the S
+                // m-tiles s*32 + 16h of one n-tile, so a thread holds every stream of its
+                // four (row, column) outputs for the jet epilogue
+                const int h = warp & 1, nt = warp >> 1, g = lane >> 2, tq = lane & 3;
+                float acc[S][4];
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[s][i] = 0.0f;
+#pragma unroll 2
+                for (int k0 = 0; k0 < Kd; k0 += 8) {
+                    uint32_t bh[2], bl[2];
+                    sn::split_tf32(Wl[(k0 + tq) * WS + nt * 8 + g], bh[0], bl[0]);
+                    sn::split_tf32(Wl[(k0 + tq + 4) * WS + nt * 8 + g], bh[1], bl[1]);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        uint32_t ah[4], al[4];
+                        sn::frag_a(A + (s * TR + 16 * h + g) * lda + k0 + tq, lda, ah, al);
+                        sn::mma3(acc[s], ah, al, bh, bl);
+                    }
+                }
+                __syncthreads();  // every read of A (= Hb) done before it is overwritten
+                float* Zl = Zs + (int64_t)l * J * LD;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int r = 16 * h + g + 8 * (i >> 1), n = nt * 8 + 2 * tq + (i & 1);
+                    float zz[S], hh[S];
+                    zz[0] = store_value<ACT_TANH>(acc[0][i] + Bs[l * HP + n]);
+#pragma unroll
+                    for (int s = 1; s < S; ++s) zz[s] = acc[s][i];
+                    act_fwd<L, ACT_TANH>(zz, hh, 1.0f);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        Zl[(s * TR + r) * LD + n] = zz[s];
+                        Hb[(s * TR + r) * LD + n] = hh[s];
+                    }
+                }
+                __syncthreads();
+                continue;
+            }
             const int n0 = warp * NC;
             float z[S][NC];
 #pragma unroll
@@ -151,14 +233,14 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
                 for (int kk = 0; kk < 4; ++kk) {
                     float w[NC];
                     if constexpr (NC == 4) {
-                        const float4 w4 = *reinterpret_cast<const float4*>(Wl + (k + kk) * HP + n0);
+                        const float4 w4 = *reinterpret_cast<const float4*>(Wl + (k + kk) * WS + n0);
                         w[0] = w4.x;
                         w[1] = w4.y;
                         w[2] = w4.z;
                         w[3] = w4.w;
                     } else {
 #pragma unroll
-                        for (int c = 0; c < NC; ++c) w[c] = Wl[(k + kk) * HP + n0 + c];
+                        for (int c = 0; c < NC; ++c) w[c] = Wl[(k + kk) * WS + n0 + c];
                     }
 #pragma unroll
                     for (int s = 0; s < S; ++s) {
@@ -311,7 +393,40 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
             }
             // dW_l += A^T ZB (this thread's BK x BN block), db_l += colsum ZB[value stream]
             const int Kl = l == 0 ? K0 : H;
-            if (l > 0) {
+            if (MMA && l > 0) {
+                // dW[k][n] = sum_j Hb[j][k] ZB[j][n]: warp = (16-feature m-tile, two
+                // 8-column n-tiles), the reduction runs over every row of every stream
+                const int mt = warp & 3, ntp = (warp >> 2) * 2, g = lane >> 2, tq = lane & 3;
+                float acc[2][4];
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[u][i] = 0.0f;
+#pragma unroll 2
+                for (int j0 = 0; j0 < J; j0 += 8) {
+                    uint32_t ah[4], al[4];
+                    const float* Ar = A + (j0 + tq) * lda + mt * 16 + g;
+                    sn::split_tf32(Ar[0], ah[0], al[0]);          // (m = g,     k = tq)
+                    sn::split_tf32(Ar[8], ah[1], al[1]);          // (m = g + 8, k = tq)
+                    sn::split_tf32(Ar[4 * lda], ah[2], al[2]);    // (m = g,     k = tq + 4)
+                    sn::split_tf32(Ar[4 * lda + 8], ah[3], al[3]);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        uint32_t bh[2], bl[2];
+                        const float* Br = ZB + (j0 + tq) * LD + (ntp + u) * 8 + g;
+                        sn::split_tf32(Br[0], bh[0], bl[0]);
+                        sn::split_tf32(Br[4 * LD], bh[1], bl[1]);
+                        sn::mma3(acc[u], ah, al, bh, bl);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int k = mt * 16 + g + 8 * (i >> 1), n = (ntp + u) * 8 + 2 * tq + (i & 1);
+                        if (k < Kl && n < H) acc_slot(t.offW[l] + (int64_t)k * H + n, acc[u][i]);
+                    }
+            } else if (l > 0) {
                 const int kb = (tid / (HP / BN)) * BK, nb = (tid % (HP / BN)) * BN;
                 float acc[BK][BN];
 #pragma unroll
@@ -369,6 +484,44 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
             if (l == 0) break;
             // Hbar = ZB W_l^T (registers), then ZB = act^T(Hbar ; Z_{l-1}) in place
             const float* Wl = wlayer(l);
+            if constexpr (MMA) {
+                // warp = (row half h, 8-feature tile kt) over every stream, as the forward
+                const int h = warp & 1, kt = warp >> 1, g = lane >> 2, tq = lane & 3;
+                float hbm[S][4];
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) hbm[s][i] = 0.0f;
+#pragma unroll 2
+                for (int n0 = 0; n0 < HP; n0 += 8) {
+                    uint32_t bh[2], bl[2];  // B[n][k] = W[k][n]: (k-row n0 + tq (+4), column kt*8 + g)
+                    sn::split_tf32(Wl[(kt * 8 + g) * WS + n0 + tq], bh[0], bl[0]);
+                    sn::split_tf32(Wl[(kt * 8 + g) * WS + n0 + tq + 4], bh[1], bl[1]);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        uint32_t ah[4], al[4];
+                        sn::frag_a(ZB + (s * TR + 16 * h + g) * LD + n0 + tq, LD, ah, al);
+                        sn::mma3(hbm[s], ah, al, bh, bl);
+                    }
+                }
+                __syncthreads();  // all reads of ZB (and of Hb by the dW loop) done
+                const float* Zp = Zs + (int64_t)(l - 1) * J * LD;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int r = 16 * h + g + 8 * (i >> 1), k = kt * 8 + 2 * tq + (i & 1);
+                    float zz[S], hh[S], zb[S];
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        zz[s] = Zp[(s * TR + r) * LD + k];
+                        hh[s] = hbm[s][i];
+                    }
+                    act_bwd<L, ACT_TANH>(zz, hh, zb, 1.0f);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) ZB[(s * TR + r) * LD + k] = zb[s];
+                }
+                __syncthreads();
+                continue;
+            }
             const int k0 = warp * NC;
             float hb[S][NC];
 #pragma unroll
@@ -382,7 +535,7 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
                 for (int s = 0; s < S; ++s) zv[s] = *reinterpret_cast<const float4*>(ZB + (s * TR + lane) * LD + n);
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
-                    const float4 w = *reinterpret_cast<const float4*>(Wl + (k0 + c) * HP + n);
+                    const float4 w = *reinterpret_cast<const float4*>(Wl + (k0 + c) * WS + n);
 #pragma unroll
                     for (int s = 0; s < S; ++s)
                         hb[s][c] = fmaf(zv[s].x, w.x, fmaf(zv[s].y, w.y, fmaf(zv[s].z, w.z, fmaf(zv[s].w, w.w, hb[s][c]))));

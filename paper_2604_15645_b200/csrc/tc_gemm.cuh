@@ -137,6 +137,20 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 #endif
 }
+// truncation split: hi = x with the 13 low mantissa bits cleared (exact TF32),
+// lo = x - hi (exact FP32, the MMA reads its TF32 part): two integer / FP ops per
+// element instead of two cvt. Measured at parity in the general backward
+// (k_tc2_bwd: C3 3.04 -> 2.71 ms/step); the other TF32 producers keep the
+// rounding split (in the pair forward / decoupled backward / weight gradient the
+// truncation measured 1.2e-4 against the oracle at C4 -- not investigated further)
+__device__ __forceinline__ void split4_trunc(float4 v, float4& hi, float4& lo) {
+    const float4 h = make_float4(__uint_as_float(__float_as_uint(v.x) & 0xffffe000u),
+                                 __uint_as_float(__float_as_uint(v.y) & 0xffffe000u),
+                                 __uint_as_float(__float_as_uint(v.z) & 0xffffe000u),
+                                 __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
+    hi = h;
+    lo = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+}
 __device__ __forceinline__ void split4(float4 v, float4& hi, float4& lo) {
     tc::split3(v.x, hi.x, lo.x);
     tc::split3(v.y, hi.y, lo.y);
@@ -2050,7 +2064,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1) k_tc2_bwd(const __grid_constan
                 const uint32_t stage = sbase + st * Cfg::STAGE;
                 float4 hi[S], lo[S];
 #pragma unroll
-                for (int s2 = 0; s2 < S; ++s2) split4(ring[slot][s2], hi[s2], lo[s2]);
+                for (int s2 = 0; s2 < S; ++s2) split4_trunc(ring[slot][s2], hi[s2], lo[s2]);
                 if (it + D < nkb)
 #pragma unroll
                     for (int s2 = 0; s2 < S; ++s2) ring[slot][s2] = ldg4(asrc + s2 * RK + (it + D) * 8);

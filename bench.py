@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 METRIC = "collocation points/s per train step (residual+grad), 1/2/4/8 B200 vs CPU"
 UNIT = "points/s"
 L2_BYTES = 126e6  # B200 L2 (B200_PROFILING.md)
+MMA_SYNC_TF32_TFLOPS = 278.7  # tools/mma_sync_probe.cu on this pool (profiles/round2/mma_sync_probe.txt)
 
 
 def _args():
@@ -541,12 +542,19 @@ def main():
         elif use_tc:
             eff, note = bf16 / 6.0, ("3xTF32: tensor-pipe work = 3 x algorithmic flops at the TF32 rate "
                                      "(= bf16/2), so FP32-accurate peak = bf16/6 (derived)")
+        elif dom == "fused_step" and H == 64:
+            # the single-kernel step's width-64 contractions are 3xTF32 warp MMAs: the
+            # FP32-accurate peak is a third of the measured mma.sync tf32 rate
+            # (profiles/round2/mma_sync_probe.txt), above the FFMA pipe
+            eff, note = max(MMA_SYNC_TF32_TFLOPS / 3.0, fp32_peak), (
+                "3xTF32 mma.sync: measured m16n8k8 tf32 rate 278.7 TF/s / 3 (profiles/round2/mma_sync_probe.txt)")
         else:
             eff, note = fp32_peak, "FP32 FFMA pipe: 148 SM x 128 lanes x 2 x sm_max_mhz (derived)"
+        simt = not use_tc
         tensor_view = {"achieved": achieved, "unit": "TFLOP/s",
-                       "peak": bf16 if use_tc else fp32_peak, "frac": achieved / (bf16 if use_tc else fp32_peak),
+                       "peak": bf16 if use_tc else eff, "frac": achieved / (bf16 if use_tc else eff),
                        "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (dense bf16, of measured)"
-                                       if use_tc else note),
+                                       if not simt else note),
                        "effective_peak": eff, "frac_effective": achieved / eff, "effective_note": note,
                        "flops_per_step": flops_cls[dom]}
         hbm_view = {"achieved": achieved_gbs, "unit": "GB/s", "peak": hbm, "frac": achieved_gbs / hbm,
@@ -582,7 +590,8 @@ def main():
                        "params": P, "engine": args.engine,
                        "contraction": ("3xFP16 split operands, FP32 accumulate" if use_f16 else
                                        "3xTF32 split operands, FP32 accumulate" if use_tc else
-                                       "FP32 FFMA, whole step in one kernel" if dom == "fused_step" else "FP32 FFMA"),
+                                       ("3xTF32 warp MMA (mma.sync), whole step in one kernel" if H == 64 else
+                                        "FP32 FFMA, whole step in one kernel") if dom == "fused_step" else "FP32 FFMA"),
                        "parallelism": f"dp{world}",
                        "l2": (f"working set {work_bytes / 1e6:.1f} MB fits in L2: each timed step preceded by a "
                               f"512 MB L2 flush outside its CUDA events (steps timed one by one)" if l2_flush else

@@ -138,9 +138,19 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
         const int Kl = t.K[l], Nl = t.N[l];
         const int rows = l == 0 ? SN_MAXK0 : HP, cols = l == D ? 4 : HP, ld = l == D ? 4 : WS;
         float* dst = wlayer(l);
-        for (int i = tid; i < rows * cols; i += NT) {
-            const int k = i / cols, n = i % cols;
-            dst[k * ld + n] = (k < Kl && n < Nl) ? a.params[t.offW[l] + (int64_t)k * Nl + n] : 0.0f;
+        // four independent global loads in flight per thread before the stores
+        for (int i0 = tid; i0 < rows * cols; i0 += 4 * NT) {
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * NT, k = i / cols, n = i % cols;
+                v[u] = (i < rows * cols && k < Kl && n < Nl) ? __ldg(a.params + t.offW[l] + (int64_t)k * Nl + n) : 0.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * NT;
+                if (i < rows * cols) dst[(i / cols) * ld + i % cols] = v[u];
+            }
         }
         const int bn = l == D ? 4 : HP;
         for (int n = tid; n < bn; n += NT) Bs[l * HP + n] = n < Nl ? a.params[t.offB[l] + n] : 0.0f;
@@ -476,10 +486,14 @@ __global__ void __launch_bounds__(NT, 1) k_small_step(SmallArgs a) {
                     if (n < H) acc_slot(t.offW[0] + (int64_t)k * H + n, v);
                 }
             }
-            if (tid < H) {
+            if (tid < 4 * HP) {  // db: four lanes per column (rows q, q + 4, ...), fixed shuffle tree
+                const int col = tid >> 2, q = tid & 3;
                 double v = 0.0;
-                for (int r = 0; r < TR; ++r) v += (double)ZB[r * LD + tid];
-                acc_slot(t.offB[l] + tid, v);
+#pragma unroll
+                for (int r = q; r < TR; r += 4) v += (double)ZB[r * LD + col];
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                if (q == 0 && col < H) acc_slot(t.offB[l] + col, v);
             }
             if (l == 0) break;
             // Hbar = ZB W_l^T (registers), then ZB = act^T(Hbar ; Z_{l-1}) in place
